@@ -1,0 +1,124 @@
+"""Attention over the packed cache (attention.hpp:25-48, attention.cpp:28-223).
+
+attend() is the fused split-K decode kernel: dequantization happens inside the q.K dot
+products and the P.V accumulation, no full-precision K/V is materialized, and scratch is
+independent of the cached token count. Query heads may be a multiple G of the cache's KV
+heads (grouped-query attention; G = 1 is the reference's case).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+from ._lib import KvmixInvalidArgument, check, lib
+from .cache import KVLayerCache
+from .quant import _as_device, _dtype_code, _ptr, _stream
+
+
+@dataclasses.dataclass
+class AttentionOutput:
+    output: torch.Tensor  # [B, Hq, t, D] fp32
+    scores_checksum: float = 0.0
+
+
+def attention_inv_scale(head_dim: int) -> float:
+    return float(np.float32(1.0) / np.sqrt(np.float32(head_dim)))
+
+
+def _check_query(q: torch.Tensor, cache: KVLayerCache, allow_gqa: bool) -> None:
+    ok = (q.dim() == 4 and q.shape[0] == cache.batch() and q.shape[3] == cache.head_dim()
+          and (q.shape[1] == cache.heads() or (allow_gqa and q.shape[1] % cache.heads() == 0 and q.shape[1] > 0)))
+    if not ok:
+        raise KvmixInvalidArgument("attention: query shape does not match cache")
+    if q.shape[2] < 1:
+        raise KvmixInvalidArgument("attention: need at least one query row")
+
+
+def attend(query, cache: KVLayerCache, *, checksum: bool = True, out: torch.Tensor | None = None) -> AttentionOutput:
+    """attend (attention.cpp:161-166). checksum=True synchronizes to return the double sum
+    of all scaled scores like AttentionOutput::scores_checksum."""
+    q = _as_device(query)
+    _check_query(q, cache, allow_gqa=True)
+    B, Hq, t, D = (int(v) for v in q.shape)
+    if out is None:
+        out = torch.empty((B, Hq, t, D), dtype=torch.float32, device=q.device)
+    cs = C.c_double(0.0)
+    check(lib().kvmix_attend(cache.handle, _ptr(q), _dtype_code(q), Hq, t, _ptr(out), C.byref(cs) if checksum else None,
+                             _stream()))
+    return AttentionOutput(out, cs.value)
+
+
+def fused_qk_scores(query, cache: KVLayerCache) -> torch.Tensor:
+    """fused_qk_scores (attention.cpp:28-81): [B,H,t,total] fp32, already * 1/sqrt(D)."""
+    q = _as_device(query)
+    _check_query(q, cache, allow_gqa=False)
+    B, H, t, D = (int(v) for v in q.shape)
+    T = cache.total_tokens()
+    scores = torch.empty((B, H, t, T), dtype=torch.float32, device=q.device)
+    check(lib().kvmix_fused_qk_scores(cache.handle, _ptr(q), _dtype_code(q), t, _ptr(scores), _stream()))
+    return scores
+
+
+def softmax_rows(scores) -> torch.Tensor:
+    """softmax_rows (attention.cpp:96-105): returns a new tensor, rows sum to 1."""
+    s = _as_device(scores, torch.float32).clone()
+    cols = int(s.shape[-1]) if s.dim() else 0
+    if cols == 0:
+        raise KvmixInvalidArgument("softmax over an empty row")
+    check(lib().kvmix_softmax_rows(_ptr(s), s.numel() // cols, cols, _stream()))
+    return s
+
+
+def fused_pv(probs, cache: KVLayerCache) -> torch.Tensor:
+    """fused_pv (attention.cpp:107-159): probs [B,H,t,total] -> [B,H,t,D]."""
+    p = _as_device(probs, torch.float32)
+    if p.dim() != 4 or p.shape[3] != cache.total_tokens():
+        raise KvmixInvalidArgument("fused_pv: probability columns do not match cached tokens")
+    if p.shape[0] != cache.batch() or p.shape[1] != cache.heads():
+        raise KvmixInvalidArgument("fused_pv: probability shape does not match cache")
+    B, H, t, _ = (int(v) for v in p.shape)
+    out = torch.empty((B, H, t, cache.head_dim()), dtype=torch.float32, device=p.device)
+    check(lib().kvmix_fused_pv(cache.handle, _ptr(p), t, _ptr(out), _stream()))
+    return out
+
+
+def reference_attend(query, cache: KVLayerCache) -> AttentionOutput:
+    """reference_attend (attention.cpp:168-211): snapshot_dequantized into scratch, then dense
+    attention -- deliberately pays the O(total * D) materialization."""
+    q = _as_device(query)
+    _check_query(q, cache, allow_gqa=False)
+    B, H, t, D = (int(v) for v in q.shape)
+    T = cache.total_tokens()
+    scratch = torch.empty(2 * B * H * max(T, 1) * D, dtype=torch.float32, device=q.device)
+    out = torch.empty((B, H, t, D), dtype=torch.float32, device=q.device)
+    cs = C.c_double(0.0)
+    check(lib().kvmix_reference_attend(cache.handle, _ptr(q), _dtype_code(q), t, _ptr(scratch), _ptr(out),
+                                       C.byref(cs), _stream()))
+    return AttentionOutput(out, cs.value)
+
+
+def dump_scores_csv(os_, scores) -> None:
+    """dump_scores_csv (attention.cpp:213-221)."""
+    s = scores.cpu().numpy() if isinstance(scores, torch.Tensor) else np.asarray(scores)
+    os_.write("b,h,query,token,score\n")
+    B, H, t, T = s.shape
+    for b in range(B):
+        for h in range(H):
+            for qi in range(t):
+                for j in range(T):
+                    os_.write(f"{b},{h},{qi},{j},{float(s[b, h, qi, j]):g}\n")
+
+
+def attend_layers(caches, queries, outs, *, stream: int | None = None) -> None:
+    """One decode step's attention over a stack of layer caches in a single C call."""
+    n = len(caches)
+    hs = (C.c_void_p * n)(*[c.handle.value for c in caches])
+    qs = (C.c_void_p * n)(*[q.data_ptr() for q in queries])
+    os_ = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    q0 = queries[0]
+    check(lib().kvmix_attend_layers(hs, n, qs, _dtype_code(q0), int(q0.shape[1]), int(q0.shape[2]), os_,
+                                    stream if stream is not None else _stream()))

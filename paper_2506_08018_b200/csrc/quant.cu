@@ -1,0 +1,370 @@
+// quant.cu -- reference-layout quantize/pack, dequantize, pack/unpack kernels (sm_100a).
+//
+// Bit-exact with the reference's QuantizedGroups (quant.hpp:107-194, quant.cpp:36-124):
+// the output words are the reference's PackedBuffer words for the whole tensor, in the
+// reference stream order (Keys si = c*T + t, Values si = tok*D + d), including the Mixed3
+// 11-per-word layout whose words straddle channel/token boundaries.
+//
+// Work decomposition (HBM-bound byte work; no tensor cores):
+//  * Keys: one CTA per (b*H+h, span of n tokens, n a multiple of gs). The CTA stages the
+//    contiguous [n][D] input slab in shared memory (coalesced 128-bit loads), computes the
+//    per-(channel, group) metadata, and writes every output word whose FIRST code lies in
+//    one of its D runs [c*T+t0, c*T+t0+n). The few trailing codes of such a word that
+//    belong to the next run are encoded straight from global memory (their group meta is
+//    recomputed from gs elements), so no word is shared between CTAs: no atomics, no
+//    memset, one pass over the input.
+//  * Values: the stream is the input order itself; one CTA per span of R rows (token
+//    slots), thread-per-output-word, same ownership rule at the span end.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace kvb {
+
+namespace {
+
+constexpr int kQThreads = 256;
+
+template <typename T>
+__device__ inline float gload(const T* x, size_t i) {
+  return ld_f<T>(x + i);
+}
+
+// ---- Keys -------------------------------------------------------------------------------
+// x: [B,H,T,D]; words/meta in reference order. Tile: n tokens (multiple of gs), all D.
+template <typename T>
+__global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __restrict__ x, int H, int T_,
+                                                                 int D, int bits, int gs, int n,
+                                                                 uint32_t* __restrict__ words,
+                                                                 uint32_t* __restrict__ meta,
+                                                                 size_t n_total) {
+  extern __shared__ float smem[];
+  float* xs = smem;                                   // [n][D]
+  uint32_t* ms = reinterpret_cast<uint32_t*>(xs + (size_t)n * D);  // [D][n/gs]
+  const int bh = blockIdx.y;
+  const int t0 = blockIdx.x * n;
+  const int nt = min(n, T_ - t0);  // always a multiple of gs (T % gs == 0)
+  const int gpt = nt / gs;
+  const int gpc = T_ / gs;
+  const int q_max = q_max_for_bits(bits);
+  const T* src = x + ((size_t)bh * T_ + t0) * D;
+
+  for (int i = threadIdx.x; i < nt * D; i += blockDim.x) xs[i] = gload(src, i);
+  __syncthreads();
+
+  for (int i = threadIdx.x; i < D * gpt; i += blockDim.x) {
+    const int d = i % D, g = i / D;  // d fastest: conflict-free smem columns
+    float mn = xs[(g * gs) * D + d], mx = mn;
+    for (int j = 1; j < gs; ++j) {
+      const float v = xs[(g * gs + j) * D + d];
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+    const uint32_t m = make_meta(mn, mx, q_max);
+    ms[d * gpt + g] = m;
+    const size_t c = (size_t)bh * D + d;
+    meta[c * gpc + t0 / gs + g] = m;
+  }
+  __syncthreads();
+
+  const int cpw = codes_per_word(bits);
+  // one thread per channel run; a run's owned words are contiguous in `words`
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const size_t c = (size_t)bh * D + d;
+    const size_t s0 = c * (size_t)T_ + t0;
+    const size_t s1 = s0 + nt;
+    const size_t w_begin = (s0 + cpw - 1) / cpw, w_end = (s1 + cpw - 1) / cpw;
+    // cache for out-of-run codes (next run): its channel/group meta
+    size_t cached_group = ~(size_t)0;
+    float o_scale = 0.f, o_min = 0.f;
+    for (size_t w = w_begin; w < w_end; ++w) {
+      uint32_t word = 0;
+      const size_t p0 = w * cpw;
+      for (int k = 0; k < cpw; ++k) {
+        const size_t p = p0 + k;
+        if (p >= n_total) break;
+        float xv, sc, mnv;
+        if (p < s1) {
+          const int tt = (int)(p - s0);
+          xv = xs[tt * D + d];
+          const uint32_t m = ms[d * gpt + tt / gs];
+          sc = meta_scale(m);
+          mnv = meta_min(m);
+        } else {
+          const size_t c2 = p / T_;
+          const int t2 = (int)(p % T_);
+          const size_t bh2 = c2 / D;
+          const int d2 = (int)(c2 % D);
+          const size_t grp = c2 * gpc + t2 / gs;
+          const T* base = x + (bh2 * T_ + (size_t)(t2 / gs) * gs) * D + d2;
+          if (grp != cached_group) {
+            float mn = gload(base, 0), mx = mn;
+            for (int j = 1; j < gs; ++j) {
+              const float v = gload(base, (size_t)j * D);
+              mn = v < mn ? v : mn;
+              mx = v > mx ? v : mx;
+            }
+            const uint32_t m = make_meta(mn, mx, q_max);
+            o_scale = meta_scale(m);
+            o_min = meta_min(m);
+            cached_group = grp;
+          }
+          xv = gload(x, (bh2 * T_ + t2) * D + d2);
+          sc = o_scale;
+          mnv = o_min;
+        }
+        const uint32_t code = encode(xv, sc, mnv, bits, is_narrow(bits, p));
+        word |= code << field_shift(bits, (uint32_t)k);
+      }
+      words[w] = word;
+    }
+  }
+}
+
+// ---- Values -----------------------------------------------------------------------------
+// x: [rows][D] with rows = B*H*T token slots; groups along channels (partial last group).
+template <typename T>
+__global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __restrict__ x, size_t rows,
+                                                                   int D, int bits, int gs, int R,
+                                                                   uint32_t* __restrict__ words,
+                                                                   uint32_t* __restrict__ meta) {
+  extern __shared__ float smem[];
+  const int gpt = (D + gs - 1) / gs;
+  const int Dp = D + 1;                                                // padded row stride
+  float* xs = smem;                                                    // [R][Dp]
+  uint32_t* ms = reinterpret_cast<uint32_t*>(xs + (size_t)R * Dp);     // [R][gpt]
+  const size_t r0 = (size_t)blockIdx.x * R;
+  const int nr = (int)min((size_t)R, rows - r0);
+  const int q_max = q_max_for_bits(bits);
+  const T* src = x + r0 * D;
+  for (int i = threadIdx.x; i < nr * D; i += blockDim.x) xs[(i / D) * Dp + i % D] = gload(src, i);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nr * gpt; i += blockDim.x) {
+    const int rr = i / gpt, g = i % gpt;
+    const int d0 = g * gs, d1 = min(d0 + gs, D);
+    float mn = xs[rr * Dp + d0], mx = mn;
+    for (int d = d0 + 1; d < d1; ++d) {
+      const float v = xs[rr * Dp + d];
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+    const uint32_t m = make_meta(mn, mx, q_max);
+    ms[i] = m;
+    meta[(r0 + rr) * gpt + g] = m;
+  }
+  __syncthreads();
+  const int cpw = codes_per_word(bits);
+  const size_t n_total = rows * (size_t)D;
+  const size_t s0 = r0 * D, s1 = s0 + (size_t)nr * D;
+  const size_t w_begin = (s0 + cpw - 1) / cpw, w_end = (s1 + cpw - 1) / cpw;
+  for (size_t w = w_begin + threadIdx.x; w < w_end; w += blockDim.x) {
+    uint32_t word = 0;
+    const size_t p0 = w * cpw;
+    for (int k = 0; k < cpw; ++k) {
+      const size_t p = p0 + k;
+      if (p >= n_total) break;
+      float xv, sc, mnv;
+      if (p < s1) {
+        const int rr = (int)((p - s0) / D), d = (int)((p - s0) % D);
+        xv = xs[rr * Dp + d];
+        const uint32_t m = ms[rr * gpt + d / gs];
+        sc = meta_scale(m);
+        mnv = meta_min(m);
+      } else {
+        const size_t row = p / D;
+        const int d = (int)(p % D);
+        const int d0 = (d / gs) * gs, d1 = min(d0 + gs, D);
+        float mn = gload(x, row * D + d0), mx = mn;
+        for (int e = d0 + 1; e < d1; ++e) {
+          const float v = gload(x, row * D + e);
+          mn = v < mn ? v : mn;
+          mx = v > mx ? v : mx;
+        }
+        const uint32_t m = make_meta(mn, mx, q_max);
+        sc = meta_scale(m);
+        mnv = meta_min(m);
+        xv = gload(x, p);
+      }
+      word |= encode(xv, sc, mnv, bits, is_narrow(bits, p)) << field_shift(bits, (uint32_t)k);
+    }
+    words[w] = word;
+  }
+}
+
+// ---- dequantize (QuantizedGroups::value_at for every element) ----------------------------
+__global__ void dequantize_kernel(int grouping, const uint32_t* __restrict__ words,
+                                  const uint32_t* __restrict__ meta, int H, int T_, int D, int bits,
+                                  int gs, size_t n, float* __restrict__ out) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int d = (int)(e % D);
+    const size_t rowi = e / D;  // (bh, t)
+    const int t = (int)(rowi % T_);
+    const size_t bh = rowi / T_;
+    size_t si, mi;
+    if (grouping == 0) {
+      const size_t c = bh * D + d;
+      si = c * T_ + t;
+      mi = c * (size_t)(T_ / gs) + t / gs;
+    } else {
+      si = rowi * D + d;
+      mi = rowi * (size_t)((D + gs - 1) / gs) + d / gs;
+    }
+    const int cpw = codes_per_word(bits);
+    const uint32_t pos = (uint32_t)(si % cpw);
+    const uint32_t code = (words[si / cpw] >> field_shift(bits, pos)) & field_mask(bits, pos);
+    const uint32_t m = meta[mi];
+    out[e] = decode(code, meta_scale(m), meta_min(m), is_narrow(bits, si));
+  }
+}
+
+// ---- pack / unpack (PackedWriter::push, PackedBuffer::get) -------------------------------
+__global__ void pack_kernel(const uint32_t* __restrict__ codes, size_t n, int bits,
+                            uint32_t* __restrict__ words, unsigned long long* bad) {
+  const int cpw = codes_per_word(bits);
+  const size_t nw = words_for(n, bits);
+  for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < nw; w += (size_t)gridDim.x * blockDim.x) {
+    uint32_t word = 0;
+    for (int k = 0; k < cpw; ++k) {
+      const size_t i = w * cpw + k;
+      if (i >= n) break;
+      const uint32_t c = codes[i];
+      if (c > field_mask(bits, (uint32_t)k)) {
+        atomicMin(bad, (unsigned long long)i);
+        continue;
+      }
+      word |= c << field_shift(bits, (uint32_t)k);
+    }
+    words[w] = word;
+  }
+}
+
+__global__ void unpack_kernel(const uint32_t* __restrict__ words, size_t n, int bits,
+                              uint32_t* __restrict__ codes) {
+  const int cpw = codes_per_word(bits);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t pos = (uint32_t)(i % cpw);
+    codes[i] = (words[i / cpw] >> field_shift(bits, pos)) & field_mask(bits, pos);
+  }
+}
+
+int grid_for(size_t n, int threads) {
+  const size_t b = (n + threads - 1) / threads;
+  const size_t cap = (size_t)num_sms() * 16;
+  return (int)std::max<size_t>(1, std::min(b, cap));
+}
+
+}  // namespace
+
+void check_quant_args(int B, int H, int T, int D, int bits, int gs) {
+  if (bits < 1 || bits > 4) invalid("unsupported bit width " + std::to_string(bits));
+  if (gs <= 0) invalid("group_size must be positive");
+  if (B < 0 || H < 0 || T < 0 || D < 0) invalid("tensor dimensions must be non-negative");
+}
+
+void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int H, int T, int D, int bits,
+              int gs, uint32_t* words, uint16_t* meta, cudaStream_t st) {
+  check_quant_args(B, H, T, D, bits, gs);
+  if (grouping == KVMIX_PER_CHANNEL_KEY) {
+    if (T % gs != 0) {
+      invalid("key quantization needs T (" + std::to_string(T) + ") to be a multiple of group_size (" +
+              std::to_string(gs) + ")");
+    }
+  } else if (grouping != KVMIX_PER_TOKEN_VALUE) {
+    invalid("unknown grouping");
+  }
+  const size_t n = (size_t)B * H * T * D;
+  if (n == 0) return;
+  if (dt != KVMIX_F32 && dt != KVMIX_F16) invalid("unsupported dtype");
+  auto* m32 = reinterpret_cast<uint32_t*>(meta);
+  const int max_smem = 96 * 1024;
+  if (grouping == KVMIX_PER_CHANNEL_KEY) {
+    // tile of k groups of gs tokens: aim for ~128 tokens, bounded by shared memory
+    int k = std::max(1, 128 / gs);
+    auto smem_of = [&](int kk) { return (size_t)kk * gs * D * 4 + (size_t)D * kk * 4; };
+    while (k > 1 && smem_of(k) > (size_t)max_smem) --k;
+    if (smem_of(k) > (size_t)227 * 1024) invalid("quantize: group_size * head_dim too large for one tile");
+    const int n_tok = k * gs;
+    const size_t smem = smem_of(k);
+    dim3 grid((T + n_tok - 1) / n_tok, B * H);
+    if (dt == KVMIX_F32) {
+      auto kern = quantize_key_kernel<float>;
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kQThreads, smem, st>>>(static_cast<const float*>(x), H, T, D, bits, gs, n_tok, words, m32, n);
+    } else {
+      auto kern = quantize_key_kernel<__half>;
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kQThreads, smem, st>>>(static_cast<const __half*>(x), H, T, D, bits, gs, n_tok, words, m32, n);
+    }
+    after_launch("quantize_key_kernel");
+  } else {
+    const int gpt = (D + gs - 1) / gs;
+    int R = std::max(1, 8192 / std::max(D, 1));
+    auto smem_of = [&](int r) { return (size_t)r * (D + 1) * 4 + (size_t)r * gpt * 4; };
+    while (R > 1 && smem_of(R) > (size_t)max_smem) --R;
+    if (smem_of(R) > (size_t)227 * 1024) invalid("quantize: head_dim too large for one tile");
+    const size_t rows = (size_t)B * H * T;
+    const size_t smem = smem_of(R);
+    const unsigned grid = (unsigned)((rows + R - 1) / R);
+    if (dt == KVMIX_F32) {
+      auto kern = quantize_value_kernel<float>;
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kQThreads, smem, st>>>(static_cast<const float*>(x), rows, D, bits, gs, R, words, m32);
+    } else {
+      auto kern = quantize_value_kernel<__half>;
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kQThreads, smem, st>>>(static_cast<const __half*>(x), rows, D, bits, gs, R, words, m32);
+    }
+    after_launch("quantize_value_kernel");
+  }
+}
+
+void dequantize(kvmix_grouping grouping, const uint32_t* words, const uint16_t* meta, int B, int H, int T,
+                int D, int bits, int gs, float* out, cudaStream_t st) {
+  check_quant_args(B, H, T, D, bits, gs);
+  if (grouping == KVMIX_PER_CHANNEL_KEY && T % gs != 0) invalid("key tensor needs T % group_size == 0");
+  const size_t n = (size_t)B * H * T * D;
+  if (n == 0) return;
+  dequantize_kernel<<<grid_for(n, 256), 256, 0, st>>>((int)grouping, words,
+                                                       reinterpret_cast<const uint32_t*>(meta), H, T, D,
+                                                       bits, gs, n, out);
+  after_launch("dequantize_kernel");
+}
+
+void pack(const uint32_t* codes, size_t n, int bits, uint32_t* words, cudaStream_t st) {
+  if (bits != 1 && bits != 2 && bits != 3 && bits != 4) {
+    invalid("feat_per_word: bits must be 1, 2 or 4, got " + std::to_string(bits));
+  }
+  if (n == 0) return;
+  unsigned long long* bad = nullptr;
+  check_cuda(cudaMallocAsync(&bad, sizeof(unsigned long long), st), "cudaMallocAsync");
+  check_cuda(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st), "memset");
+  const size_t nw = words_for(n, bits);
+  pack_kernel<<<grid_for(nw, 256), 256, 0, st>>>(codes, n, bits, words, bad);
+  after_launch("pack_kernel");
+  unsigned long long first = 0;
+  check_cuda(cudaMemcpyAsync(&first, bad, sizeof(first), cudaMemcpyDeviceToHost, st), "memcpy");
+  check_cuda(cudaFreeAsync(bad, st), "cudaFreeAsync");
+  check_cuda(cudaStreamSynchronize(st), "sync");
+  if (first != ~0ull) {
+    // same wording as PackedWriter::push (bitpack.cpp:26-41)
+    uint32_t c = 0;
+    check_cuda(cudaMemcpy(&c, codes + first, 4, cudaMemcpyDeviceToHost), "memcpy");
+    if (bits == 3) {
+      const size_t pos = first % 11;
+      invalid("pack_mixed3: code " + std::to_string(c) + " in block " + std::to_string(first / 11) +
+              " at intra-block index " + std::to_string(pos) + " exceeds " + std::to_string(pos == 10 ? 3 : 7));
+    }
+    invalid("pack_uniform: code " + std::to_string(c) + " at index " + std::to_string(first) + " exceeds " +
+            std::to_string((1u << bits) - 1u) + " for " + std::to_string(bits) + "-bit fields");
+  }
+}
+
+void unpack(const uint32_t* words, size_t n, int bits, uint32_t* codes, cudaStream_t st) {
+  if (bits != 1 && bits != 2 && bits != 3 && bits != 4) invalid("unsupported bit width");
+  if (n == 0) return;
+  unpack_kernel<<<grid_for(n, 256), 256, 0, st>>>(words, n, bits, codes);
+  after_launch("unpack_kernel");
+}
+
+}  // namespace kvb

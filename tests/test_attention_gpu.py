@@ -1,0 +1,205 @@
+"""GPU parity: decode attention over the packed cache vs the CPU oracle.
+
+Tolerance (stated): elementwise relative error is meaningless for
+near-zero outputs at long contexts, so errors are scaled by max|V|:
+  * primary, vs an fp64 evaluation over the reference's bit-exact snapshot:
+        max |out - out64| <= ATTN_TOL_F64 * max|V|
+  * secondary, vs the reference's own fp32 attend order (oracle attend_f32):
+        max |out - out32| <= ATTN_TOL_F32 * max|V|
+  * scores_checksum within CHECKSUM_RTOL relative (plus a small absolute floor).
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2506_08018_b200 as K
+
+pytestmark = pytest.mark.gpu
+
+ATTN_TOL_F64 = 2e-5
+ATTN_TOL_F32 = 4e-5
+CHECKSUM_RTOL = 1e-5
+
+
+def build(kb, vb, rk, rv, gs, B, H, D, chunks, seed=0, tail_dtype=torch.float32, cap=None):
+    cap = cap or sum(chunks) + 16
+    dev = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, rk, rv, gs), B, H, D, capacity_tokens=cap, tail_dtype=tail_dtype)
+    ora = O.CacheOracle(kb, vb, rk, rv, gs, B, H, D)
+    for i, t in enumerate(chunks):
+        k = O.random_h16(seed + 2 * i, (B, H, t, D))
+        v = O.random_h16(seed + 2 * i + 1, (B, H, t, D))
+        dev.append(k, v)
+        ora.append(k, v)
+    return dev, ora
+
+
+def check_attend(dev, ora, q, G=1):
+    ks, vs = ora.snapshot()
+    if G > 1:  # GQA: KV head h serves query heads h*G .. h*G+G-1 (= reference t=G rows)
+        B, Hq, t, D = q.shape
+        qr = q.reshape(B, Hq // G, G * t, D)
+        o64, cs64 = O.attend_f64(qr, ks, vs)
+        o32, cs32 = O.attend_f32(qr, ks, vs)
+        o64, o32 = o64.reshape(q.shape), o32.reshape(q.shape)
+    else:
+        o64, cs64 = O.attend_f64(q, ks, vs)
+        o32, cs32 = O.attend_f32(q, ks, vs)
+    res = K.attend(torch.from_numpy(q).cuda(), dev)
+    out = res.output.cpu().numpy()
+    vmax = float(np.abs(vs).max())
+    e64 = float(np.abs(out - o64).max()) / vmax
+    e32 = float(np.abs(out - o32).max()) / vmax
+    assert e64 <= ATTN_TOL_F64, e64
+    assert e32 <= ATTN_TOL_F32, e32
+    assert abs(res.scores_checksum - cs64) <= CHECKSUM_RTOL * abs(cs64) + 1e-3, (res.scores_checksum, cs64)
+    return e64
+
+
+@pytest.mark.parametrize("kb,vb", [(2, 2), (3, 4), (4, 4), (3, 3), (2, 4), (4, 2)])
+def test_attend_fill_states(cuda, kb, vb):
+    rng = np.random.default_rng(kb * 7 + vb)
+    for trial in range(4):
+        r = float(rng.uniform(0.0, 0.5))
+        chunks = [int(x) for x in rng.integers(1, 96, size=int(rng.integers(1, 8)))]
+        dev, ora = build(kb, vb, r, r, 32, 1, 2, 64, chunks, seed=trial * 100)
+        q = O.random_h16(999 + trial, (1, 2, 1 + trial % 3, 64))
+        check_attend(dev, ora, q)
+
+
+@pytest.mark.parametrize("sigma", [1.0, 3.0])
+def test_attend_long_context_config1(cuda, sigma):
+    """Config 1: B1, H32, D128, K2/V2 gs32 r=0.1, 4096 tokens (prefill + decode steps)."""
+    dev, ora = build(2, 2, 0.1, 0.1, 32, 1, 32, 128, [4032] + [1] * 64, seed=7, cap=4200)
+    q = O.random_h16(5, (1, 32, 1, 128), sigma=sigma)
+    check_attend(dev, ora, q)
+
+
+def test_attend_right_after_prefill(cuda):
+    dev, ora = build(2, 2, 0.1, 0.1, 32, 1, 8, 128, [4096], seed=3, cap=4200)
+    assert dev.key_tail_tokens() == 416 and dev.value_tail_tokens() == 409
+    check_attend(dev, ora, O.random_h16(6, (1, 8, 1, 128)))
+
+
+def test_attend_mixed_tier_fp16(cuda):
+    dev, ora = build(3, 4, 0.2, 0.2, 32, 2, 4, 128, [2000] + [1] * 40, seed=11, tail_dtype=torch.float16)
+    q = O.random_h16(8, (2, 4, 1, 128))
+    check_attend(dev, ora, q)
+    # fp16 queries give the same result as their fp32 copy
+    a = K.attend(torch.from_numpy(q).cuda(), dev).output
+    b = K.attend(torch.from_numpy(q).cuda().half(), dev).output
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_attend_gqa(cuda, G):
+    dev, ora = build(2, 2, 0.1, 0.1, 32, 2, 4, 128, [1500] + [1] * 33, seed=21)
+    q = O.random_h16(12, (2, 4 * G, 1, 128), sigma=2.0)
+    check_attend(dev, ora, q, G=G)
+
+
+@pytest.mark.parametrize("gs", [64, 128])
+def test_attend_group_sizes(cuda, gs):
+    dev, ora = build(2, 4, 0.1, 0.1, gs, 1, 4, 128, [1200, 1, 1, 300] + [1] * 20, seed=31)
+    check_attend(dev, ora, O.random_h16(13, (1, 4, 2, 128)))
+
+
+def test_full_precision_cache_exact_dot(cuda):
+    """test_attention.cpp:73-87: r=1 cache -> scores are plain scaled dot products."""
+    dev, ora = build(2, 2, 1.0, 1.0, 32, 1, 2, 64, [50], seed=1)
+    q = O.random_h16(2, (1, 2, 1, 64))
+    s = K.fused_qk_scores(q, dev).cpu().numpy()
+    ks, _ = ora.snapshot()
+    ref = np.einsum("bhtd,bhjd->bhtj", q.astype(np.float64), ks.astype(np.float64)) / np.sqrt(64.0)
+    assert np.abs(s - ref).max() < 1e-5
+
+
+def test_zero_query_uniform(cuda):
+    dev, ora = build(4, 4, 0.2, 0.2, 32, 1, 1, 64, [200], seed=2)
+    q = np.zeros((1, 1, 1, 64), np.float32)
+    s = K.fused_qk_scores(q, dev)
+    assert torch.count_nonzero(s) == 0
+    p = K.softmax_rows(s).cpu().numpy()
+    assert np.allclose(p, 1.0 / 200, rtol=1e-6)
+
+
+def test_separate_kernels_compose_to_attend(cuda):
+    dev, ora = build(3, 4, 0.2, 0.2, 32, 1, 2, 64, [150, 7, 1], seed=8)
+    q = O.random_h16(3, (1, 2, 3, 64))
+    p = K.softmax_rows(K.fused_qk_scores(q, dev))
+    assert torch.allclose(p.sum(-1), torch.ones(1, 2, 3, device="cuda"), atol=1e-6)
+    out = K.fused_pv(p, dev).cpu().numpy()
+    ks, vs = ora.snapshot()
+    o64, _ = O.attend_f64(q, ks, vs)
+    assert np.abs(out - o64).max() / np.abs(vs).max() < ATTN_TOL_F64
+
+
+def test_one_hot_tail_token_exact(cuda):
+    """test_attention.cpp:131-143."""
+    dev, ora = build(2, 2, 0.25, 0.25, 32, 1, 1, 64, [60, 40], seed=4)
+    total = dev.total_tokens()
+    j = total - dev.value_tail_tokens() + 1
+    probs = torch.zeros(1, 1, 1, total, device="cuda")
+    probs[0, 0, 0, j] = 1.0
+    out = K.fused_pv(probs, dev)
+    _, vs = dev.snapshot_dequantized()
+    assert torch.equal(out[0, 0, 0], vs[0, 0, j])
+
+
+def test_reference_attend_matches_oracle(cuda):
+    dev, ora = build(2, 3, 0.3, 0.2, 32, 1, 2, 64, [333, 1, 1], seed=5)
+    q = O.random_h16(4, (1, 2, 2, 64))
+    ref = K.reference_attend(q, dev)
+    ks, vs = ora.snapshot()
+    o64, cs = O.attend_f64(q, ks, vs)
+    assert np.abs(ref.output.cpu().numpy() - o64).max() / np.abs(vs).max() < ATTN_TOL_F64
+    assert abs(ref.scores_checksum - cs) <= CHECKSUM_RTOL * abs(cs) + 1e-3
+
+
+def test_bits_monotone_error(cuda):
+    """test_attention.cpp:251-275 / acceptance criterion 9, fewer trials."""
+    err = {}
+    for bits in (2, 3, 4):
+        tot = 0.0
+        for trial in range(6):
+            qd, _ = build(bits, bits, 0.1, 0.1, 32, 1, 2, 64, [160, 1, 1], seed=1000 + trial)
+            fp, _ = build(bits, bits, 1.0, 1.0, 32, 1, 2, 64, [160, 1, 1], seed=1000 + trial)
+            q = O.random_h16(trial, (1, 2, 1, 64))
+            tot += float((K.attend(q, qd).output - K.attend(q, fp).output).abs().mean())
+        err[bits] = tot
+    assert err[2] >= err[3] >= err[4] > 0
+
+
+def test_concurrent_readers_identical(cuda):
+    dev, _ = build(2, 2, 0.2, 0.2, 32, 1, 2, 64, [300], seed=9)
+    q = torch.from_numpy(O.random_h16(1, (1, 2, 1, 64))).cuda()
+    serial = K.attend(q, dev).output.clone()
+    outs = [None, None]
+
+    def run(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            outs[i] = K.attend(q, dev).output
+        s.synchronize()
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert torch.equal(outs[0], serial) and torch.equal(outs[1], serial)
+
+
+def test_errors(cuda):
+    dev, _ = build(2, 2, 0.2, 0.2, 32, 1, 2, 64, [40], seed=10)
+    with pytest.raises(K.KvmixInvalidArgument):
+        K.fused_qk_scores(np.zeros((1, 2, 1, 32), np.float32), dev)
+    with pytest.raises(K.KvmixInvalidArgument):
+        K.fused_pv(torch.zeros(1, 2, 1, 39), dev)
+    empty = K.KVLayerCache(K.LayerQuantConfig(0, 2, 2, 0.2, 0.2, 32), 1, 1, 64, capacity_tokens=8)
+    with pytest.raises(K.KvmixInvalidArgument):
+        K.attend(np.zeros((1, 1, 1, 64), np.float32), empty)
+    with pytest.raises(K.KvmixInvalidArgument):
+        K.attend(np.zeros((1, 3, 1, 64), np.float32), dev)
