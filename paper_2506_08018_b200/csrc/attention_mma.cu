@@ -1,11 +1,12 @@
-// attention_mma.cu -- fused split-K decode attention on the tensor cores (mma.sync m16n8k16).
+// attention_mma.cu -- fused split-K decode attention on the tensor cores (mma.sync m16n8k16),
+// fed by TMA bulk copies (cp.async.bulk + mbarrier) into a per-warp shared-memory ring.
 //
 // Decode is a GEMV per (b, kv-head): scores = K q, out = V^T p. At 2-bit gs32 a K+V element
 // pair is 0.75 B of HBM traffic, so a CUDA-core loop (unpack + dequant + FMA per element)
 // runs out of issue slots before HBM does. Here the codes go straight
-// from registers into tensor-core A fragments: the device tile layout (common.cuh) is
-// "fragment-native", so one 128-bit load per lane yields that lane's A operands and each
-// fragment register is unpacked with shift/LOP3/HSUB2 into exact fp16 integers. The
+// from shared memory into tensor-core A fragments: the device tile layout (common.cuh) is
+// "fragment-native", so one 128-bit shared load per lane yields that lane's A operands and
+// each fragment register is unpacked with shift/LOP3/HSUB2 into exact fp16 integers. The
 // dequantization is factored out of the dot products:
 //     q.k_j  = sum_d (q_d s_gd) c_jd + sum_d q_d m_gd          (Keys, per channel group)
 //     out_d  = sum_j (p_j s_jg) c_jd + sum_j p_j m_jg          (Values, per token group)
@@ -13,11 +14,20 @@
 // two MMA columns, so products carry ~22 mantissa bits and accumulate in fp32. The Value
 // min term is a second small MMA with A = the binary16 mins (exact in fp16).
 //
-// CTA = 4 warps over one (b, kv-head) and a chunk of Key groups; warps own whole groups
-// (interleaved). Per 16-token tile a warp: K MMA (D/16 k-steps) -> scores -> online
-// softmax (log2 domain) -> builds the P.V B fragments in shared memory -> V MMA (D/16
-// m-tiles). Tokens past the last fully packed group (the ragged tail and the
-// full-precision window) use a per-token CUDA-core loop updating the same state. Partials
+// Mixed3 (3-bit) Keys: the reference's narrow slots (stream index % 11 == 10) dequantize
+// with scale*7/3. For channel d of a group the narrow tokens are t = tau_d (mod 11), so the
+// correction sum_d [t == tau_d mod 11] c_td q_d (s'_d - s_d) is 11 extra B columns (one per
+// residue class, hi/lo) in the same MMAs; each token picks the column of its residue.
+//
+// Memory pipeline: every unit of work (one Key group of gs tokens of one (b, kv-head))
+// is four contiguous byte ranges in HBM -- Key tiles, Value tiles, Value meta, Key meta --
+// copied by one elected lane with cp.async.bulk into a ring of S stages; the warp waits on
+// the stage's mbarrier (complete_tx), computes, and refills the stage S groups ahead. Each
+// warp keeps S-1 groups in flight, enough to cover HBM latency at 3-4 CTAs/SM.
+//
+// CTA = 4 warps over one (b, kv-head) and a chunk of groups (warps interleave groups).
+// Tokens past the last fully packed group (the ragged tail and the full-precision window)
+// use a per-token CUDA-core loop updating the same online-softmax state. Partials
 // (m, l, acc) go to the split-K combine kernel shared with the generic path.
 #include <algorithm>
 #include <cmath>
@@ -32,6 +42,45 @@ constexpr int kMmaWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA bulk copy global -> shared, completion counted on `bar`, evict-first in L2 (the
+// packed cache is streamed once per step).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -39,6 +88,12 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
       "{%0,%1,%2,%3};\n"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, const void* row_addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];\n"
+               : "=r"(b0), "=r"(b1)
+               : "r"(smem_u32(row_addr)));
 }
 
 __device__ __forceinline__ uint32_t h2_sub_magic(uint32_t x) {
@@ -49,39 +104,53 @@ __device__ __forceinline__ uint32_t h2_sub_magic(uint32_t x) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Unpack fragment register r at slot s from a lane's words of a b-bit plane.
+// Fragment register r at slot s from a lane's words. B in {2,4}: one plane. B == 3: 2-bit
+// plane (w[0..NS/2)) + 1-bit plane (w[NS/2..)).
 template <int B, int NS>
 __device__ __forceinline__ uint32_t frag(const uint32_t* w, int r, int s) {
-  constexpr int SPH = 16 / B;
-  constexpr uint32_t MASK = B == 2 ? 0x00030003u : B == 4 ? 0x000F000Fu : 0x00010001u;
   const int vs = r * NS + s;
-  const uint32_t x = ((w[vs / SPH] >> (B * (vs % SPH))) & MASK) | 0x64006400u;
-  return h2_sub_magic(x);
-}
-
-template <int WPL>
-__device__ __forceinline__ void load_plane(const uint32_t* __restrict__ tile, int lane, uint32_t (&w)[WPL]) {
-  if constexpr (WPL >= 4) {
-#pragma unroll
-    for (int c = 0; c < WPL / 4; ++c) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(tile + c * 128 + lane * 4));
-      w[4 * c] = v.x;
-      w[4 * c + 1] = v.y;
-      w[4 * c + 2] = v.z;
-      w[4 * c + 3] = v.w;
-    }
-  } else if constexpr (WPL == 2) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2*>(tile + lane * 2));
-    w[0] = v.x;
-    w[1] = v.y;
+  if constexpr (B == 3) {
+    const uint32_t lo = (w[vs >> 3] >> (2 * (vs & 7))) & 0x00030003u;
+    const uint32_t hi = (w[NS / 2 + (vs >> 4)] >> (vs & 15)) & 0x00010001u;
+    return h2_sub_magic(lo | (hi << 2) | 0x64006400u);
   } else {
-    w[0] = __ldg(tile + lane);
+    constexpr int SPH = 16 / B;
+    constexpr uint32_t MASK = B == 2 ? 0x00030003u : 0x000F000Fu;
+    const uint32_t x = ((w[vs / SPH] >> (B * (vs % SPH))) & MASK) | 0x64006400u;
+    return h2_sub_magic(x);
   }
 }
 
-__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
-  __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
+// Lane's words of one tile in shared memory (layout: plane_addr in common.cuh).
+template <int B, int D>
+__device__ __forceinline__ void lds_tile(const uint32_t* tile, int lane, uint32_t* w) {
+  if constexpr (B == 3) {
+    lds_tile<2, D>(tile, lane, w);
+    lds_tile<1, D>(tile + 32 * (D / 32), lane, w + D / 32);
+  } else {
+    constexpr int WPL = D * B / 64;
+    if constexpr (WPL >= 4) {
+#pragma unroll
+      for (int c = 0; c < WPL / 4; ++c) {
+        const uint4 v = *reinterpret_cast<const uint4*>(tile + c * 128 + lane * 4);
+        w[4 * c] = v.x;
+        w[4 * c + 1] = v.y;
+        w[4 * c + 2] = v.z;
+        w[4 * c + 3] = v.w;
+      }
+    } else if constexpr (WPL == 2) {
+      const uint2 v = *reinterpret_cast<const uint2*>(tile + lane * 2);
+      w[0] = v.x;
+      w[1] = v.y;
+    } else {
+      w[0] = tile[lane];
+    }
+  }
+}
+
+template <int D, int B>
+constexpr int lane_words() {
+  return B == 3 ? D * 3 / 64 : D * B / 64;
 }
 
 struct MmaParams {
@@ -91,30 +160,43 @@ struct MmaParams {
   int64_t T, P;          // total tokens; fast-path limit (multiple of gs)
   int64_t groups_total;  // ceil(T / gs)
   int chunk_groups;
-  float inv;             // 1/sqrt(D)
+  int stages;
+  uint32_t kt_bytes, vt_bytes, vm_bytes, km_bytes;  // per-group copy sizes
+  uint32_t stage_bytes;
+  float inv;  // 1/sqrt(D)
   float2* part_ml;
   float* part_acc;
   double* part_cs;
 };
 
-// Per-warp shared memory (halves unless noted).
-template <int D>
-struct WarpSmem {
-  static constexpr int KST = D + 8;  // padded row stride: conflict-free B fragment reads
-  static constexpr int VST = 24;     // padded token stride (16 tokens)
-  __half bk[8][KST];                 // K B operand: [column][channel]
-  __half bv[8][8][VST];              // V B operand: [channel group][column][token]
-  __half bp[8][VST];                 // P (bias MMA) B operand: [column][token]
-  uint32_t vm[16][8];                // staged Value meta of the tile: [token][channel group]
+// Per-warp shared layout (bytes), dynamic:
+//   ring[S][stage_bytes] | bk[D][NB*8] half | bv[8][8][24] half | bp[8][24] half |
+//   sd[16][NB*8] float (3-bit Keys only) | bars[S] u64
+template <int D, int NB>
+struct WarpLayout {
+  static constexpr int kBk = D * NB * 8 * 2;
+  static constexpr int kBv = 8 * 8 * 24 * 2;
+  static constexpr int kBp = 8 * 24 * 2;
+  static constexpr int kSd = NB > 1 ? 16 * NB * 8 * 4 : 0;
+  __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
+    const size_t n = (size_t)stages * stage_bytes + kBk + kBv + kBp + kSd + (size_t)stages * 8;
+    return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
+  }
 };
 
 template <int D, int KB, int VB, int R, typename TT, typename TQ>
 __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams p) {
-  constexpr int NS = D / 16;        // k-steps (Keys) / m-tiles (Values)
-  constexpr int KW = D * KB / 64;   // words per lane, Key tile
-  constexpr int VW = D * VB / 64;   // words per lane, Value tile
-  constexpr int LC = D / 32;        // channels per lane for meta / q
-  __shared__ WarpSmem<D> wsm[kMmaWarps];
+  constexpr int NS = D / 16;                   // k-steps (Keys) / m-tiles (Values)
+  constexpr int KW = lane_words<D, KB>();      // words per lane, Key tile
+  constexpr int VW = lane_words<D, VB>();      // words per lane, Value tile
+  constexpr int LC = D / 32;                   // channels per lane for meta / q
+  constexpr bool K3 = KB == 3;
+  constexpr int NCOL = 2 * R + (K3 ? 22 * R : 0);
+  constexpr int NB = (NCOL + 7) / 8;           // 8-column MMA blocks for the Key GEMV
+  using WL = WarpLayout<D, NB>;
+  static_assert(!K3 || R <= 2, "3-bit Keys support up to 2 query rows per KV head");
+
+  extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float s_m[kMmaWarps][R], s_l[kMmaWarps][R];
   __shared__ float s_acc[kMmaWarps][R][D];
   __shared__ float s_bias[kMmaWarps][R][8];
@@ -124,14 +206,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
-  const int gs = p.gs, CG = p.cg;
-  WarpSmem<D>& sm = wsm[warp];
+  const int gs = p.gs, CG = p.cg, S = p.stages;
+  const int TPG = gs / 16;  // tiles per group
 
-  // zero this warp's B operand staging (unused columns must stay 0)
+  uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
+  uint8_t* ring = wbase;
+  __half* bk = reinterpret_cast<__half*>(ring + (size_t)S * p.stage_bytes);            // [D][NB*8]
+  __half(*bv)[8][24] = reinterpret_cast<__half(*)[8][24]>(reinterpret_cast<uint8_t*>(bk) + WL::kBk);
+  __half(*bp)[24] = reinterpret_cast<__half(*)[24]>(reinterpret_cast<uint8_t*>(bv) + WL::kBv);
+  float* sd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bp) + WL::kBp);      // [16][NB*8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sd) + WL::kSd);
+
+  // zero B staging (unused columns must stay 0)
   {
-    uint32_t* z = reinterpret_cast<uint32_t*>(&sm);
-    for (int i = lane; i < (int)(sizeof(WarpSmem<D>) / 4); i += 32) z[i] = 0u;
+    uint32_t* z = reinterpret_cast<uint32_t*>(bk);
+    const int n = (WL::kBk + WL::kBv + WL::kBp) / 4;
+    for (int i = lane; i < n; i += 32) z[i] = 0u;
   }
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+
   // query rows: lane owns channels [lane*LC, lane*LC+LC)
   float qv[R][LC];
 #pragma unroll
@@ -142,7 +239,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
 #pragma unroll
     for (int c = 0; c < LC; ++c) qv[r][c] = r < p.rows ? ld_f<TQ>(qp + c) : 0.f;
   }
-  __syncwarp();
 
   float m_run = -INFINITY, l_run = 0.f;  // row t (threads with t < rows)
   float accv[NS][4];
@@ -155,10 +251,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   const int64_t g_beg = (int64_t)split * p.chunk_groups;
   const int64_t g_end = min(g_beg + p.chunk_groups, p.groups_total);
   const int64_t g_fast_end = min(g_end, p.P / gs);
-  const size_t ktile_base = (size_t)bh * p.k.tiles_per_bh * p.k.tile_words;
-  const size_t vtile_base = (size_t)bh * p.v.tiles_per_bh * p.v.tile_words;
-  const uint32_t* kmeta_bh = p.k.meta + (size_t)bh * p.k.meta_per_bh;
-  const uint32_t* vmeta_bh = p.v.meta + (size_t)bh * p.v.meta_per_bh;
+  const uint8_t* ktiles = reinterpret_cast<const uint8_t*>(p.k.tiles + (size_t)bh * p.k.tiles_per_bh * p.k.tile_words);
+  const uint8_t* vtiles = reinterpret_cast<const uint8_t*>(p.v.tiles + (size_t)bh * p.v.tiles_per_bh * p.v.tile_words);
+  const uint8_t* kmeta = reinterpret_cast<const uint8_t*>(p.k.meta + (size_t)bh * p.k.meta_per_bh);
+  const uint8_t* vmeta = reinterpret_cast<const uint8_t*>(p.v.meta + (size_t)bh * p.v.meta_per_bh);
+  const uint64_t policy = evict_first_policy();
+
+  auto issue = [&](int64_t grp, int s) {
+    uint8_t* st = ring + (size_t)s * p.stage_bytes;
+    mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
+    bulk_g2s(st, ktiles + (size_t)grp * p.kt_bytes, p.kt_bytes, &bars[s], policy);
+    bulk_g2s(st + p.kt_bytes, vtiles + (size_t)grp * p.vt_bytes, p.vt_bytes, &bars[s], policy);
+    bulk_g2s(st + p.kt_bytes + p.vt_bytes, vmeta + (size_t)grp * p.vm_bytes, p.vm_bytes, &bars[s], policy);
+    bulk_g2s(st + p.kt_bytes + p.vt_bytes + p.vm_bytes, kmeta + (size_t)grp * p.km_bytes, p.km_bytes, &bars[s], policy);
+  };
 
   auto rescale = [&](float alpha) {
     if (__any_sync(0xffffffffu, alpha != 1.0f)) {
@@ -176,25 +282,51 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     }
   };
 
-  for (int64_t grp = g_beg + warp; grp < g_fast_end; grp += kMmaWarps) {
+  // prologue: fill the ring
+  const int64_t first = g_beg + warp;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      const int64_t grp = first + (int64_t)s * kMmaWarps;
+      if (grp < g_fast_end) issue(grp, s);
+    }
+  }
+
+  int it = 0;
+  for (int64_t grp = first; grp < g_fast_end; grp += kMmaWarps, ++it) {
+    const int s = it % S;
+    mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
+    const uint8_t* st = ring + (size_t)s * p.stage_bytes;
+    const uint32_t* kt = reinterpret_cast<const uint32_t*>(st);
+    const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + p.kt_bytes);
+    const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes);
+    const uint32_t* km = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes + p.vm_bytes);
+
     // ---- Key group: B operand (q*s split hi/lo, pre-scaled by 2^e per row) and beta ----
     float beta[R], inv_sig[R];
     {
-      uint32_t km[LC];
-      const uint32_t* mp = kmeta_bh + (size_t)grp * D + lane * LC;
-      if constexpr (LC == 4) {
-        const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(mp));
-        km[0] = v4.x; km[1] = v4.y; km[2] = v4.z; km[3] = v4.w;
-      } else {
-#pragma unroll
-        for (int c = 0; c < LC; ++c) km[c] = __ldg(mp + c);
-      }
       float sc[LC], mn[LC];
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
-        sc[c] = meta_scale(km[c]);
-        mn[c] = meta_min(km[c]);
+        const uint32_t m = km[lane * LC + c];
+        sc[c] = meta_scale(m);
+        mn[c] = meta_min(m);
       }
+      int tau[LC];
+      if constexpr (K3) {
+        const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
+        const int nmod = inf.x % 11, omod = inf.y % 11;
+#pragma unroll
+        for (int c = 0; c < LC; ++c) {
+          const int cmod = (int)(((size_t)bh * D + lane * LC + c) % 11);
+          const int phi = (cmod * nmod + omod) % 11;  // stream index % 11 of the group's first token
+          tau[c] = (21 - phi) % 11;                   // narrow tokens: t = tau (mod 11)
+        }
+      }
+      __half rowbuf[LC][NB * 8];
+#pragma unroll
+      for (int c = 0; c < LC; ++c)
+#pragma unroll
+        for (int j = 0; j < NB * 8; ++j) rowbuf[c][j] = __ushort_as_half(0);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         float qs[LC], mx = 0.f, bt = 0.f;
@@ -203,6 +335,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
           qs[c] = qv[r][c] * sc[c];
           mx = fmaxf(mx, fabsf(qs[c]));
           bt = fmaf(qv[r][c], mn[c], bt);
+          if constexpr (K3) mx = fmaxf(mx, fabsf(qv[r][c] * (wide_scale(sc[c]) - sc[c])));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -219,19 +352,31 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
         for (int c = 0; c < LC; ++c) {
           const float x = qs[c] * sig;
           const __half hi = __float2half_rn(x);
-          const __half lo = __float2half_rn(x - __half2float(hi));
-          sm.bk[2 * r][lane * LC + c] = hi;
-          sm.bk[2 * r + 1][lane * LC + c] = lo;
+          rowbuf[c][2 * r] = hi;
+          rowbuf[c][2 * r + 1] = __float2half_rn(x - __half2float(hi));
+          if constexpr (K3) {
+            const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sig;
+            const __half yh = __float2half_rn(y);
+#pragma unroll
+            for (int xr = 0; xr < 11; ++xr) {
+              if (tau[c] == xr) {
+                rowbuf[c][2 * R + (r * 11 + xr) * 2] = yh;
+                rowbuf[c][2 * R + (r * 11 + xr) * 2 + 1] = __float2half_rn(y - __half2float(yh));
+              }
+            }
+          }
         }
+      }
+      __syncwarp();  // previous group's ldmatrix reads of bk are done
+#pragma unroll
+      for (int c = 0; c < LC; ++c) {
+        uint4* dst = reinterpret_cast<uint4*>(bk + (size_t)(lane * LC + c) * NB * 8);
+        const uint4* srcv = reinterpret_cast<const uint4*>(rowbuf[c]);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) dst[j] = srcv[j];
       }
     }
     __syncwarp();
-    uint32_t bk0[NS], bk1[NS];
-#pragma unroll
-    for (int kk = 0; kk < NS; ++kk) {
-      bk0[kk] = *reinterpret_cast<const uint32_t*>(&sm.bk[g][16 * kk + 2 * t]);
-      bk1[kk] = *reinterpret_cast<const uint32_t*>(&sm.bk[g][16 * kk + 2 * t + 8]);
-    }
     float my_beta = beta[0], my_isig = inv_sig[0];
 #pragma unroll
     for (int r = 1; r < R; ++r) {
@@ -241,24 +386,50 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       }
     }
 
-    for (int tt = 0; tt < gs / 16; ++tt) {
-      const int64_t tile = grp * (gs / 16) + tt;
+    for (int tt = 0; tt < TPG; ++tt) {
       uint32_t kw[KW], vw[VW];
-      load_plane<KW>(p.k.tiles + ktile_base + (size_t)tile * p.k.tile_words, lane, kw);
-      load_plane<VW>(p.v.tiles + vtile_base + (size_t)tile * p.v.tile_words, lane, vw);
-      // stage the tile's Value meta [16 tokens][CG]
-      for (int i = lane; i < 16 * CG; i += 32) sm.vm[i / CG][i % CG] = __ldg(vmeta_bh + (size_t)tile * 16 * CG + i);
+      lds_tile<KB, D>(kt + (size_t)tt * tile_words(D, KB), lane, kw);
+      lds_tile<VB, D>(vt + (size_t)tt * tile_words(D, VB), lane, vw);
 
       // ---- scores: K (16 tokens x D) . B ----
-      float dk[4] = {0.f, 0.f, 0.f, 0.f};
+      float dk[NB][4];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dk[nb][0] = dk[nb][1] = dk[nb][2] = dk[nb][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < NS; ++kk) {
-        mma16816(dk, frag<KB, NS>(kw, 0, kk), frag<KB, NS>(kw, 1, kk), frag<KB, NS>(kw, 2, kk),
-                 frag<KB, NS>(kw, 3, kk), bk0[kk], bk1[kk]);
+        const uint32_t a0 = frag<KB, NS>(kw, 0, kk), a1 = frag<KB, NS>(kw, 1, kk);
+        const uint32_t a2 = frag<KB, NS>(kw, 2, kk), a3 = frag<KB, NS>(kw, 3, kk);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          uint32_t b0, b1;
+          ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB * 8 + nb * 8);
+          mma16816(dk[nb], a0, a1, a2, a3, b0, b1);
+        }
       }
-      // row t: token g -> dk[0] + dk[1]; token g+8 -> dk[2] + dk[3]
-      const float sa = ((dk[0] + dk[1]) * my_isig + my_beta) * p.inv;
-      const float sb = ((dk[2] + dk[3]) * my_isig + my_beta) * p.inv;
+      float va, vb_;  // row t: token g / token g+8 (K-sum * sigma)
+      if constexpr (K3) {
+        // residue-class corrections: dump the fragments, pick each token's residue column
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          sd[g * NB * 8 + nb * 8 + 2 * t] = dk[nb][0];
+          sd[g * NB * 8 + nb * 8 + 2 * t + 1] = dk[nb][1];
+          sd[(g + 8) * NB * 8 + nb * 8 + 2 * t] = dk[nb][2];
+          sd[(g + 8) * NB * 8 + nb * 8 + 2 * t + 1] = dk[nb][3];
+        }
+        __syncwarp();
+        const int rr = t < R ? t : 0;
+        const int xa = (tt * 16 + g) % 11, xb = (tt * 16 + g + 8) % 11;
+        const float* ra = sd + g * NB * 8;
+        const float* rb = sd + (g + 8) * NB * 8;
+        va = ra[2 * rr] + ra[2 * rr + 1] + ra[2 * R + (rr * 11 + xa) * 2] + ra[2 * R + (rr * 11 + xa) * 2 + 1];
+        vb_ = rb[2 * rr] + rb[2 * rr + 1] + rb[2 * R + (rr * 11 + xb) * 2] + rb[2 * R + (rr * 11 + xb) * 2 + 1];
+        __syncwarp();
+      } else {
+        va = dk[0][0] + dk[0][1];
+        vb_ = dk[0][2] + dk[0][3];
+      }
+      const float sa = (va * my_isig + my_beta) * p.inv;
+      const float sb = (vb_ * my_isig + my_beta) * p.inv;
       if (row_ok) cs += (double)(sa + sb);
       const float la = sa * kLog2e, lb = sb * kLog2e;
       float tmax = fmaxf(la, lb);
@@ -274,7 +445,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       rescale(alpha);
 
       // ---- P.V B operands: lane -> token j = lane % 16 ----
-      __syncwarp();
+      const uint32_t* vmt = vm + (size_t)tt * 16 * CG;  // [16][CG]
       {
         const int j = lane & 15, hh = lane >> 4;
 #pragma unroll
@@ -286,14 +457,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
           if (r < p.rows) {
             if (hh == 0) {
               const __half hi = __float2half_rn(pj);
-              sm.bp[2 * r][j] = hi;
-              sm.bp[2 * r + 1][j] = __float2half_rn(pj - __half2float(hi));
+              bp[2 * r][j] = hi;
+              bp[2 * r + 1][j] = __float2half_rn(pj - __half2float(hi));
             }
             for (int c = hh; c < CG; c += 2) {
-              const float x = pj * meta_scale(sm.vm[j][c]);
+              const float x = pj * meta_scale(vmt[j * CG + c]);
               const __half hi = __float2half_rn(x);
-              sm.bv[c][2 * r][j] = hi;
-              sm.bv[c][2 * r + 1][j] = __float2half_rn(x - __half2float(hi));
+              bv[c][2 * r][j] = hi;
+              bv[c][2 * r + 1][j] = __float2half_rn(x - __half2float(hi));
             }
           }
         }
@@ -303,22 +474,27 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       {
         uint32_t a0 = 0u, a2 = 0u;
         if (g < CG) {
-          a0 = __byte_perm(sm.vm[2 * t][g], sm.vm[2 * t + 1][g], 0x7632);
-          a2 = __byte_perm(sm.vm[2 * t + 8][g], sm.vm[2 * t + 9][g], 0x7632);
+          a0 = __byte_perm(vmt[(2 * t) * CG + g], vmt[(2 * t + 1) * CG + g], 0x7632);
+          a2 = __byte_perm(vmt[(2 * t + 8) * CG + g], vmt[(2 * t + 9) * CG + g], 0x7632);
         }
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.bp[g][2 * t]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.bp[g][2 * t + 8]);
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bp[g][2 * t]);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bp[g][2 * t + 8]);
         mma16816(accb, a0, 0u, a2, 0u, b0, b1);
       }
 #pragma unroll
       for (int mt = 0; mt < NS; ++mt) {
         const int c = (mt * 16) / gs;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.bv[c][g][2 * t]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.bv[c][g][2 * t + 8]);
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
         mma16816(accv[mt], frag<VB, NS>(vw, 0, mt), frag<VB, NS>(vw, 1, mt), frag<VB, NS>(vw, 2, mt),
                  frag<VB, NS>(vw, 3, mt), b0, b1);
       }
       __syncwarp();
+    }
+    // refill this stage S groups ahead
+    if (lane == 0) {
+      const int64_t nxt = grp + (int64_t)S * kMmaWarps;
+      if (nxt < g_fast_end) issue(nxt, s);
     }
   }
 
@@ -380,9 +556,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       s_acc[warp][t][mt * 16 + g] = accv[mt][0] + accv[mt][1];
       s_acc[warp][t][mt * 16 + g + 8] = accv[mt][2] + accv[mt][3];
     }
-    if (g < 8) s_bias[warp][t][g] = accb[0] + accb[1];
+    s_bias[warp][t][g] = accb[0] + accb[1];
   }
-  // checksum: reduce the warp's doubles
   for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
   if (lane == 0) s_cs[warp] = cs;
   __syncthreads();
@@ -417,28 +592,41 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
 
 template <int D, int KB, int VB, int R, typename TT, typename TQ>
 void launch(const MmaParams& p, int nsplit, int BH, cudaStream_t st) {
-  attend_mma_kernel<D, KB, VB, R, TT, TQ><<<dim3(nsplit, BH), kMmaWarps * 32, 0, st>>>(p);
+  constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
+  constexpr int NB = (NCOL + 7) / 8;
+  const size_t smem = (size_t)kMmaWarps * WarpLayout<D, NB>::bytes(p.stages, p.stage_bytes);
+  auto kern = attend_mma_kernel<D, KB, VB, R, TT, TQ>;
+  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  kern<<<dim3(nsplit, BH), kMmaWarps * 32, smem, st>>>(p);
 }
 
 template <int D, int KB, int VB, int R>
 bool dispatch_types(const MmaParams& p, int nsplit, int BH, bool tail16, bool q16, cudaStream_t st) {
-  if (tail16) {
-    if (q16) launch<D, KB, VB, R, __half, __half>(p, nsplit, BH, st);
-    else launch<D, KB, VB, R, __half, float>(p, nsplit, BH, st);
+  if constexpr (KB == 3 && R > 2) {
+    return false;
   } else {
-    if (q16) launch<D, KB, VB, R, float, __half>(p, nsplit, BH, st);
-    else launch<D, KB, VB, R, float, float>(p, nsplit, BH, st);
+    if (tail16) {
+      if (q16) launch<D, KB, VB, R, __half, __half>(p, nsplit, BH, st);
+      else launch<D, KB, VB, R, __half, float>(p, nsplit, BH, st);
+    } else {
+      if (q16) launch<D, KB, VB, R, float, __half>(p, nsplit, BH, st);
+      else launch<D, KB, VB, R, float, float>(p, nsplit, BH, st);
+    }
+    return true;
   }
-  return true;
 }
 
 template <int D, int R>
 bool dispatch_bits(const MmaParams& p, int kb, int vb, int nsplit, int BH, bool tail16, bool q16, cudaStream_t st) {
-  if (kb == 2 && vb == 2) return dispatch_types<D, 2, 2, R>(p, nsplit, BH, tail16, q16, st);
-  if (kb == 2 && vb == 4) return dispatch_types<D, 2, 4, R>(p, nsplit, BH, tail16, q16, st);
-  if (kb == 4 && vb == 2) return dispatch_types<D, 4, 2, R>(p, nsplit, BH, tail16, q16, st);
-  if (kb == 4 && vb == 4) return dispatch_types<D, 4, 4, R>(p, nsplit, BH, tail16, q16, st);
-  return false;
+  switch (kb * 10 + vb) {
+    case 22: return dispatch_types<D, 2, 2, R>(p, nsplit, BH, tail16, q16, st);
+    case 24: return dispatch_types<D, 2, 4, R>(p, nsplit, BH, tail16, q16, st);
+    case 42: return dispatch_types<D, 4, 2, R>(p, nsplit, BH, tail16, q16, st);
+    case 44: return dispatch_types<D, 4, 4, R>(p, nsplit, BH, tail16, q16, st);
+    case 32: return dispatch_types<D, 3, 2, R>(p, nsplit, BH, tail16, q16, st);
+    case 34: return dispatch_types<D, 3, 4, R>(p, nsplit, BH, tail16, q16, st);
+    default: return false;
+  }
 }
 
 }  // namespace
@@ -456,8 +644,9 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   const int rows = (Hq / c->H) * tq;
   if (rows > 4) return false;
   const int kb = c->k.bits, vb = c->v.bits;
-  if (kb == 3 || vb == 3) return false;
+  if (vb == 3 || (kb == 3 && rows > 2)) return false;
   const int D = c->D, gs = c->cfg.group_size;
+  if (D != 64 && D != 128) return false;
   const int BH = c->B * c->H;
   const int64_t T = c->total();
   MmaParams p{};
@@ -476,6 +665,14 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.groups_total = (T + gs - 1) / gs;
   const int nsplit = mma_splits(BH, p.groups_total);
   p.chunk_groups = (int)((p.groups_total + nsplit - 1) / nsplit);
+  p.kt_bytes = (uint32_t)((gs / 16) * c->k.tile_words * 4);
+  p.vt_bytes = (uint32_t)((gs / 16) * c->v.tile_words * 4);
+  p.vm_bytes = (uint32_t)(gs * p.cg * 4);
+  p.km_bytes = (uint32_t)(D * 4);
+  p.stage_bytes = p.kt_bytes + p.vt_bytes + p.vm_bytes + p.km_bytes;
+  if (p.vm_bytes % 16) return false;
+  // ring depth: ~12 KB in flight per warp, 2..4 stages
+  p.stages = (int)std::max<uint32_t>(2, std::min<uint32_t>(4, 12288 / p.stage_bytes));
   p.inv = 1.0f / sqrtf((float)D);
   const int cap_splits = mma_splits(BH, (int64_t)1 << 40);
   p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
@@ -484,11 +681,11 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   const bool tail16 = c->tail_dtype == KVMIX_F16, q16 = dt == KVMIX_F16;
   const int R = rows <= 1 ? 1 : rows <= 2 ? 2 : 4;
   bool ok = false;
-#define KVB_DISPATCH_D(DD)                                                                     \
-  if (D == DD) {                                                                               \
-    if (R == 1) ok = dispatch_bits<DD, 1>(p, kb, vb, nsplit, BH, tail16, q16, st);             \
-    else if (R == 2) ok = dispatch_bits<DD, 2>(p, kb, vb, nsplit, BH, tail16, q16, st);        \
-    else ok = dispatch_bits<DD, 4>(p, kb, vb, nsplit, BH, tail16, q16, st);                    \
+#define KVB_DISPATCH_D(DD)                                                              \
+  if (D == DD) {                                                                        \
+    if (R == 1) ok = dispatch_bits<DD, 1>(p, kb, vb, nsplit, BH, tail16, q16, st);      \
+    else if (R == 2) ok = dispatch_bits<DD, 2>(p, kb, vb, nsplit, BH, tail16, q16, st); \
+    else ok = dispatch_bits<DD, 4>(p, kb, vb, nsplit, BH, tail16, q16, st);             \
   }
   KVB_DISPATCH_D(64)
   KVB_DISPATCH_D(128)
