@@ -291,10 +291,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     }
   }
 
-  int it = 0;
-  for (int64_t grp = first; grp < g_fast_end; grp += kMmaWarps, ++it) {
-    const int s = it % S;
-    mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
+  // channel group of each Value m-tile (gs is a multiple of 16)
+  int cg_of[NS];
+#pragma unroll
+  for (int mt = 0; mt < NS; ++mt) cg_of[mt] = (mt * 16) / gs;
+
+  int s = 0;
+  uint32_t phase = 0;
+  for (int64_t grp = first; grp < g_fast_end; grp += kMmaWarps) {
+    mbar_wait(&bars[s], phase);
     const uint8_t* st = ring + (size_t)s * p.stage_bytes;
     const uint32_t* kt = reinterpret_cast<const uint32_t*>(st);
     const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + p.kt_bytes);
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       }
 #pragma unroll
       for (int mt = 0; mt < NS; ++mt) {
-        const int c = (mt * 16) / gs;
+        const int c = cg_of[mt];
         const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
         const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
         mma16816(accv[mt], frag<VB, NS>(vw, 0, mt), frag<VB, NS>(vw, 1, mt), frag<VB, NS>(vw, 2, mt),
@@ -495,6 +500,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     if (lane == 0) {
       const int64_t nxt = grp + (int64_t)S * kMmaWarps;
       if (nxt < g_fast_end) issue(nxt, s);
+    }
+    if (++s == S) {
+      s = 0;
+      phase ^= 1u;
     }
   }
 

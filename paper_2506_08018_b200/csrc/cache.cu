@@ -213,8 +213,24 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
         a.v_info[tile * 16 + i] = make_int2((int)a.v_n, (int)(tile * 16 + i - a.v_q0));
     }
     __syncthreads();
+    // only the aged rows' fields: one atomicOr per code into the (zero-initialised) tile
     uint32_t* tp = a.v_tiles + (size_t)bh * a.v_tiles_per_bh * a.v_tile_words + (size_t)tile * a.v_tile_words;
-    emit_tile(false, D, a.vbits, codes, tp, true, i_lo, i_hi);
+    for (int e = threadIdx.x; e < (i_hi - i_lo) * D; e += blockDim.x) {
+      const int i = i_lo + e / D, d = e % D;
+      const uint32_t code = codes[i * D + d];
+      if (code == 0) continue;
+      const TileCoord tc = value_coord(i, d);
+      int w, sh;
+      if (a.vbits == 3) {
+        plane_field(tc, D, 2, &w, &sh);
+        if (code & 3u) atomicOr(tp + w, (code & 3u) << sh);
+        plane_field(tc, D, 1, &w, &sh);
+        if (code >> 2) atomicOr(tp + 32 * plane_wpl(D, 2) + w, (code >> 2) << sh);
+      } else {
+        plane_field(tc, D, a.vbits, &w, &sh);
+        atomicOr(tp + w, code << sh);
+      }
+    }
     return;
   }
   blk -= n_v_blocks;

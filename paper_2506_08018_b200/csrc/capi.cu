@@ -171,10 +171,11 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
       s.tail_cap = std::min<int64_t>(capacity_tokens, bound) + 64;
       alloc((void**)&s.tiles, BH * s.tiles_per_bh * s.tile_words * 4);
       if (sp.key) {
-        s.meta_per_bh = (size_t)((capacity_tokens + gs - 1) / gs) * head_dim;
+        s.meta_per_bh = (size_t)((ntiles * 16 + gs - 1) / gs) * head_dim;
         alloc((void**)&s.info, sizeof(int2) * (size_t)((capacity_tokens + gs - 1) / gs));
       } else {
-        s.meta_per_bh = (size_t)capacity_tokens * ((head_dim + gs - 1) / gs);
+        // whole tiles of tokens: keeps every (b,h) row 16-byte aligned for bulk copies
+        s.meta_per_bh = (size_t)ntiles * 16 * ((head_dim + gs - 1) / gs);
         alloc((void**)&s.info, sizeof(int2) * (size_t)capacity_tokens);
       }
       alloc((void**)&s.meta, BH * s.meta_per_bh * 4);
