@@ -5,14 +5,20 @@
 // pair is 0.75 B of HBM traffic, so a CUDA-core loop (unpack + dequant + FMA per element)
 // runs out of issue slots before HBM does. Here the codes go straight
 // from shared memory into tensor-core A fragments: the device tile layout (common.cuh) is
-// "fragment-native", so one 128-bit shared load per lane yields that lane's A operands and
-// each fragment register is unpacked with shift/LOP3/HSUB2 into exact fp16 integers. The
-// dequantization is factored out of the dot products:
+// "fragment-native", so one 128-bit shared load per lane yields that lane's A operands.
+// The dequantization is factored out of the dot products:
 //     q.k_j  = sum_d (q_d s_gd) c_jd + sum_d q_d m_gd          (Keys, per channel group)
 //     out_d  = sum_j (p_j s_jg) c_jd + sum_j p_j m_jg          (Values, per token group)
 // The B operands (q*s, p*s, p) are split into an fp16 hi part and an fp16 lo remainder in
 // two MMA columns, so products carry ~22 mantissa bits and accumulate in fp32. The Value
 // min term is a second small MMA with A = the binary16 mins (exact in fp16).
+//
+// Unpack ("scale classes"): a fragment register holds two codes at the same bit offset of
+// the two 16-bit halves. OR-ing the masked word into 0x6400 (fp16 1024) and subtracting
+// 1024 gives the codes exactly, scaled by 2^offset -- so codes at offsets 0..9 need no
+// shift at all. The slot -> offset map only depends on the k-step (Keys) / m-tile
+// (Values), so the power of two is folded into the Key B operand per channel and into the
+// Value accumulator of each m-tile at the end: one LOP3 + one HADD2 per register.
 //
 // Mixed3 (3-bit) Keys: the reference's narrow slots (stream index % 11 == 10) dequantize
 // with scale*7/3. For channel d of a group the narrow tokens are t = tau_d (mod 11), so the
@@ -22,13 +28,13 @@
 // Memory pipeline: every unit of work (one Key group of gs tokens of one (b, kv-head))
 // is four contiguous byte ranges in HBM -- Key tiles, Value tiles, Value meta, Key meta --
 // copied by one elected lane with cp.async.bulk into a ring of S stages; the warp waits on
-// the stage's mbarrier (complete_tx), computes, and refills the stage S groups ahead. Each
-// warp keeps S-1 groups in flight, enough to cover HBM latency at 3-4 CTAs/SM.
+// the stage's mbarrier (complete_tx), computes, and refills the stage S groups ahead.
 //
 // CTA = 4 warps over one (b, kv-head) and a chunk of groups (warps interleave groups).
-// Tokens past the last fully packed group (the ragged tail and the full-precision window)
-// use a per-token CUDA-core loop updating the same online-softmax state. Partials
-// (m, l, acc) go to the split-K combine kernel shared with the generic path.
+// Tokens past the last group whose Keys and Values are both packed (the full-precision
+// window, a partially aged Value tile) are processed lane-parallel over channels (each
+// lane owns D/32 channels) with the same online-softmax state. Partials (m, l, acc) go to
+// the split-K combine kernel shared with the generic path.
 #include <algorithm>
 #include <cmath>
 
@@ -97,29 +103,80 @@ __device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, co
 }
 
 __device__ __forceinline__ uint32_t h2_sub_magic(uint32_t x) {
-  // (1024 + c_lo, 1024 + c_hi) - 1024 -> exact (c_lo, c_hi)
+  // (1024 + v_lo, 1024 + v_hi) - 1024 -> exact (v_lo, v_hi)
   __half2 v = *reinterpret_cast<__half2*>(&x);
   const __half2 m = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
   v = __hsub2(v, m);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Fragment register r at slot s from a lane's words. B in {2,4}: one plane. B == 3: 2-bit
-// plane (w[0..NS/2)) + 1-bit plane (w[NS/2..)).
+// ---- unpack ---------------------------------------------------------------------------
+// Slots per 16-bit half: 16/B. With the class trick slot position p lives at bit offset
+// off(p) of either w (low positions) or w >> SH (high positions), giving value c * 2^off.
+template <int B>
+struct Cls;
+template <>
+struct Cls<2> {  // positions 0..4 from w (offsets 0,2,..,8), 5..7 from w >> 10
+  static constexpr int SPH = 8;
+  __host__ __device__ static constexpr int split() { return 5; }
+  __host__ __device__ static constexpr int sh() { return 10; }
+  __host__ __device__ static constexpr int off(int p) { return 2 * (p < 5 ? p : p - 5); }
+};
+template <>
+struct Cls<4> {  // positions 0,1 from w (offsets 0,4), 2,3 from w >> 8
+  static constexpr int SPH = 4;
+  __host__ __device__ static constexpr int split() { return 2; }
+  __host__ __device__ static constexpr int sh() { return 8; }
+  __host__ __device__ static constexpr int off(int p) { return 4 * (p < 2 ? p : p - 2); }
+};
+template <>
+struct Cls<3> {  // 2-bit low plane at positions 0..3 of w / w >> 8 (hi bit lands at off+2 <= 8)
+  static constexpr int SPH = 8;
+  __host__ __device__ static constexpr int split() { return 4; }
+  __host__ __device__ static constexpr int sh() { return 8; }
+  __host__ __device__ static constexpr int off(int p) { return 2 * (p < 4 ? p : p - 4); }
+};
+
 template <int B, int NS>
-__device__ __forceinline__ uint32_t frag(const uint32_t* w, int r, int s) {
-  const int vs = r * NS + s;
-  if constexpr (B == 3) {
-    const uint32_t lo = (w[vs >> 3] >> (2 * (vs & 7))) & 0x00030003u;
-    const uint32_t hi = (w[NS / 2 + (vs >> 4)] >> (vs & 15)) & 0x00010001u;
-    return h2_sub_magic(lo | (hi << 2) | 0x64006400u);
-  } else {
-    constexpr int SPH = 16 / B;
-    constexpr uint32_t MASK = B == 2 ? 0x00030003u : 0x000F000Fu;
-    const uint32_t x = ((w[vs / SPH] >> (B * (vs % SPH))) & MASK) | 0x64006400u;
-    return h2_sub_magic(x);
+struct Unpacker {
+  // class trick valid iff the offset depends on the slot only: NS % SPH == 0
+  static constexpr bool kClass = (NS % Cls<B>::SPH) == 0;
+  // exponent of the power of two carried by slot s
+  __host__ __device__ static constexpr int exp_of_slot(int s) { return kClass ? Cls<B>::off(s % Cls<B>::SPH) : 0; }
+
+  __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
+    const int vs = r * NS + s;
+    if constexpr (B == 3) {
+      // low 2 bits from the 2-bit plane w[0..NS/2), high bit from the 1-bit plane w[NS/2..)
+      const uint32_t hw = w[NS / 2 + (vs >> 4)];
+      const int hb = vs & 15;  // bit of the high plane in each half
+      if constexpr (kClass) {
+        const int p = vs & 7;
+        const int o = Cls<3>::off(p);
+        const uint32_t lw = p < Cls<3>::split() ? w[vs >> 3] : (w[vs >> 3] >> Cls<3>::sh());
+        const uint32_t lo = lw & (0x00030003u << o);
+        const int tgt = o + 2;
+        const uint32_t hs = hb >= tgt ? (hw >> (hb - tgt)) : (hw << (tgt - hb));
+        return h2_sub_magic(lo | (hs & (0x00010001u << tgt)) | 0x64006400u);
+      } else {
+        const uint32_t lo = (w[vs >> 3] >> (2 * (vs & 7))) & 0x00030003u;
+        const uint32_t hi = (hw >> hb) & 0x00010001u;
+        return h2_sub_magic(lo | (hi << 2) | 0x64006400u);
+      }
+    } else {
+      constexpr int SPH = Cls<B>::SPH;
+      constexpr uint32_t MASK = B == 2 ? 0x00030003u : 0x000F000Fu;
+      const uint32_t word = w[vs / SPH];
+      if constexpr (kClass) {
+        const int p = vs % SPH;
+        const uint32_t src = p < Cls<B>::split() ? word : (word >> Cls<B>::sh());
+        return h2_sub_magic((src & (MASK << Cls<B>::off(p))) | 0x64006400u);
+      } else {
+        return h2_sub_magic(((word >> (B * (vs % SPH))) & MASK) | 0x64006400u);
+      }
+    }
   }
-}
+};
 
 // Lane's words of one tile in shared memory (layout: plane_addr in common.cuh).
 template <int B, int D>
@@ -153,9 +210,12 @@ constexpr int lane_words() {
   return B == 3 ? D * 3 / 64 : D * B / 64;
 }
 
+__device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }
+
 struct MmaParams {
   SideView k, v;
   const void* q;
+  int q16, tail16;
   int H, Hq, tq, rows, gs, cg;
   int64_t T, P;          // total tokens; fast-path limit (multiple of gs)
   int64_t groups_total;  // ceil(T / gs)
@@ -168,6 +228,10 @@ struct MmaParams {
   float* part_acc;
   double* part_cs;
 };
+
+__device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, int64_t j, int d, int D) {
+  return f16 ? tail_at<__half>(s, bh, j, d, D) : tail_at<float>(s, bh, j, d, D);
+}
 
 // Per-warp shared layout (bytes), dynamic:
 //   ring[S][stage_bytes] | bk[D][NB*8] half | bv[8][8][24] half | bp[8][24] half |
@@ -184,16 +248,19 @@ struct WarpLayout {
   }
 };
 
-template <int D, int KB, int VB, int R, typename TT, typename TQ>
+// GS: 0 = runtime group size, else compile-time (32 is the KVmix default).
+template <int D, int KB, int VB, int R, int GS>
 __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams p) {
   constexpr int NS = D / 16;                   // k-steps (Keys) / m-tiles (Values)
   constexpr int KW = lane_words<D, KB>();      // words per lane, Key tile
   constexpr int VW = lane_words<D, VB>();      // words per lane, Value tile
-  constexpr int LC = D / 32;                   // channels per lane for meta / q
+  constexpr int LC = D / 32;                   // channels per lane for meta / q / tail
   constexpr bool K3 = KB == 3;
   constexpr int NCOL = 2 * R + (K3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;           // 8-column MMA blocks for the Key GEMV
   using WL = WarpLayout<D, NB>;
+  using UK = Unpacker<KB, NS>;
+  using UV = Unpacker<VB, NS>;
   static_assert(!K3 || R <= 2, "3-bit Keys support up to 2 query rows per KV head");
 
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -206,8 +273,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
-  const int gs = p.gs, CG = p.cg, S = p.stages;
+  const int gs = GS ? GS : p.gs;
+  const int CG = GS ? D / GS : p.cg;
   const int TPG = gs / 16;  // tiles per group
+  const int S = p.stages;
 
   uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
   uint8_t* ring = wbase;
@@ -217,11 +286,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   float* sd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bp) + WL::kBp);      // [16][NB*8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sd) + WL::kSd);
 
-  // zero B staging (unused columns must stay 0)
+  // zero the P.V B staging (columns of absent query rows must stay 0)
   {
-    uint32_t* z = reinterpret_cast<uint32_t*>(bk);
-    const int n = (WL::kBk + WL::kBv + WL::kBp) / 4;
-    for (int i = lane; i < n; i += 32) z[i] = 0u;
+    uint32_t* z = reinterpret_cast<uint32_t*>(bv);
+    for (int i = lane; i < (WL::kBv + WL::kBp) / 4; i += 32) z[i] = 0u;
   }
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -235,9 +303,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   for (int r = 0; r < R; ++r) {
     const int rr = r < p.rows ? r : 0;
     const int gi = rr / p.tq, qi = rr % p.tq;
-    const TQ* qp = static_cast<const TQ*>(p.q) + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
+    const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
 #pragma unroll
-    for (int c = 0; c < LC; ++c) qv[r][c] = r < p.rows ? ld_f<TQ>(qp + c) : 0.f;
+    for (int c = 0; c < LC; ++c) {
+      const float x = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
+      qv[r][c] = r < p.rows ? x : 0.f;
+    }
   }
 
   float m_run = -INFINITY, l_run = 0.f;  // row t (threads with t < rows)
@@ -282,6 +353,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     }
   };
 
+  // channel group of each Value m-tile
+  int cg_of[NS];
+#pragma unroll
+  for (int mt = 0; mt < NS; ++mt) cg_of[mt] = (mt * 16) / gs;
+
   // prologue: fill the ring
   const int64_t first = g_beg + warp;
   if (lane == 0) {
@@ -290,11 +366,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       if (grp < g_fast_end) issue(grp, s);
     }
   }
-
-  // channel group of each Value m-tile (gs is a multiple of 16)
-  int cg_of[NS];
-#pragma unroll
-  for (int mt = 0; mt < NS; ++mt) cg_of[mt] = (mt * 16) / gs;
 
   int s = 0;
   uint32_t phase = 0;
@@ -306,7 +377,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes);
     const uint32_t* km = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes + p.vm_bytes);
 
-    // ---- Key group: B operand (q*s split hi/lo, pre-scaled by 2^e per row) and beta ----
+    // ---- Key group: B operand (q*s split hi/lo, pre-scaled by 2^(e - class) per row) ----
     float beta[R], inv_sig[R];
     {
       float sc[LC], mn[LC];
@@ -316,13 +387,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
         sc[c] = meta_scale(m);
         mn[c] = meta_min(m);
       }
+      // the k-step of this lane's channels, and the power of two its A codes carry
+      const int kk = (lane * LC) / 16;
+      int cls_e = 0;
+#pragma unroll
+      for (int x = 0; x < NS; ++x)
+        if (x == kk) cls_e = UK::exp_of_slot(x);
+      const float cls_scale = pow2i(-cls_e);
       int tau[LC];
       if constexpr (K3) {
         const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
         const int nmod = inf.x % 11, omod = inf.y % 11;
 #pragma unroll
         for (int c = 0; c < LC; ++c) {
-          const int cmod = (int)(((size_t)bh * D + lane * LC + c) % 11);
+          const int cmod = (int)(((unsigned)bh * D + lane * LC + c) % 11u);
           const int phi = (cmod * nmod + omod) % 11;  // stream index % 11 of the group's first token
           tau[c] = (21 - phi) % 11;                   // narrow tokens: t = tau (mod 11)
         }
@@ -353,14 +431,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
         const float sig = __int_as_float(se << 23);
         inv_sig[r] = __int_as_float((254 - se) << 23);
         beta[r] = bt;
+        const float sgc = sig * cls_scale;
 #pragma unroll
         for (int c = 0; c < LC; ++c) {
-          const float x = qs[c] * sig;
+          const float x = qs[c] * sgc;
           const __half hi = __float2half_rn(x);
           rowbuf[c][2 * r] = hi;
           rowbuf[c][2 * r + 1] = __float2half_rn(x - __half2float(hi));
           if constexpr (K3) {
-            const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sig;
+            const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc;
             const __half yh = __float2half_rn(y);
 #pragma unroll
             for (int xr = 0; xr < 11; ++xr) {
@@ -375,10 +454,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       __syncwarp();  // previous group's ldmatrix reads of bk are done
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
-        uint4* dst = reinterpret_cast<uint4*>(bk + (size_t)(lane * LC + c) * NB * 8);
-        const uint4* srcv = reinterpret_cast<const uint4*>(rowbuf[c]);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(bk + (size_t)(lane * LC + c) * NB * 8);
 #pragma unroll
-        for (int j = 0; j < NB; ++j) dst[j] = srcv[j];
+        for (int j = 0; j < NB * 4; ++j) {
+          dst[j] = (uint32_t)__half_as_ushort(rowbuf[c][2 * j]) | ((uint32_t)__half_as_ushort(rowbuf[c][2 * j + 1]) << 16);
+        }
       }
     }
     __syncwarp();
@@ -402,8 +482,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       for (int nb = 0; nb < NB; ++nb) dk[nb][0] = dk[nb][1] = dk[nb][2] = dk[nb][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < NS; ++kk) {
-        const uint32_t a0 = frag<KB, NS>(kw, 0, kk), a1 = frag<KB, NS>(kw, 1, kk);
-        const uint32_t a2 = frag<KB, NS>(kw, 2, kk), a3 = frag<KB, NS>(kw, 3, kk);
+        const uint32_t a0 = UK::frag(kw, 0, kk), a1 = UK::frag(kw, 1, kk);
+        const uint32_t a2 = UK::frag(kw, 2, kk), a3 = UK::frag(kw, 3, kk);
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
           uint32_t b0, b1;
@@ -416,10 +496,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
         // residue-class corrections: dump the fragments, pick each token's residue column
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
-          sd[g * NB * 8 + nb * 8 + 2 * t] = dk[nb][0];
-          sd[g * NB * 8 + nb * 8 + 2 * t + 1] = dk[nb][1];
-          sd[(g + 8) * NB * 8 + nb * 8 + 2 * t] = dk[nb][2];
-          sd[(g + 8) * NB * 8 + nb * 8 + 2 * t + 1] = dk[nb][3];
+          *reinterpret_cast<float2*>(&sd[g * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[nb][0], dk[nb][1]);
+          *reinterpret_cast<float2*>(&sd[(g + 8) * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[nb][2], dk[nb][3]);
         }
         __syncwarp();
         const int rr = t < R ? t : 0;
@@ -465,11 +543,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
               bp[2 * r][j] = hi;
               bp[2 * r + 1][j] = __float2half_rn(pj - __half2float(hi));
             }
-            for (int c = hh; c < CG; c += 2) {
-              const float x = pj * meta_scale(vmt[j * CG + c]);
-              const __half hi = __float2half_rn(x);
-              bv[c][2 * r][j] = hi;
-              bv[c][2 * r + 1][j] = __float2half_rn(x - __half2float(hi));
+#pragma unroll
+            for (int c = hh; c < (GS ? D / GS : 8); c += 2) {
+              if (GS || c < CG) {
+                const float x = pj * meta_scale(vmt[j * CG + c]);
+                const __half hi = __float2half_rn(x);
+                bv[c][2 * r][j] = hi;
+                bv[c][2 * r + 1][j] = __float2half_rn(x - __half2float(hi));
+              }
             }
           }
         }
@@ -486,13 +567,30 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
         const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bp[g][2 * t + 8]);
         mma16816(accb, a0, 0u, a2, 0u, b0, b1);
       }
+      if constexpr (GS != 0) {
+        // compile-time channel groups: load each group's B fragment once
+        constexpr int CGC = D / GS;
+        uint32_t bf0[CGC], bf1[CGC];
 #pragma unroll
-      for (int mt = 0; mt < NS; ++mt) {
-        const int c = cg_of[mt];
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
-        mma16816(accv[mt], frag<VB, NS>(vw, 0, mt), frag<VB, NS>(vw, 1, mt), frag<VB, NS>(vw, 2, mt),
-                 frag<VB, NS>(vw, 3, mt), b0, b1);
+        for (int c = 0; c < CGC; ++c) {
+          bf0[c] = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
+          bf1[c] = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < NS; ++mt) {
+          const int c = (mt * 16) / GS;
+          mma16816(accv[mt], UV::frag(vw, 0, mt), UV::frag(vw, 1, mt), UV::frag(vw, 2, mt), UV::frag(vw, 3, mt),
+                   bf0[c], bf1[c]);
+        }
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < NS; ++mt) {
+          const int c = cg_of[mt];
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
+          mma16816(accv[mt], UV::frag(vw, 0, mt), UV::frag(vw, 1, mt), UV::frag(vw, 2, mt), UV::frag(vw, 3, mt), b0,
+                   b1);
+        }
       }
       __syncwarp();
     }
@@ -507,46 +605,84 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     }
   }
 
-  // ---- tokens past the fast region: per-token CUDA-core path --------------------------
-  {
-    const int64_t j_lo = max(g_beg * gs, p.P), j_hi = min(g_end * (int64_t)gs, p.T);
-    for (int64_t j = j_lo + warp; j < j_hi; j += kMmaWarps) {
-      float part[R];
+  // undo the per-m-tile power of two carried by the Value codes
 #pragma unroll
-      for (int r = 0; r < R; ++r) part[r] = 0.f;
+  for (int mt = 0; mt < NS; ++mt) {
+    const float f = pow2i(-UV::exp_of_slot(mt));
+    accv[mt][0] *= f;
+    accv[mt][1] *= f;
+    accv[mt][2] *= f;
+    accv[mt][3] *= f;
+  }
+
+  // ---- tokens past the fast region: lane-parallel over channels ------------------------
+  // Every lane tracks all R rows (identical values across lanes); the Value contribution
+  // accumulates per lane for its LC channels and joins the fragments in the epilogue.
+  float acct[R][LC];
 #pragma unroll
-      for (int c = 0; c < LC; ++c) {
-        const int d = lane * LC + c;
-        const float kx = j < p.k.quantized ? packed_value(true, p.k, bh, j, d, D, gs)
-                                           : tail_at<TT>(p.k, bh, j - p.k.quantized, d, D);
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int r = 0; r < R; ++r) part[r] = fmaf(qv[r][c], kx, part[r]);
-      }
-      float s_mine = 0.f;
+    for (int c = 0; c < LC; ++c) acct[r][c] = 0.f;
+  const int64_t j_lo = max(g_beg * gs, p.P), j_hi = min(g_end * (int64_t)gs, p.T);
+  if (j_lo + warp < j_hi) {
+    float m_all[R], l_all[R];
+    {
+      float lr = l_run;
+      lr += __shfl_xor_sync(0xffffffffu, lr, 4);
+      lr += __shfl_xor_sync(0xffffffffu, lr, 8);
+      lr += __shfl_xor_sync(0xffffffffu, lr, 16);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        float x = part[r];
+        m_all[r] = __shfl_sync(0xffffffffu, m_run, r);  // lane r = (g 0, t r)
+        l_all[r] = __shfl_sync(0xffffffffu, lr, r);
+      }
+    }
+    const int d0 = lane * LC;
+    for (int64_t j = j_lo + warp; j < j_hi; j += kMmaWarps) {
+      float kx[LC], vx[LC];
+      if (j >= p.k.quantized) {
+#pragma unroll
+        for (int c = 0; c < LC; ++c) kx[c] = tail_val(p.k, p.tail16, bh, j - p.k.quantized, d0 + c, D);
+      } else {
+#pragma unroll
+        for (int c = 0; c < LC; ++c) kx[c] = packed_value(true, p.k, bh, j, d0 + c, D, gs);
+      }
+      if (j >= p.v.quantized) {
+#pragma unroll
+        for (int c = 0; c < LC; ++c) vx[c] = tail_val(p.v, p.tail16, bh, j - p.v.quantized, d0 + c, D);
+      } else {
+#pragma unroll
+        for (int c = 0; c < LC; ++c) vx[c] = packed_value(false, p.v, bh, j, d0 + c, D, gs);
+      }
+      float alpha_mine = 1.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float x = 0.f;
+#pragma unroll
+        for (int c = 0; c < LC; ++c) x = fmaf(qv[r][c], kx[c], x);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (r == t) s_mine = x * p.inv;
-      }
-      if (row_ok && g == 0) cs += (double)s_mine;
-      const float ls = s_mine * kLog2e;
-      const float m_new = row_ok ? fmaxf(m_run, ls) : m_run;
-      const float alpha = row_ok ? exp2f(m_run - m_new) : 1.f;
-      const float pj = row_ok ? exp2f(ls - m_new) : 0.f;
-      l_run = l_run * alpha + (g == 0 ? pj : 0.f);
-      m_run = m_new;
-      rescale(alpha);
+        if (r < p.rows) {
+          const float sc = x * p.inv;
+          if (lane == 0) cs += (double)sc;
+          const float ls = sc * kLog2e;
+          const float m_new = fmaxf(m_all[r], ls);
+          const float alpha = exp2f(m_all[r] - m_new);
+          const float pj = exp2f(ls - m_new);
+          l_all[r] = l_all[r] * alpha + pj;
+          m_all[r] = m_new;
 #pragma unroll
-      for (int mt = 0; mt < NS; ++mt) {
-        const int d0 = mt * 16 + g, d1 = d0 + 8;
-        const float v0 = j < p.v.quantized ? packed_value(false, p.v, bh, j, d0, D, gs)
-                                           : tail_at<TT>(p.v, bh, j - p.v.quantized, d0, D);
-        const float v1 = j < p.v.quantized ? packed_value(false, p.v, bh, j, d1, D, gs)
-                                           : tail_at<TT>(p.v, bh, j - p.v.quantized, d1, D);
-        accv[mt][0] = fmaf(pj, v0, accv[mt][0]);
-        accv[mt][2] = fmaf(pj, v1, accv[mt][2]);
+          for (int c = 0; c < LC; ++c) acct[r][c] = acct[r][c] * alpha + pj * vx[c];
+          if (t == r) alpha_mine = alpha;
+        }
+      }
+      rescale(alpha_mine);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (t == r) {
+        m_run = m_all[r];
+        l_run = g == 0 ? l_all[r] : 0.f;
       }
     }
   }
@@ -566,6 +702,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       s_acc[warp][t][mt * 16 + g + 8] = accv[mt][2] + accv[mt][3];
     }
     s_bias[warp][t][g] = accb[0] + accb[1];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r < p.rows) {
+#pragma unroll
+      for (int c = 0; c < LC; ++c) s_acc[warp][r][lane * LC + c] += acct[r][c];
+    }
   }
   for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
   if (lane == 0) s_cs[warp] = cs;
@@ -599,41 +743,36 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   }
 }
 
-template <int D, int KB, int VB, int R, typename TT, typename TQ>
+template <int D, int KB, int VB, int R, int GS>
 void launch(const MmaParams& p, int nsplit, int BH, cudaStream_t st) {
   constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;
   const size_t smem = (size_t)kMmaWarps * WarpLayout<D, NB>::bytes(p.stages, p.stage_bytes);
-  auto kern = attend_mma_kernel<D, KB, VB, R, TT, TQ>;
+  auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   kern<<<dim3(nsplit, BH), kMmaWarps * 32, smem, st>>>(p);
 }
 
 template <int D, int KB, int VB, int R>
-bool dispatch_types(const MmaParams& p, int nsplit, int BH, bool tail16, bool q16, cudaStream_t st) {
+bool dispatch_gs(const MmaParams& p, int nsplit, int BH, cudaStream_t st) {
   if constexpr (KB == 3 && R > 2) {
     return false;
   } else {
-    if (tail16) {
-      if (q16) launch<D, KB, VB, R, __half, __half>(p, nsplit, BH, st);
-      else launch<D, KB, VB, R, __half, float>(p, nsplit, BH, st);
-    } else {
-      if (q16) launch<D, KB, VB, R, float, __half>(p, nsplit, BH, st);
-      else launch<D, KB, VB, R, float, float>(p, nsplit, BH, st);
-    }
+    if (p.gs == 32) launch<D, KB, VB, R, 32>(p, nsplit, BH, st);
+    else launch<D, KB, VB, R, 0>(p, nsplit, BH, st);
     return true;
   }
 }
 
 template <int D, int R>
-bool dispatch_bits(const MmaParams& p, int kb, int vb, int nsplit, int BH, bool tail16, bool q16, cudaStream_t st) {
+bool dispatch_bits(const MmaParams& p, int kb, int vb, int nsplit, int BH, cudaStream_t st) {
   switch (kb * 10 + vb) {
-    case 22: return dispatch_types<D, 2, 2, R>(p, nsplit, BH, tail16, q16, st);
-    case 24: return dispatch_types<D, 2, 4, R>(p, nsplit, BH, tail16, q16, st);
-    case 42: return dispatch_types<D, 4, 2, R>(p, nsplit, BH, tail16, q16, st);
-    case 44: return dispatch_types<D, 4, 4, R>(p, nsplit, BH, tail16, q16, st);
-    case 32: return dispatch_types<D, 3, 2, R>(p, nsplit, BH, tail16, q16, st);
-    case 34: return dispatch_types<D, 3, 4, R>(p, nsplit, BH, tail16, q16, st);
+    case 22: return dispatch_gs<D, 2, 2, R>(p, nsplit, BH, st);
+    case 24: return dispatch_gs<D, 2, 4, R>(p, nsplit, BH, st);
+    case 42: return dispatch_gs<D, 4, 2, R>(p, nsplit, BH, st);
+    case 44: return dispatch_gs<D, 4, 4, R>(p, nsplit, BH, st);
+    case 32: return dispatch_gs<D, 3, 2, R>(p, nsplit, BH, st);
+    case 34: return dispatch_gs<D, 3, 4, R>(p, nsplit, BH, st);
     default: return false;
   }
 }
@@ -662,6 +801,8 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.k = view(c->k);
   p.v = view(c->v);
   p.q = q;
+  p.q16 = dt == KVMIX_F16;
+  p.tail16 = c->tail_dtype == KVMIX_F16;
   p.H = c->H;
   p.Hq = Hq;
   p.tq = tq;
@@ -687,14 +828,13 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
   p.part_acc = ws.acc(st, (size_t)BH * cap_splits * rows * D);
   p.part_cs = ws.cs(st, (size_t)BH * cap_splits + 1);
-  const bool tail16 = c->tail_dtype == KVMIX_F16, q16 = dt == KVMIX_F16;
   const int R = rows <= 1 ? 1 : rows <= 2 ? 2 : 4;
   bool ok = false;
-#define KVB_DISPATCH_D(DD)                                                              \
-  if (D == DD) {                                                                        \
-    if (R == 1) ok = dispatch_bits<DD, 1>(p, kb, vb, nsplit, BH, tail16, q16, st);      \
-    else if (R == 2) ok = dispatch_bits<DD, 2>(p, kb, vb, nsplit, BH, tail16, q16, st); \
-    else ok = dispatch_bits<DD, 4>(p, kb, vb, nsplit, BH, tail16, q16, st);             \
+#define KVB_DISPATCH_D(DD)                                                  \
+  if (D == DD) {                                                            \
+    if (R == 1) ok = dispatch_bits<DD, 1>(p, kb, vb, nsplit, BH, st);      \
+    else if (R == 2) ok = dispatch_bits<DD, 2>(p, kb, vb, nsplit, BH, st); \
+    else ok = dispatch_bits<DD, 4>(p, kb, vb, nsplit, BH, st);             \
   }
   KVB_DISPATCH_D(64)
   KVB_DISPATCH_D(128)

@@ -59,29 +59,41 @@ inline SideView view(const kvmix_cache::Side& s) {
 
 template <typename TT>
 __device__ inline float tail_at(const SideView& s, int bh, int64_t j, int d, int D) {
-  return ld_f<TT>(static_cast<const TT*>(s.tail) + ((size_t)bh * s.tail_cap + (size_t)((s.tail_start + j) % s.tail_cap)) * D + d);
+  int64_t slot = s.tail_start + j;  // j < tail_len <= tail_cap
+  if (slot >= s.tail_cap) slot -= s.tail_cap;
+  return ld_f<TT>(static_cast<const TT*>(s.tail) + ((size_t)bh * s.tail_cap + (size_t)slot) * D + d);
+}
+
+// Narrow-slot test for the Mixed3 layout from the segment info, in mod-11 arithmetic
+// (stream index = (bh*D + d)*n + t_local for Keys, (bh*n + t_local)*D + d for Values).
+__device__ inline bool narrow_key(int bh, int d, int D, int2 info, int t_in_group) {
+  const int c = (int)(((unsigned)bh * (unsigned)D + (unsigned)d) % 11u);
+  return (c * (info.x % 11) + (info.y + t_in_group) % 11) % 11 == 10;
+}
+__device__ inline bool narrow_value(int bh, int d, int D, int2 info) {
+  const int tok = (int)(((unsigned)bh % 11u) * (unsigned)(info.x % 11) % 11u + (unsigned)(info.y % 11)) % 11;
+  return (tok * (D % 11) + d % 11) % 11 == 10;
 }
 
 // Dequantized value of quantized token j (j < s.quantized) of one side, bit-exact.
-__device__ inline float packed_value(bool key, const SideView& s, int bh, int64_t j, int d, int D, int gs) {
+__device__ inline float packed_value(bool key, const SideView& s, int bh, int64_t j64, int d, int D, int gs) {
+  const int j = (int)j64;
   const uint32_t* tile = s.tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
-  const int i = (int)(j & 15);
+  const int i = j & 15;
   const uint32_t code = tile_get(tile, key ? key_coord(i, d) : value_coord(i, d), D, s.bits);
   uint32_t m;
-  uint64_t si;
+  bool narrow = false;
   if (key) {
-    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)(j / gs) * D + d];
-    const int2 inf = s.info[j / gs];
-    si = ((uint64_t)bh * D + d) * (uint64_t)inf.x + (uint64_t)(inf.y + j % gs);
+    const int grp = j / gs;
+    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)grp * D + d];
+    if (s.bits == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
   } else {
     const int cg = (D + gs - 1) / gs;
     m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)j * cg + d / gs];
-    const int2 inf = s.info[j];
-    si = ((uint64_t)bh * inf.x + (uint64_t)inf.y) * D + d;
+    if (s.bits == 3) narrow = narrow_value(bh, d, D, s.info[j]);
   }
-  return decode(code, meta_scale(m), meta_min(m), is_narrow(s.bits, si));
+  return decode(code, meta_scale(m), meta_min(m), narrow);
 }
-
 
 void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, int t, cudaStream_t st);
 void cache_snapshot(const kvmix_cache* c, float* keys, float* values, cudaStream_t st);
