@@ -234,14 +234,14 @@ __device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, i
 }
 
 // Per-warp shared layout (bytes), dynamic:
-//   ring[S][stage_bytes] | bk[D][NB*8] half | bv[8][8][24] half | bp[8][24] half |
-//   sd[16][NB*8] float (3-bit Keys only) | bars[S] u64
-template <int D, int NB>
+//   ring[S][stage_bytes] | bk[D][NB*8] half | bv[2][8][8][24] half | bp[2][8][24] half |
+//   sd[32][NB*8] float (3-bit Keys only) | bars[S] u64
+template <int D, int NB, int CGMAX>
 struct WarpLayout {
   static constexpr int kBk = D * NB * 8 * 2;
-  static constexpr int kBv = 8 * 8 * 24 * 2;
-  static constexpr int kBp = 8 * 24 * 2;
-  static constexpr int kSd = NB > 1 ? 16 * NB * 8 * 4 : 0;
+  static constexpr int kBv = 2 * CGMAX * 8 * 24 * 2;
+  static constexpr int kBp = 2 * 8 * 24 * 2;
+  static constexpr int kSd = NB > 1 ? 32 * NB * 8 * 4 : 0;
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
     const size_t n = (size_t)stages * stage_bytes + kBk + kBv + kBp + kSd + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
@@ -258,7 +258,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   constexpr bool K3 = KB == 3;
   constexpr int NCOL = 2 * R + (K3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;           // 8-column MMA blocks for the Key GEMV
-  using WL = WarpLayout<D, NB>;
+  constexpr int CGMAX = GS ? D / GS : 8;       // channel groups held in the P.V staging
+  using WL = WarpLayout<D, NB, CGMAX>;
   using UK = Unpacker<KB, NS>;
   using UV = Unpacker<VB, NS>;
   static_assert(!K3 || R <= 2, "3-bit Keys support up to 2 query rows per KV head");
@@ -281,15 +282,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
   uint8_t* ring = wbase;
   __half* bk = reinterpret_cast<__half*>(ring + (size_t)S * p.stage_bytes);            // [D][NB*8]
-  __half(*bv)[8][24] = reinterpret_cast<__half(*)[8][24]>(reinterpret_cast<uint8_t*>(bk) + WL::kBk);
-  __half(*bp)[24] = reinterpret_cast<__half(*)[24]>(reinterpret_cast<uint8_t*>(bv) + WL::kBv);
-  float* sd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bp) + WL::kBp);      // [16][NB*8]
+  __half(*bv)[CGMAX][8][24] = reinterpret_cast<__half(*)[CGMAX][8][24]>(reinterpret_cast<uint8_t*>(bk) + WL::kBk);  // [tile][cg][col][tok]
+  __half(*bp)[8][24] = reinterpret_cast<__half(*)[8][24]>(reinterpret_cast<uint8_t*>(bv) + WL::kBv);          // [tile][col][tok]
+  float* sd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bp) + WL::kBp);      // [32][NB*8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sd) + WL::kSd);
 
-  // zero the P.V B staging (columns of absent query rows must stay 0)
+  // zero the B staging (columns of absent query rows must stay 0)
   {
-    uint32_t* z = reinterpret_cast<uint32_t*>(bv);
-    for (int i = lane; i < (WL::kBv + WL::kBp) / 4; i += 32) z[i] = 0u;
+    uint32_t* z = reinterpret_cast<uint32_t*>(bk);
+    for (int i = lane; i < (WL::kBk + WL::kBv + WL::kBp) / 4; i += 32) z[i] = 0u;
   }
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -367,6 +368,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
     }
   }
 
+  // the k-step of this lane's channels and the power of two its A codes carry
+  float cls_scale = 1.f;
+  {
+    const int kk = (lane * LC) / 16;
+#pragma unroll
+    for (int x = 0; x < NS; ++x)
+      if (x == kk) cls_scale = pow2i(-UK::exp_of_slot(x));
+  }
+
   int s = 0;
   uint32_t phase = 0;
   for (int64_t grp = first; grp < g_fast_end; grp += kMmaWarps) {
@@ -387,13 +397,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
         sc[c] = meta_scale(m);
         mn[c] = meta_min(m);
       }
-      // the k-step of this lane's channels, and the power of two its A codes carry
-      const int kk = (lane * LC) / 16;
-      int cls_e = 0;
-#pragma unroll
-      for (int x = 0; x < NS; ++x)
-        if (x == kk) cls_e = UK::exp_of_slot(x);
-      const float cls_scale = pow2i(-cls_e);
       int tau[LC];
       if constexpr (K3) {
         const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
@@ -405,11 +408,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
           tau[c] = (21 - phi) % 11;                   // narrow tokens: t = tau (mod 11)
         }
       }
-      __half rowbuf[LC][NB * 8];
+      uint32_t row[LC][NB * 4];  // this lane's B rows (channel-major), packed half2
 #pragma unroll
       for (int c = 0; c < LC; ++c)
 #pragma unroll
-        for (int j = 0; j < NB * 8; ++j) rowbuf[c][j] = __ushort_as_half(0);
+        for (int j = 0; j < NB * 4; ++j) row[c][j] = 0u;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         float qs[LC], mx = 0.f, bt = 0.f;
@@ -420,34 +423,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
           bt = fmaf(qv[r][c], mn[c], bt);
           if constexpr (K3) mx = fmaxf(mx, fabsf(qv[r][c] * (wide_scale(sc[c]) - sc[c])));
         }
+        // max over the warp on the (non-negative) float bits: one REDUX
+        const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          bt += __shfl_xor_sync(0xffffffffu, bt, o);
-        }
+        for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
         // sigma = 2^(14 - floor(log2 max|qs|)): max|qs*sigma| in [2^14, 2^15)
-        const int e = (__float_as_int(mx) >> 23) & 0xff;
+        const int e = (int)((mxu >> 23) & 0xffu);
         const int se = min(max(268 - e, 1), 254);
-        const float sig = __int_as_float(se << 23);
         inv_sig[r] = __int_as_float((254 - se) << 23);
         beta[r] = bt;
-        const float sgc = sig * cls_scale;
+        const float sgc = __int_as_float(se << 23) * cls_scale;
 #pragma unroll
         for (int c = 0; c < LC; ++c) {
           const float x = qs[c] * sgc;
           const __half hi = __float2half_rn(x);
-          rowbuf[c][2 * r] = hi;
-          rowbuf[c][2 * r + 1] = __float2half_rn(x - __half2float(hi));
+          const __half lo = __float2half_rn(x - __half2float(hi));
+          row[c][r] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
           if constexpr (K3) {
             const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc;
             const __half yh = __float2half_rn(y);
+            const __half yl = __float2half_rn(y - __half2float(yh));
+            const uint32_t yp = (uint32_t)__half_as_ushort(yh) | ((uint32_t)__half_as_ushort(yl) << 16);
 #pragma unroll
-            for (int xr = 0; xr < 11; ++xr) {
-              if (tau[c] == xr) {
-                rowbuf[c][2 * R + (r * 11 + xr) * 2] = yh;
-                rowbuf[c][2 * R + (r * 11 + xr) * 2 + 1] = __float2half_rn(y - __half2float(yh));
-              }
-            }
+            for (int xr = 0; xr < 11; ++xr) row[c][R + r * 11 + xr] = tau[c] == xr ? yp : 0u;
           }
         }
       }
@@ -455,10 +453,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
         uint32_t* dst = reinterpret_cast<uint32_t*>(bk + (size_t)(lane * LC + c) * NB * 8);
+        // columns of absent rows stay zero from the kernel prologue
 #pragma unroll
-        for (int j = 0; j < NB * 4; ++j) {
-          dst[j] = (uint32_t)__half_as_ushort(rowbuf[c][2 * j]) | ((uint32_t)__half_as_ushort(rowbuf[c][2 * j + 1]) << 16);
-        }
+        for (int j = 0; j < (K3 ? NB * 4 : R); ++j) dst[j] = row[c][j];
       }
     }
     __syncwarp();
@@ -471,125 +468,152 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       }
     }
 
-    for (int tt = 0; tt < TPG; ++tt) {
-      uint32_t kw[KW], vw[VW];
-      lds_tile<KB, D>(kt + (size_t)tt * tile_words(D, KB), lane, kw);
-      lds_tile<VB, D>(vt + (size_t)tt * tile_words(D, VB), lane, vw);
-
-      // ---- scores: K (16 tokens x D) . B ----
-      float dk[NB][4];
+    // ---- the group's tiles, two at a time (independent MMA chains, one softmax round) ----
+    for (int tp = 0; tp < TPG; tp += 2) {
+      uint32_t kw[2][KW], vw[2][VW];
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) dk[nb][0] = dk[nb][1] = dk[nb][2] = dk[nb][3] = 0.f;
+      for (int u = 0; u < 2; ++u) {
+        lds_tile<KB, D>(kt + (size_t)(tp + u) * tile_words(D, KB), lane, kw[u]);
+        lds_tile<VB, D>(vt + (size_t)(tp + u) * tile_words(D, VB), lane, vw[u]);
+      }
+      // scores: K (16 tokens x D) . B, both tiles
+      float dk[2][NB][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) dk[u][nb][0] = dk[u][nb][1] = dk[u][nb][2] = dk[u][nb][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < NS; ++kk) {
-        const uint32_t a0 = UK::frag(kw, 0, kk), a1 = UK::frag(kw, 1, kk);
-        const uint32_t a2 = UK::frag(kw, 2, kk), a3 = UK::frag(kw, 3, kk);
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
           uint32_t b0, b1;
           ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB * 8 + nb * 8);
-          mma16816(dk[nb], a0, a1, a2, a3, b0, b1);
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            mma16816(dk[u][nb], UK::frag(kw[u], 0, kk), UK::frag(kw[u], 1, kk), UK::frag(kw[u], 2, kk),
+                     UK::frag(kw[u], 3, kk), b0, b1);
         }
       }
-      float va, vb_;  // row t: token g / token g+8 (K-sum * sigma)
+      float sa[2], sb[2];  // row t: token g / token g+8 of each tile
       if constexpr (K3) {
         // residue-class corrections: dump the fragments, pick each token's residue column
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          *reinterpret_cast<float2*>(&sd[g * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[nb][0], dk[nb][1]);
-          *reinterpret_cast<float2*>(&sd[(g + 8) * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[nb][2], dk[nb][3]);
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            *reinterpret_cast<float2*>(&sd[(u * 16 + g) * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[u][nb][0], dk[u][nb][1]);
+            *reinterpret_cast<float2*>(&sd[(u * 16 + g + 8) * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[u][nb][2], dk[u][nb][3]);
+          }
         }
         __syncwarp();
         const int rr = t < R ? t : 0;
-        const int xa = (tt * 16 + g) % 11, xb = (tt * 16 + g + 8) % 11;
-        const float* ra = sd + g * NB * 8;
-        const float* rb = sd + (g + 8) * NB * 8;
-        va = ra[2 * rr] + ra[2 * rr + 1] + ra[2 * R + (rr * 11 + xa) * 2] + ra[2 * R + (rr * 11 + xa) * 2 + 1];
-        vb_ = rb[2 * rr] + rb[2 * rr + 1] + rb[2 * R + (rr * 11 + xb) * 2] + rb[2 * R + (rr * 11 + xb) * 2 + 1];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int xa = ((tp + u) * 16 + g) % 11, xb = ((tp + u) * 16 + g + 8) % 11;
+          const float* ra = sd + (u * 16 + g) * NB * 8;
+          const float* rb = sd + (u * 16 + g + 8) * NB * 8;
+          sa[u] = ra[2 * rr] + ra[2 * rr + 1] + ra[2 * R + (rr * 11 + xa) * 2] + ra[2 * R + (rr * 11 + xa) * 2 + 1];
+          sb[u] = rb[2 * rr] + rb[2 * rr + 1] + rb[2 * R + (rr * 11 + xb) * 2] + rb[2 * R + (rr * 11 + xb) * 2 + 1];
+        }
         __syncwarp();
       } else {
-        va = dk[0][0] + dk[0][1];
-        vb_ = dk[0][2] + dk[0][3];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          sa[u] = dk[u][0][0] + dk[u][0][1];
+          sb[u] = dk[u][0][2] + dk[u][0][3];
+        }
       }
-      const float sa = (va * my_isig + my_beta) * p.inv;
-      const float sb = (vb_ * my_isig + my_beta) * p.inv;
-      if (row_ok) cs += (double)(sa + sb);
-      const float la = sa * kLog2e, lb = sb * kLog2e;
-      float tmax = fmaxf(la, lb);
+      float la[2], lb[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        sa[u] = (sa[u] * my_isig + my_beta) * p.inv;
+        sb[u] = (sb[u] * my_isig + my_beta) * p.inv;
+        la[u] = sa[u] * kLog2e;
+        lb[u] = sb[u] * kLog2e;
+      }
+      if (row_ok) cs += (double)((sa[0] + sb[0]) + (sa[1] + sb[1]));
+      float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
       const float m_new = fmaxf(m_run, tmax);
       const float alpha = exp2f(m_run - m_new);
-      const float pa = row_ok ? exp2f(la - m_new) : 0.f;
-      const float pb = row_ok ? exp2f(lb - m_new) : 0.f;
-      l_run = l_run * alpha + pa + pb;
+      float pa[2], pb[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        pa[u] = row_ok ? exp2f(la[u] - m_new) : 0.f;
+        pb[u] = row_ok ? exp2f(lb[u] - m_new) : 0.f;
+      }
+      l_run = l_run * alpha + ((pa[0] + pb[0]) + (pa[1] + pb[1]));
       m_run = m_new;
       rescale(alpha);
 
-      // ---- P.V B operands: lane -> token j = lane % 16 ----
-      const uint32_t* vmt = vm + (size_t)tt * 16 * CG;  // [16][CG]
+      // ---- P.V B operands: lane j -> token j of the 32 (tile j/16, row-in-tile j%16) ----
       {
-        const int j = lane & 15, hh = lane >> 4;
+        const int u = lane >> 4, i = lane & 15;
+        const uint32_t* vmt = vm + (size_t)(tp * 16 + lane) * CG;  // this token's Value meta
+        float vsc[GS ? D / GS : 8];
+#pragma unroll
+        for (int c = 0; c < (GS ? D / GS : 8); ++c)
+          if (GS || c < CG) vsc[c] = meta_scale(vmt[c]);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int src = (j & 7) * 4 + r;
-          const float xa = __shfl_sync(0xffffffffu, pa, src);
-          const float xb = __shfl_sync(0xffffffffu, pb, src);
-          const float pj = j < 8 ? xa : xb;
+          const int src = (i & 7) * 4 + r;
+          const float x0 = __shfl_sync(0xffffffffu, pa[0], src);
+          const float x1 = __shfl_sync(0xffffffffu, pb[0], src);
+          const float x2 = __shfl_sync(0xffffffffu, pa[1], src);
+          const float x3 = __shfl_sync(0xffffffffu, pb[1], src);
+          const float pj = u == 0 ? (i < 8 ? x0 : x1) : (i < 8 ? x2 : x3);
           if (r < p.rows) {
-            if (hh == 0) {
-              const __half hi = __float2half_rn(pj);
-              bp[2 * r][j] = hi;
-              bp[2 * r + 1][j] = __float2half_rn(pj - __half2float(hi));
-            }
+            const __half hi = __float2half_rn(pj);
+            bp[u][2 * r][i] = hi;
+            bp[u][2 * r + 1][i] = __float2half_rn(pj - __half2float(hi));
 #pragma unroll
-            for (int c = hh; c < (GS ? D / GS : 8); c += 2) {
+            for (int c = 0; c < (GS ? D / GS : 8); ++c) {
               if (GS || c < CG) {
-                const float x = pj * meta_scale(vmt[j * CG + c]);
-                const __half hi = __float2half_rn(x);
-                bv[c][2 * r][j] = hi;
-                bv[c][2 * r + 1][j] = __float2half_rn(x - __half2float(hi));
+                const float x = pj * vsc[c];
+                const __half xh = __float2half_rn(x);
+                bv[u][c][2 * r][i] = xh;
+                bv[u][c][2 * r + 1][i] = __float2half_rn(x - __half2float(xh));
               }
             }
           }
         }
       }
       __syncwarp();
-      // bias MMA: A = Value mins [group][token] (rows >= CG are zero), B = p
-      {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t* vmt = vm + (size_t)(tp + u) * 16 * CG;  // [16][CG]
+        // bias MMA: A = Value mins [group][token] (rows >= CG are zero), B = p
         uint32_t a0 = 0u, a2 = 0u;
         if (g < CG) {
           a0 = __byte_perm(vmt[(2 * t) * CG + g], vmt[(2 * t + 1) * CG + g], 0x7632);
           a2 = __byte_perm(vmt[(2 * t + 8) * CG + g], vmt[(2 * t + 9) * CG + g], 0x7632);
         }
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bp[g][2 * t]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bp[g][2 * t + 8]);
-        mma16816(accb, a0, 0u, a2, 0u, b0, b1);
-      }
-      if constexpr (GS != 0) {
-        // compile-time channel groups: load each group's B fragment once
-        constexpr int CGC = D / GS;
-        uint32_t bf0[CGC], bf1[CGC];
+        mma16816(accb, a0, 0u, a2, 0u, *reinterpret_cast<const uint32_t*>(&bp[u][g][2 * t]),
+                 *reinterpret_cast<const uint32_t*>(&bp[u][g][2 * t + 8]));
+        if constexpr (GS != 0) {
+          constexpr int CGC = D / GS;
+          uint32_t bf0[CGC], bf1[CGC];
 #pragma unroll
-        for (int c = 0; c < CGC; ++c) {
-          bf0[c] = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
-          bf1[c] = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
-        }
+          for (int c = 0; c < CGC; ++c) {
+            bf0[c] = *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t]);
+            bf1[c] = *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t + 8]);
+          }
 #pragma unroll
-        for (int mt = 0; mt < NS; ++mt) {
-          const int c = (mt * 16) / GS;
-          mma16816(accv[mt], UV::frag(vw, 0, mt), UV::frag(vw, 1, mt), UV::frag(vw, 2, mt), UV::frag(vw, 3, mt),
-                   bf0[c], bf1[c]);
-        }
-      } else {
+          for (int mt = 0; mt < NS; ++mt) {
+            const int c = (mt * 16) / GS;
+            mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
+                     UV::frag(vw[u], 3, mt), bf0[c], bf1[c]);
+          }
+        } else {
 #pragma unroll
-        for (int mt = 0; mt < NS; ++mt) {
-          const int c = cg_of[mt];
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t]);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&bv[c][g][2 * t + 8]);
-          mma16816(accv[mt], UV::frag(vw, 0, mt), UV::frag(vw, 1, mt), UV::frag(vw, 2, mt), UV::frag(vw, 3, mt), b0,
-                   b1);
+          for (int mt = 0; mt < NS; ++mt) {
+            const int c = cg_of[mt];
+            mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
+                     UV::frag(vw[u], 3, mt), *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t]),
+                     *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t + 8]));
+          }
         }
       }
       __syncwarp();
@@ -747,7 +771,7 @@ template <int D, int KB, int VB, int R, int GS>
 void launch(const MmaParams& p, int nsplit, int BH, cudaStream_t st) {
   constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;
-  const size_t smem = (size_t)kMmaWarps * WarpLayout<D, NB>::bytes(p.stages, p.stage_bytes);
+  const size_t smem = (size_t)kMmaWarps * WarpLayout<D, NB, GS ? D / GS : 8>::bytes(p.stages, p.stage_bytes);
   auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   kern<<<dim3(nsplit, BH), kMmaWarps * 32, smem, st>>>(p);
@@ -794,6 +818,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   const int kb = c->k.bits, vb = c->v.bits;
   if (vb == 3 || (kb == 3 && rows > 2)) return false;
   const int D = c->D, gs = c->cfg.group_size;
+  if (gs % 32 != 0) return false;  // groups are processed two tiles at a time
   if (D != 64 && D != 128) return false;
   const int BH = c->B * c->H;
   const int64_t T = c->total();
@@ -821,8 +846,8 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.km_bytes = (uint32_t)(D * 4);
   p.stage_bytes = p.kt_bytes + p.vt_bytes + p.vm_bytes + p.km_bytes;
   if (p.vm_bytes % 16) return false;
-  // ring depth: ~12 KB in flight per warp, 2..4 stages
-  p.stages = (int)std::max<uint32_t>(2, std::min<uint32_t>(4, 12288 / p.stage_bytes));
+  // ring depth: ~9 KB in flight per warp, 2..4 stages
+  p.stages = (int)std::max<uint32_t>(2, std::min<uint32_t>(4, 9216 / p.stage_bytes));
   p.inv = 1.0f / sqrtf((float)D);
   const int cap_splits = mma_splits(BH, (int64_t)1 << 40);
   p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
