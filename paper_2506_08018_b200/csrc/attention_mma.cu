@@ -102,6 +102,14 @@ __device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, co
                : "r"(smem_u32(row_addr)));
 }
 
+// (a & MASK) | c in one LOP3 (MASK as the immediate, the 0x6400 magic in a register)
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t h2_sub_magic(uint32_t x) {
   // (1024 + v_lo, 1024 + v_hi) - 1024 -> exact (v_lo, v_hi)
   __half2 v = *reinterpret_cast<__half2*>(&x);
@@ -170,7 +178,16 @@ struct Unpacker {
       if constexpr (kClass) {
         const int p = vs % SPH;
         const uint32_t src = p < Cls<B>::split() ? word : (word >> Cls<B>::sh());
-        return h2_sub_magic((src & (MASK << Cls<B>::off(p))) | 0x64006400u);
+        const uint32_t magic = 0x64006400u;
+        uint32_t x;
+        switch (Cls<B>::off(p)) {  // compile-time after unrolling
+          case 0: x = and_or<MASK>(src, magic); break;
+          case 2: x = and_or<(MASK << 2)>(src, magic); break;
+          case 4: x = and_or<(MASK << 4)>(src, magic); break;
+          case 6: x = and_or<(MASK << 6)>(src, magic); break;
+          default: x = and_or<(MASK << 8)>(src, magic); break;
+        }
+        return h2_sub_magic(x);
       } else {
         return h2_sub_magic(((word >> (B * (vs % SPH))) & MASK) | 0x64006400u);
       }
@@ -289,8 +306,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
 
   // zero the B staging (columns of absent query rows must stay 0)
   {
-    uint32_t* z = reinterpret_cast<uint32_t*>(bk);
-    for (int i = lane; i < (WL::kBk + WL::kBv + WL::kBp) / 4; i += 32) z[i] = 0u;
+    uint4* z = reinterpret_cast<uint4*>(bk);
+    for (int i = lane; i < (WL::kBk + WL::kBv + WL::kBp) / 16; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -453,9 +470,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
         uint32_t* dst = reinterpret_cast<uint32_t*>(bk + (size_t)(lane * LC + c) * NB * 8);
-        // columns of absent rows stay zero from the kernel prologue
+        if constexpr (K3) {
 #pragma unroll
-        for (int j = 0; j < (K3 ? NB * 4 : R); ++j) dst[j] = row[c][j];
+          for (int j = 0; j < NB; ++j)
+            reinterpret_cast<uint4*>(dst)[j] = make_uint4(row[c][4 * j], row[c][4 * j + 1], row[c][4 * j + 2], row[c][4 * j + 3]);
+        } else {
+          // columns of absent rows stay zero from the kernel prologue
+#pragma unroll
+          for (int j = 0; j < R; ++j) dst[j] = row[c][j];
+        }
       }
     }
     __syncwarp();
@@ -767,49 +790,75 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   }
 }
 
+// Split count: pick the number of CTAs per (b, kv-head) that fills whole waves of the
+// kernel's real residency (occupancy query), with at least two groups per warp; bounded by
+// a cap that depends on (B, H) only, so scratch never depends on the token count.
+int split_cap(int BH) {
+  // up to ~16 waves of 3 CTAs/SM; depends on (B, H) only
+  return std::max(1, std::min(512, (16 * 3 * num_sms() + BH - 1) / std::max(1, BH)));
+}
+
+int pick_splits(int BH, int64_t groups, int slots) {
+  const int cap = split_cap(BH);
+  int best = 1;
+  double best_score = -1.0;
+  for (int n = 1; n <= cap; ++n) {
+    const int64_t chunk = (groups + n - 1) / n;
+    if (n > 1 && chunk < 2 * kMmaWarps) break;
+    const double waves = (double)n * BH / slots;
+    const double eff = waves / std::ceil(waves);
+    const double score = eff - 0.002 * n;
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = n;
+    }
+  }
+  return best;
+}
+
 template <int D, int KB, int VB, int R, int GS>
-void launch(const MmaParams& p, int nsplit, int BH, cudaStream_t st) {
+int launch(MmaParams& p, int BH, cudaStream_t st) {
   constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;
   const size_t smem = (size_t)kMmaWarps * WarpLayout<D, NB, GS ? D / GS : 8>::bytes(p.stages, p.stage_bytes);
   auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  static thread_local size_t occ_smem = 0;
+  static thread_local int occ = 0;
+  if (occ_smem != smem) {  // residency of this instantiation at this ring size (cached)
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMmaWarps * 32, smem), "occupancy");
+    occ_smem = smem;
+  }
+  const int nsplit = pick_splits(BH, p.groups_total, std::max(1, occ) * num_sms());
+  p.chunk_groups = (int)((p.groups_total + nsplit - 1) / nsplit);
   kern<<<dim3(nsplit, BH), kMmaWarps * 32, smem, st>>>(p);
+  return nsplit;
 }
 
 template <int D, int KB, int VB, int R>
-bool dispatch_gs(const MmaParams& p, int nsplit, int BH, cudaStream_t st) {
+int dispatch_gs(MmaParams& p, int BH, cudaStream_t st) {
   if constexpr (KB == 3 && R > 2) {
-    return false;
+    return 0;
   } else {
-    if (p.gs == 32) launch<D, KB, VB, R, 32>(p, nsplit, BH, st);
-    else launch<D, KB, VB, R, 0>(p, nsplit, BH, st);
-    return true;
+    return p.gs == 32 ? launch<D, KB, VB, R, 32>(p, BH, st) : launch<D, KB, VB, R, 0>(p, BH, st);
   }
 }
 
 template <int D, int R>
-bool dispatch_bits(const MmaParams& p, int kb, int vb, int nsplit, int BH, cudaStream_t st) {
+int dispatch_bits(MmaParams& p, int kb, int vb, int BH, cudaStream_t st) {
   switch (kb * 10 + vb) {
-    case 22: return dispatch_gs<D, 2, 2, R>(p, nsplit, BH, st);
-    case 24: return dispatch_gs<D, 2, 4, R>(p, nsplit, BH, st);
-    case 42: return dispatch_gs<D, 4, 2, R>(p, nsplit, BH, st);
-    case 44: return dispatch_gs<D, 4, 4, R>(p, nsplit, BH, st);
-    case 32: return dispatch_gs<D, 3, 2, R>(p, nsplit, BH, st);
-    case 34: return dispatch_gs<D, 3, 4, R>(p, nsplit, BH, st);
-    default: return false;
+    case 22: return dispatch_gs<D, 2, 2, R>(p, BH, st);
+    case 24: return dispatch_gs<D, 2, 4, R>(p, BH, st);
+    case 42: return dispatch_gs<D, 4, 2, R>(p, BH, st);
+    case 44: return dispatch_gs<D, 4, 4, R>(p, BH, st);
+    case 32: return dispatch_gs<D, 3, 2, R>(p, BH, st);
+    case 34: return dispatch_gs<D, 3, 4, R>(p, BH, st);
+    default: return 0;
   }
 }
 
 }  // namespace
 
-int mma_splits(int BH, int64_t groups_total) {
-  // ~8 waves of (148 SMs x 3 CTAs), at least one Key group per warp; the cap depends on
-  // (B, H) only so the scratch size never depends on the token count.
-  const int cap = std::max(1, std::min(512, (8 * 3 * num_sms() + BH - 1) / std::max(1, BH)));
-  const int64_t by_len = std::max<int64_t>(1, (groups_total + kMmaWarps - 1) / kMmaWarps);
-  return (int)std::min<int64_t>(cap, by_len);
-}
 
 bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
                 Workspace& ws, cudaStream_t st) {
@@ -838,8 +887,6 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.T = T;
   p.P = (std::min(c->k.quantized, c->v.quantized) / gs) * gs;
   p.groups_total = (T + gs - 1) / gs;
-  const int nsplit = mma_splits(BH, p.groups_total);
-  p.chunk_groups = (int)((p.groups_total + nsplit - 1) / nsplit);
   p.kt_bytes = (uint32_t)((gs / 16) * c->k.tile_words * 4);
   p.vt_bytes = (uint32_t)((gs / 16) * c->v.tile_words * 4);
   p.vm_bytes = (uint32_t)(gs * p.cg * 4);
@@ -849,22 +896,22 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   // ring depth: ~9 KB in flight per warp, 2..4 stages
   p.stages = (int)std::max<uint32_t>(2, std::min<uint32_t>(4, 9216 / p.stage_bytes));
   p.inv = 1.0f / sqrtf((float)D);
-  const int cap_splits = mma_splits(BH, (int64_t)1 << 40);
+  const int cap_splits = split_cap(BH);
   p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
   p.part_acc = ws.acc(st, (size_t)BH * cap_splits * rows * D);
   p.part_cs = ws.cs(st, (size_t)BH * cap_splits + 1);
   const int R = rows <= 1 ? 1 : rows <= 2 ? 2 : 4;
-  bool ok = false;
+  int nsplit = 0;
 #define KVB_DISPATCH_D(DD)                                                  \
   if (D == DD) {                                                            \
-    if (R == 1) ok = dispatch_bits<DD, 1>(p, kb, vb, nsplit, BH, st);      \
-    else if (R == 2) ok = dispatch_bits<DD, 2>(p, kb, vb, nsplit, BH, st); \
-    else ok = dispatch_bits<DD, 4>(p, kb, vb, nsplit, BH, st);             \
+    if (R == 1) nsplit = dispatch_bits<DD, 1>(p, kb, vb, BH, st);          \
+    else if (R == 2) nsplit = dispatch_bits<DD, 2>(p, kb, vb, BH, st);     \
+    else nsplit = dispatch_bits<DD, 4>(p, kb, vb, BH, st);                 \
   }
   KVB_DISPATCH_D(64)
   KVB_DISPATCH_D(128)
 #undef KVB_DISPATCH_D
-  if (!ok) return false;
+  if (nsplit == 0) return false;
   after_launch("attend_mma_kernel");
   attend_combine_kernel<<<dim3(BH, rows), 128, 0, st>>>(p.part_ml, p.part_acc, nsplit, rows, c->H, Hq, tq, D, out);
   after_launch("attend_combine_kernel");
