@@ -670,7 +670,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < LC; ++c) acct[r][c] = 0.f;
-  const int64_t j_lo = max(g_beg * gs, p.P), j_hi = min(g_end * (int64_t)gs, p.T);
+  // spread over every CTA of this (b, kv-head) so no split becomes a straggler
+  const int64_t j_lo = p.P + (int64_t)split * kMmaWarps, j_hi = p.T;
+  const int64_t j_step = (int64_t)nsplit * kMmaWarps;
   if (j_lo + warp < j_hi) {
     float m_all[R], l_all[R];
     {
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams
       }
     }
     const int d0 = lane * LC;
-    for (int64_t j = j_lo + warp; j < j_hi; j += kMmaWarps) {
+    for (int64_t j = j_lo + warp; j < j_hi; j += j_step) {
       float kx[LC], vx[LC];
       if (j >= p.k.quantized) {
 #pragma unroll
