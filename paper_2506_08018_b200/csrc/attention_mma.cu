@@ -267,7 +267,7 @@ struct WarpLayout {
 
 // GS: 0 = runtime group size, else compile-time (32 is the KVmix default).
 template <int D, int KB, int VB, int R, int GS>
-__global__ void __launch_bounds__(kMmaWarps * 32, 3) attend_mma_kernel(MmaParams p) {
+__global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams p) {
   constexpr int NS = D / 16;                   // k-steps (Keys) / m-tiles (Values)
   constexpr int KW = lane_words<D, KB>();      // words per lane, Key tile
   constexpr int VW = lane_words<D, VB>();      // words per lane, Value tile
