@@ -796,8 +796,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
 // kernel's real residency (occupancy query), with at least two groups per warp; bounded by
 // a cap that depends on (B, H) only, so scratch never depends on the token count.
 int split_cap(int BH) {
-  // up to ~16 waves of 3 CTAs/SM; depends on (B, H) only
-  return std::max(1, std::min(512, (16 * 3 * num_sms() + BH - 1) / std::max(1, BH)));
+  // up to ~16 waves of 4 CTAs/SM; depends on (B, H) only
+  return std::max(1, std::min(512, (16 * 4 * num_sms() + BH - 1) / std::max(1, BH)));
 }
 
 int pick_splits(int BH, int64_t groups, int slots) {
@@ -822,8 +822,29 @@ template <int D, int KB, int VB, int R, int GS>
 int launch(MmaParams& p, int BH, cudaStream_t st) {
   constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;
-  const size_t smem = (size_t)kMmaWarps * WarpLayout<D, NB, GS ? D / GS : 8>::bytes(p.stages, p.stage_bytes);
+  using WL = WarpLayout<D, NB, GS ? D / GS : 8>;
   auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
+  // ring depth: as many stages (2..4) as fit while keeping the highest CTA residency
+  // the registers allow (4, else 3, else 2 CTAs per SM)
+  static thread_local int static_smem = -1;
+  if (static_smem < 0) {
+    cudaFuncAttributes fa;
+    check_cuda(cudaFuncGetAttributes(&fa, kern), "func attributes");
+    static_smem = (int)fa.sharedSizeBytes;
+  }
+  const size_t fixed = WL::bytes(0, 0);
+  int stages = 2;
+  for (int occ_target = 4; occ_target >= 2; --occ_target) {
+    const long per_cta = 227L * 1024 / occ_target - 1024 - static_smem;
+    const long per_warp = per_cta / kMmaWarps - (long)fixed - 4 * 8 - 128;
+    const long s_fit = per_warp / (long)p.stage_bytes;
+    if (s_fit >= 2) {
+      stages = (int)std::min<long>(4, s_fit);
+      break;
+    }
+  }
+  p.stages = stages;
+  const size_t smem = (size_t)kMmaWarps * WL::bytes(p.stages, p.stage_bytes);
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   static thread_local size_t occ_smem = 0;
   static thread_local int occ = 0;
@@ -895,8 +916,6 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.km_bytes = (uint32_t)(D * 4);
   p.stage_bytes = p.kt_bytes + p.vt_bytes + p.vm_bytes + p.km_bytes;
   if (p.vm_bytes % 16) return false;
-  // ring depth: ~9 KB in flight per warp, 2..4 stages
-  p.stages = (int)std::max<uint32_t>(2, std::min<uint32_t>(4, 9216 / p.stage_bytes));
   p.inv = 1.0f / sqrtf((float)D);
   const int cap_splits = split_cap(BH);
   p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
