@@ -151,7 +151,14 @@ struct Unpacker {
   static constexpr bool kClass = (NS % Cls<B>::SPH) == 0;
   // exponent of the power of two carried by slot s
   __host__ __device__ static constexpr int exp_of_slot(int s) { return kClass ? Cls<B>::off(s % Cls<B>::SPH) : 0; }
+  // slots at offset >= MIN_RAW skip the magic subtraction: A = 1024 + c * 2^off, and the
+  // caller removes 1024 * sum(B) (exact enough once 2^off*c is within ~2^5 of 1024)
+  template <int MIN_RAW>
+  __host__ __device__ static constexpr bool raw_slot(int s) {
+    return B != 3 && kClass && Cls<B>::off(s % Cls<B>::SPH) >= MIN_RAW;
+  }
 
+  template <int MIN_RAW = 99>
   __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
     const int vs = r * NS + s;
     if constexpr (B == 3) {
@@ -187,6 +194,7 @@ struct Unpacker {
           case 6: x = and_or<(MASK << 6)>(src, magic); break;
           default: x = and_or<(MASK << 8)>(src, magic); break;
         }
+        if (Cls<B>::off(p) >= MIN_RAW) return x;
         return h2_sub_magic(x);
       } else {
         return h2_sub_magic(((word >> (B * (vs % SPH))) & MASK) | 0x64006400u);
@@ -251,16 +259,18 @@ __device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, i
 }
 
 // Per-warp shared layout (bytes), dynamic:
-//   ring[S][stage_bytes] | bk[D][NB*8] half | bv[2][8][8][24] half | bp[2][8][24] half |
-//   sd[32][NB*8] float (3-bit Keys only) | bars[S] u64
+//   ring[S][stage_bytes] | bk[D][NB*8] half | { bv[2][CGMAX][16][8] half, bp[2][16][8] half }
+//   aliased with sd[32][NB*8] float (3-bit Keys; dead before the P.V operands are built) |
+//   bars[S] u64. B rows are 16 bytes (8 columns) so ldmatrix.trans yields the fragments.
 template <int D, int NB, int CGMAX>
 struct WarpLayout {
   static constexpr int kBk = D * NB * 8 * 2;
-  static constexpr int kBv = 2 * CGMAX * 8 * 24 * 2;
-  static constexpr int kBp = 2 * 8 * 24 * 2;
+  static constexpr int kBv = 2 * CGMAX * 16 * 8 * 2;
+  static constexpr int kBp = 2 * 16 * 8 * 2;
   static constexpr int kSd = NB > 1 ? 32 * NB * 8 * 4 : 0;
+  static constexpr int kPV = (kBv + kBp) > kSd ? (kBv + kBp) : kSd;  // union
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
-    const size_t n = (size_t)stages * stage_bytes + kBk + kBv + kBp + kSd + (size_t)stages * 8;
+    const size_t n = (size_t)stages * stage_bytes + kBk + kPV + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
   }
 };
@@ -280,6 +290,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   using UK = Unpacker<KB, NS>;
   using UV = Unpacker<VB, NS>;
   static_assert(!K3 || R <= 2, "3-bit Keys support up to 2 query rows per KV head");
+  // bias MMA A operand straight from the staged Value meta rows (16 B = 4 groups per token)
+  constexpr bool kMetaRows = GS != 0 && D / (GS ? GS : 1) == 4;
+  constexpr int KRAW = 6;                    // Key slots at offset >= 6 skip the magic subtraction
+  constexpr int VRAW = kMetaRows ? 6 : 99;   // Value m-tiles at offset >= 6 (needs the scale rows)
 
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float s_m[kMmaWarps][R], s_l[kMmaWarps][R];
@@ -299,15 +313,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
   uint8_t* ring = wbase;
   __half* bk = reinterpret_cast<__half*>(ring + (size_t)S * p.stage_bytes);            // [D][NB*8]
-  __half(*bv)[CGMAX][8][24] = reinterpret_cast<__half(*)[CGMAX][8][24]>(reinterpret_cast<uint8_t*>(bk) + WL::kBk);  // [tile][cg][col][tok]
-  __half(*bp)[8][24] = reinterpret_cast<__half(*)[8][24]>(reinterpret_cast<uint8_t*>(bv) + WL::kBv);          // [tile][col][tok]
-  float* sd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bp) + WL::kBp);      // [32][NB*8]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sd) + WL::kSd);
+  uint8_t* pv = reinterpret_cast<uint8_t*>(bk) + WL::kBk;
+  uint4(*bv)[CGMAX][16] = reinterpret_cast<uint4(*)[CGMAX][16]>(pv);          // [tile][cg][token] -> 8 cols
+  uint4(*bp)[16] = reinterpret_cast<uint4(*)[16]>(pv + WL::kBv);              // [tile][token] -> 8 cols
+  float* sd = reinterpret_cast<float*>(pv);                                    // [32][NB*8] (aliases bv/bp)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pv + WL::kPV);
 
   // zero the B staging (columns of absent query rows must stay 0)
   {
     uint4* z = reinterpret_cast<uint4*>(bk);
-    for (int i = lane; i < (WL::kBk + WL::kBv + WL::kBp) / 16; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = lane; i < (WL::kBk + WL::kPV) / 16; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -385,13 +400,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
 
-  // the k-step of this lane's channels and the power of two its A codes carry
+  // the k-step of this lane's channels, the power of two its A codes carry, and whether
+  // that k-step is a raw slot (magic offset removed through beta)
   float cls_scale = 1.f;
+  bool my_raw = false;
   {
     const int kk = (lane * LC) / 16;
 #pragma unroll
-    for (int x = 0; x < NS; ++x)
-      if (x == kk) cls_scale = pow2i(-UK::exp_of_slot(x));
+    for (int x = 0; x < NS; ++x) {
+      if (x == kk) {
+        cls_scale = pow2i(-UK::exp_of_slot(x));
+        my_raw = UK::template raw_slot<KRAW>(x);
+      }
+    }
   }
 
   int s = 0;
@@ -442,20 +463,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         }
         // max over the warp on the (non-negative) float bits: one REDUX
         const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
         // sigma = 2^(14 - floor(log2 max|qs|)): max|qs*sigma| in [2^14, 2^15)
         const int e = (int)((mxu >> 23) & 0xffu);
         const int se = min(max(268 - e, 1), 254);
-        inv_sig[r] = __int_as_float((254 - se) << 23);
-        beta[r] = bt;
+        const float isg = __int_as_float((254 - se) << 23);
+        inv_sig[r] = isg;
         const float sgc = __int_as_float(se << 23) * cls_scale;
+        float off = 0.f;  // 1024 * sum(B) of this lane's raw-slot channels
 #pragma unroll
         for (int c = 0; c < LC; ++c) {
           const float x = qs[c] * sgc;
           const __half hi = __float2half_rn(x);
           const __half lo = __float2half_rn(x - __half2float(hi));
           row[c][r] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+          off += __half2float(hi) + __half2float(lo);
           if constexpr (K3) {
             const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc;
             const __half yh = __float2half_rn(y);
@@ -465,6 +486,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
             for (int xr = 0; xr < 11; ++xr) row[c][R + r * 11 + xr] = tau[c] == xr ? yp : 0u;
           }
         }
+        // beta - (1024 * sum_raw B) / sigma, reduced over the warp in one chain
+        bt -= my_raw ? off * 1024.f * isg : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
+        beta[r] = bt;
       }
       __syncwarp();  // previous group's ldmatrix reads of bk are done
 #pragma unroll
@@ -513,8 +539,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
           ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB * 8 + nb * 8);
 #pragma unroll
           for (int u = 0; u < 2; ++u)
-            mma16816(dk[u][nb], UK::frag(kw[u], 0, kk), UK::frag(kw[u], 1, kk), UK::frag(kw[u], 2, kk),
-                     UK::frag(kw[u], 3, kk), b0, b1);
+            mma16816(dk[u][nb], UK::template frag<KRAW>(kw[u], 0, kk), UK::template frag<KRAW>(kw[u], 1, kk),
+                     UK::template frag<KRAW>(kw[u], 2, kk), UK::template frag<KRAW>(kw[u], 3, kk), b0, b1);
         }
       }
       float sa[2], sb[2];  // row t: token g / token g+8 of each tile
@@ -572,13 +598,25 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       rescale(alpha);
 
       // ---- P.V B operands: lane j -> token j of the 32 (tile j/16, row-in-tile j%16) ----
+      // each (token, group) row is 8 fp16 columns {hi_r, lo_r}: one 16-byte store per row
       {
         const int u = lane >> 4, i = lane & 15;
         const uint32_t* vmt = vm + (size_t)(tp * 16 + lane) * CG;  // this token's Value meta
-        float vsc[GS ? D / GS : 8];
+        float vsc[CGMAX];
+        if constexpr (kMetaRows) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(vmt);
+          vsc[0] = meta_scale(q4.x);
+          vsc[1] = meta_scale(q4.y);
+          vsc[2] = meta_scale(q4.z);
+          vsc[3] = meta_scale(q4.w);
+        } else {
 #pragma unroll
-        for (int c = 0; c < (GS ? D / GS : 8); ++c)
-          if (GS || c < CG) vsc[c] = meta_scale(vmt[c]);
+          for (int c = 0; c < CGMAX; ++c) vsc[c] = (GS || c < CG) ? meta_scale(vmt[c]) : 0.f;
+        }
+        uint32_t prow[4] = {0u, 0u, 0u, 0u};
+        uint32_t vrow[CGMAX][4];
+#pragma unroll
+        for (int c = 0; c < CGMAX; ++c) vrow[c][0] = vrow[c][1] = vrow[c][2] = vrow[c][3] = 0u;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int src = (i & 7) * 4 + r;
@@ -586,56 +624,60 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
           const float x1 = __shfl_sync(0xffffffffu, pb[0], src);
           const float x2 = __shfl_sync(0xffffffffu, pa[1], src);
           const float x3 = __shfl_sync(0xffffffffu, pb[1], src);
-          const float pj = u == 0 ? (i < 8 ? x0 : x1) : (i < 8 ? x2 : x3);
-          if (r < p.rows) {
-            const __half hi = __float2half_rn(pj);
-            bp[u][2 * r][i] = hi;
-            bp[u][2 * r + 1][i] = __float2half_rn(pj - __half2float(hi));
+          const float pj = u == 0 ? (i < 8 ? x0 : x1) : (i < 8 ? x2 : x3);  // 0 for absent rows
+          const __half hi = __float2half_rn(pj);
+          prow[r] = (uint32_t)__half_as_ushort(hi) |
+                    ((uint32_t)__half_as_ushort(__float2half_rn(pj - __half2float(hi))) << 16);
 #pragma unroll
-            for (int c = 0; c < (GS ? D / GS : 8); ++c) {
-              if (GS || c < CG) {
-                const float x = pj * vsc[c];
-                const __half xh = __float2half_rn(x);
-                bv[u][c][2 * r][i] = xh;
-                bv[u][c][2 * r + 1][i] = __float2half_rn(x - __half2float(xh));
-              }
-            }
+          for (int c = 0; c < CGMAX; ++c) {
+            const float x = pj * vsc[c];
+            const __half xh = __float2half_rn(x);
+            vrow[c][r] = (uint32_t)__half_as_ushort(xh) |
+                         ((uint32_t)__half_as_ushort(__float2half_rn(x - __half2float(xh))) << 16);
           }
         }
+        bp[u][i] = make_uint4(prow[0], prow[1], prow[2], prow[3]);
+#pragma unroll
+        for (int c = 0; c < CGMAX; ++c)
+          if (GS || c < CG) bv[u][c][i] = make_uint4(vrow[c][0], vrow[c][1], vrow[c][2], vrow[c][3]);
       }
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const uint32_t* vmt = vm + (size_t)(tp + u) * 16 * CG;  // [16][CG]
-        // bias MMA: A = Value mins [group][token] (rows >= CG are zero), B = p
+        uint32_t pb0, pb1;
+        ldmatrix_x2_trans(pb0, pb1, &bp[u][lane & 15]);
+        // bias MMA: A rows = per-token meta halves, B = p
         uint32_t a0 = 0u, a2 = 0u;
-        if (g < CG) {
-          a0 = __byte_perm(vmt[(2 * t) * CG + g], vmt[(2 * t + 1) * CG + g], 0x7632);
-          a2 = __byte_perm(vmt[(2 * t + 8) * CG + g], vmt[(2 * t + 9) * CG + g], 0x7632);
+        if constexpr (kMetaRows) {
+          // rows = {s0, m0, s1, m1, s2, m2, s3, m3} of the 16 tokens (ldmatrix.trans of the
+          // staged 16-byte meta rows): odd rows give sum_j m_jg p_j, even rows sum_j s_jg p_j
+          ldmatrix_x2_trans(a0, a2, vm + (size_t)((tp + u) * 16 + (lane & 15)) * CG);
+        } else {
+          const uint32_t* vmt = vm + (size_t)(tp + u) * 16 * CG;  // [16][CG]
+          if (g < CG) {
+            a0 = __byte_perm(vmt[(2 * t) * CG + g], vmt[(2 * t + 1) * CG + g], 0x7632);
+            a2 = __byte_perm(vmt[(2 * t + 8) * CG + g], vmt[(2 * t + 9) * CG + g], 0x7632);
+          }
         }
-        mma16816(accb, a0, 0u, a2, 0u, *reinterpret_cast<const uint32_t*>(&bp[u][g][2 * t]),
-                 *reinterpret_cast<const uint32_t*>(&bp[u][g][2 * t + 8]));
+        mma16816(accb, a0, 0u, a2, 0u, pb0, pb1);
         if constexpr (GS != 0) {
           constexpr int CGC = D / GS;
           uint32_t bf0[CGC], bf1[CGC];
 #pragma unroll
-          for (int c = 0; c < CGC; ++c) {
-            bf0[c] = *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t]);
-            bf1[c] = *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t + 8]);
-          }
+          for (int c = 0; c < CGC; ++c) ldmatrix_x2_trans(bf0[c], bf1[c], &bv[u][c][lane & 15]);
 #pragma unroll
           for (int mt = 0; mt < NS; ++mt) {
             const int c = (mt * 16) / GS;
-            mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
-                     UV::frag(vw[u], 3, mt), bf0[c], bf1[c]);
+            mma16816(accv[mt], UV::template frag<VRAW>(vw[u], 0, mt), UV::template frag<VRAW>(vw[u], 1, mt),
+                     UV::template frag<VRAW>(vw[u], 2, mt), UV::template frag<VRAW>(vw[u], 3, mt), bf0[c], bf1[c]);
           }
         } else {
 #pragma unroll
           for (int mt = 0; mt < NS; ++mt) {
-            const int c = cg_of[mt];
+            uint32_t b0, b1;
+            ldmatrix_x2_trans(b0, b1, &bv[u][cg_of[mt]][lane & 15]);
             mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
-                     UV::frag(vw[u], 3, mt), *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t]),
-                     *reinterpret_cast<const uint32_t*>(&bv[u][c][g][2 * t + 8]));
+                     UV::frag(vw[u], 3, mt), b0, b1);
           }
         }
       }
@@ -652,6 +694,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
 
+  // raw Value m-tiles carry 1024 * sum_j B_j(group): taken from the scale rows of the bias
+  // MMA (even rows 2c hold sum_j s_jc p_j, split over the hi/lo columns)
+  if constexpr (kMetaRows) {
+    const float srow = accb[0] + accb[1];
+#pragma unroll
+    for (int mt = 0; mt < NS; ++mt) {
+      if (UV::template raw_slot<VRAW>(mt)) {
+        const int c = (mt * 16) / GS;
+        const float sc = __shfl_sync(0xffffffffu, srow, (2 * c) * 4 + t);  // row 2c, this thread's columns
+        const float o = 1024.f * sc;
+        // the offset sits in the hi column sum; subtract it once from (hi + lo)
+        accv[mt][0] -= o;
+        accv[mt][2] -= o;
+      }
+    }
+  }
   // undo the per-m-tile power of two carried by the Value codes
 #pragma unroll
   for (int mt = 0; mt < NS; ++mt) {
@@ -750,7 +808,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       s_acc[warp][t][mt * 16 + g] = accv[mt][0] + accv[mt][1];
       s_acc[warp][t][mt * 16 + g + 8] = accv[mt][2] + accv[mt][3];
     }
-    s_bias[warp][t][g] = accb[0] + accb[1];
+    if constexpr (kMetaRows) {
+      if (g & 1) s_bias[warp][t][g >> 1] = accb[0] + accb[1];  // min rows
+    } else {
+      s_bias[warp][t][g] = accb[0] + accb[1];
+    }
   }
   __syncwarp();
 #pragma unroll
