@@ -249,26 +249,45 @@ struct MmaParams {
   uint32_t kt_bytes, vt_bytes, vm_bytes, km_bytes;  // per-group copy sizes
   uint32_t stage_bytes;
   float inv;  // 1/sqrt(D)
+  int want_cs;  // accumulate the double scores checksum (only when the caller asks)
   float2* part_ml;
   float* part_acc;
   double* part_cs;
 };
+
+// Dequantized packed element (token j < quantized, channel d) with compile-time D (gs is a
+// compile-time constant too when the kernel is instantiated with GS): the tail path's
+// per-element cost without runtime divisions.
+template <int D, bool KEY>
+__device__ __forceinline__ float deq_lane(const SideView& s, int bh, int j, int d, int gs) {
+  const uint32_t* tile = s.tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
+  const uint32_t code = tile_get(tile, KEY ? key_coord(j & 15, d) : value_coord(j & 15, d), D, s.bits);
+  uint32_t m;
+  bool narrow = false;
+  if (KEY) {
+    const int grp = j / gs;
+    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)grp * D + d];
+    if (s.bits == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
+  } else {
+    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)j * ((D + gs - 1) / gs) + d / gs];
+    if (s.bits == 3) narrow = narrow_value(bh, d, D, s.info[j]);
+  }
+  return decode(code, meta_scale(m), meta_min(m), narrow);
+}
 
 __device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, int64_t j, int d, int D) {
   return f16 ? tail_at<__half>(s, bh, j, d, D) : tail_at<float>(s, bh, j, d, D);
 }
 
 // Per-warp shared layout (bytes), dynamic:
-//   ring[S][stage_bytes] | bk[D][NB*8] half | { bv[2][CGMAX][16][8] half, bp[2][16][8] half }
-//   aliased with sd[32][NB*8] float (3-bit Keys; dead before the P.V operands are built) |
+//   ring[S][stage_bytes] | bk[D][NB*8] half | bv[2][CGMAX][16][8] half | bp[2][16][8] half |
 //   bars[S] u64. B rows are 16 bytes (8 columns) so ldmatrix.trans yields the fragments.
 template <int D, int NB, int CGMAX>
 struct WarpLayout {
   static constexpr int kBk = D * NB * 8 * 2;
   static constexpr int kBv = 2 * CGMAX * 16 * 8 * 2;
   static constexpr int kBp = 2 * 16 * 8 * 2;
-  static constexpr int kSd = NB > 1 ? 32 * NB * 8 * 4 : 0;
-  static constexpr int kPV = (kBv + kBp) > kSd ? (kBv + kBp) : kSd;  // union
+  static constexpr int kPV = kBv + kBp;
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
     const size_t n = (size_t)stages * stage_bytes + kBk + kPV + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
@@ -316,7 +335,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   uint8_t* pv = reinterpret_cast<uint8_t*>(bk) + WL::kBk;
   uint4(*bv)[CGMAX][16] = reinterpret_cast<uint4(*)[CGMAX][16]>(pv);          // [tile][cg][token] -> 8 cols
   uint4(*bp)[16] = reinterpret_cast<uint4(*)[16]>(pv + WL::kBv);              // [tile][token] -> 8 cols
-  float* sd = reinterpret_cast<float*>(pv);                                    // [32][NB*8] (aliases bv/bp)
   uint64_t* bars = reinterpret_cast<uint64_t*>(pv + WL::kPV);
 
   // zero the B staging (columns of absent query rows must stay 0)
@@ -545,26 +563,32 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       }
       float sa[2], sb[2];  // row t: token g / token g+8 of each tile
       if constexpr (K3) {
-        // residue-class corrections: dump the fragments, pick each token's residue column
+        // residue-class corrections without shared memory: for token row x the column pair
+        // of residue class (tile*16 + row) % 11 lives in lane (row, t_src); every lane of
+        // row `g` computes the same source, so the source lane itself knows which register
+        // block to expose, and one shuffle per (row, query row) delivers it.
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) {
-            *reinterpret_cast<float2*>(&sd[(u * 16 + g) * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[u][nb][0], dk[u][nb][1]);
-            *reinterpret_cast<float2*>(&sd[(u * 16 + g + 8) * NB * 8 + nb * 8 + 2 * t]) = make_float2(dk[u][nb][2], dk[u][nb][3]);
+          for (int hlf = 0; hlf < 2; ++hlf) {  // token g, then token g+8
+            const int x = ((tp + u) * 16 + g + 8 * hlf) % 11;
+            float tot = 0.f;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int col = 2 * R + (r * 11 + x) * 2;     // even: hi, odd: lo
+              const int nb = col >> 3, tsrc = (col & 7) >> 1;
+              float mine = 0.f;                              // this lane's (hi+lo) in block nb
+#pragma unroll
+              for (int q = 0; q < NB; ++q)
+                if (q == nb) mine = dk[u][q][2 * hlf] + dk[u][q][2 * hlf + 1];
+              const float corr = __shfl_sync(0xffffffffu, mine, g * 4 + tsrc);
+              if (r == t) tot = corr;
+            }
+            const float mainv = dk[u][0][2 * hlf] + dk[u][0][2 * hlf + 1];
+            if (hlf == 0) sa[u] = mainv + tot;
+            else sb[u] = mainv + tot;
           }
         }
-        __syncwarp();
-        const int rr = t < R ? t : 0;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int xa = ((tp + u) * 16 + g) % 11, xb = ((tp + u) * 16 + g + 8) % 11;
-          const float* ra = sd + (u * 16 + g) * NB * 8;
-          const float* rb = sd + (u * 16 + g + 8) * NB * 8;
-          sa[u] = ra[2 * rr] + ra[2 * rr + 1] + ra[2 * R + (rr * 11 + xa) * 2] + ra[2 * R + (rr * 11 + xa) * 2 + 1];
-          sb[u] = rb[2 * rr] + rb[2 * rr + 1] + rb[2 * R + (rr * 11 + xb) * 2] + rb[2 * R + (rr * 11 + xb) * 2 + 1];
-        }
-        __syncwarp();
       } else {
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -580,7 +604,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         la[u] = sa[u] * kLog2e;
         lb[u] = sb[u] * kLog2e;
       }
-      if (row_ok) cs += (double)((sa[0] + sb[0]) + (sa[1] + sb[1]));
+      if (p.want_cs && row_ok) cs += (double)((sa[0] + sb[0]) + (sa[1] + sb[1]));
       float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
@@ -752,14 +776,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         for (int c = 0; c < LC; ++c) kx[c] = tail_val(p.k, p.tail16, bh, j - p.k.quantized, d0 + c, D);
       } else {
 #pragma unroll
-        for (int c = 0; c < LC; ++c) kx[c] = packed_value(true, p.k, bh, j, d0 + c, D, gs);
+        for (int c = 0; c < LC; ++c) kx[c] = deq_lane<D, true>(p.k, bh, (int)j, d0 + c, gs);
       }
       if (j >= p.v.quantized) {
 #pragma unroll
         for (int c = 0; c < LC; ++c) vx[c] = tail_val(p.v, p.tail16, bh, j - p.v.quantized, d0 + c, D);
       } else {
 #pragma unroll
-        for (int c = 0; c < LC; ++c) vx[c] = packed_value(false, p.v, bh, j, d0 + c, D, gs);
+        for (int c = 0; c < LC; ++c) vx[c] = deq_lane<D, false>(p.v, bh, (int)j, d0 + c, gs);
       }
       float alpha_mine = 1.f;
 #pragma unroll
@@ -771,7 +795,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         if (r < p.rows) {
           const float sc = x * p.inv;
-          if (lane == 0) cs += (double)sc;
+          if (p.want_cs && lane == 0) cs += (double)sc;
           const float ls = sc * kLog2e;
           const float m_new = fmaxf(m_all[r], ls);
           const float alpha = exp2f(m_all[r] - m_new);
@@ -822,7 +846,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       for (int c = 0; c < LC; ++c) s_acc[warp][r][lane * LC + c] += acct[r][c];
     }
   }
-  for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+  if (p.want_cs) {
+    for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+  }
   if (lane == 0) s_cs[warp] = cs;
   __syncthreads();
 
@@ -979,6 +1005,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.stage_bytes = p.kt_bytes + p.vt_bytes + p.vm_bytes + p.km_bytes;
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
+  p.want_cs = checksum != nullptr;
   const int cap_splits = split_cap(BH);
   p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
   p.part_acc = ws.acc(st, (size_t)BH * cap_splits * rows * D);
