@@ -237,6 +237,24 @@ constexpr int lane_words() {
 
 __device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }
 
+// 2^x via MUFU.EX2 without the denormal fix-up (x <= 0 here; 2^x < 2^-126 flushes to 0)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// (hi, lo) fp16 split of x packed as {hi | lo << 16}: x ~= hi + lo to ~22 bits. Two values
+// at a time through the packed converter (F2FP) instead of four scalar F2F on the XU pipe.
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& p0, uint32_t& p1) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  const uint32_t hu = *reinterpret_cast<const uint32_t*>(&h), lu = *reinterpret_cast<const uint32_t*>(&l);
+  p0 = __byte_perm(hu, lu, 0x5410);
+  p1 = __byte_perm(hu, lu, 0x7632);
+}
+
 struct MmaParams {
   SideView k, v;
   const void* q;
@@ -258,19 +276,19 @@ struct MmaParams {
 // Dequantized packed element (token j < quantized, channel d) with compile-time D (gs is a
 // compile-time constant too when the kernel is instantiated with GS): the tail path's
 // per-element cost without runtime divisions.
-template <int D, bool KEY>
+template <int D, bool KEY, int BITS>
 __device__ __forceinline__ float deq_lane(const SideView& s, int bh, int j, int d, int gs) {
   const uint32_t* tile = s.tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
-  const uint32_t code = tile_get(tile, KEY ? key_coord(j & 15, d) : value_coord(j & 15, d), D, s.bits);
+  const uint32_t code = tile_get(tile, KEY ? key_coord(j & 15, d) : value_coord(j & 15, d), D, BITS);
   uint32_t m;
   bool narrow = false;
   if (KEY) {
     const int grp = j / gs;
     m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)grp * D + d];
-    if (s.bits == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
+    if (BITS == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
   } else {
     m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)j * ((D + gs - 1) / gs) + d / gs];
-    if (s.bits == 3) narrow = narrow_value(bh, d, D, s.info[j]);
+    if (BITS == 3) narrow = narrow_value(bh, d, D, s.info[j]);
   }
   return decode(code, meta_scale(m), meta_min(m), narrow);
 }
@@ -489,13 +507,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         const float sgc = __int_as_float(se << 23) * cls_scale;
         float off = 0.f;  // 1024 * sum(B) of this lane's raw-slot channels
 #pragma unroll
-        for (int c = 0; c < LC; ++c) {
-          const float x = qs[c] * sgc;
-          const __half hi = __float2half_rn(x);
-          const __half lo = __float2half_rn(x - __half2float(hi));
-          row[c][r] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
-          off += __half2float(hi) + __half2float(lo);
-          if constexpr (K3) {
+        for (int c = 0; c < LC; c += 2) {
+          const float x0 = qs[c] * sgc, x1 = qs[c + 1] * sgc;
+          split2(x0, x1, row[c][r], row[c + 1][r]);
+          off += x0 + x1;  // == sum of the hi+lo pairs to ~2^-22
+        }
+        if constexpr (K3) {
+#pragma unroll
+          for (int c = 0; c < LC; ++c) {
             const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc;
             const __half yh = __float2half_rn(y);
             const __half yl = __float2half_rn(y - __half2float(yh));
@@ -544,22 +563,32 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         lds_tile<VB, D>(vt + (size_t)(tp + u) * tile_words(D, VB), lane, vw[u]);
       }
       // scores: K (16 tokens x D) . B, both tiles
-      float dk[2][NB][4];
+      // NB == 1: two accumulator chains per tile (even/odd k-steps) halve the HMMA
+      // dependency chain; NB > 1 already has NB independent chains
+      constexpr int NCH = NB == 1 ? 2 : 1;
+      float dk[2][NB * NCH][4];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dk[u][nb][0] = dk[u][nb][1] = dk[u][nb][2] = dk[u][nb][3] = 0.f;
+        for (int nb = 0; nb < NB * NCH; ++nb) dk[u][nb][0] = dk[u][nb][1] = dk[u][nb][2] = dk[u][nb][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < NS; ++kk) {
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
           uint32_t b0, b1;
           ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB * 8 + nb * 8);
+          const int acc = NCH == 2 ? (kk & 1) : nb;
 #pragma unroll
           for (int u = 0; u < 2; ++u)
-            mma16816(dk[u][nb], UK::template frag<KRAW>(kw[u], 0, kk), UK::template frag<KRAW>(kw[u], 1, kk),
+            mma16816(dk[u][acc], UK::template frag<KRAW>(kw[u], 0, kk), UK::template frag<KRAW>(kw[u], 1, kk),
                      UK::template frag<KRAW>(kw[u], 2, kk), UK::template frag<KRAW>(kw[u], 3, kk), b0, b1);
         }
+      }
+      if constexpr (NCH == 2) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dk[u][0][e] += dk[u][1][e];
       }
       float sa[2], sb[2];  // row t: token g / token g+8 of each tile
       if constexpr (K3) {
@@ -610,12 +639,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
       tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
       const float m_new = fmaxf(m_run, tmax);
-      const float alpha = exp2f(m_run - m_new);
+      const float alpha = fast_exp2(m_run - m_new);
       float pa[2], pb[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        pa[u] = row_ok ? exp2f(la[u] - m_new) : 0.f;
-        pb[u] = row_ok ? exp2f(lb[u] - m_new) : 0.f;
+        pa[u] = row_ok ? fast_exp2(la[u] - m_new) : 0.f;
+        pb[u] = row_ok ? fast_exp2(lb[u] - m_new) : 0.f;
       }
       l_run = l_run * alpha + ((pa[0] + pb[0]) + (pa[1] + pb[1]));
       m_run = m_new;
@@ -649,16 +678,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
           const float x2 = __shfl_sync(0xffffffffu, pa[1], src);
           const float x3 = __shfl_sync(0xffffffffu, pb[1], src);
           const float pj = u == 0 ? (i < 8 ? x0 : x1) : (i < 8 ? x2 : x3);  // 0 for absent rows
-          const __half hi = __float2half_rn(pj);
-          prow[r] = (uint32_t)__half_as_ushort(hi) |
-                    ((uint32_t)__half_as_ushort(__float2half_rn(pj - __half2float(hi))) << 16);
+          float xs[CGMAX + 1];
+          xs[0] = pj;
 #pragma unroll
-          for (int c = 0; c < CGMAX; ++c) {
-            const float x = pj * vsc[c];
-            const __half xh = __float2half_rn(x);
-            vrow[c][r] = (uint32_t)__half_as_ushort(xh) |
-                         ((uint32_t)__half_as_ushort(__float2half_rn(x - __half2float(xh))) << 16);
-          }
+          for (int c = 0; c < CGMAX; ++c) xs[c + 1] = pj * vsc[c];
+          uint32_t pk[CGMAX + 2];
+#pragma unroll
+          for (int c = 0; c < CGMAX + 1; c += 2) split2(xs[c], c + 1 <= CGMAX ? xs[c + 1] : 0.f, pk[c], pk[c + 1]);
+          prow[r] = pk[0];
+#pragma unroll
+          for (int c = 0; c < CGMAX; ++c) vrow[c][r] = pk[c + 1];
         }
         bp[u][i] = make_uint4(prow[0], prow[1], prow[2], prow[3]);
 #pragma unroll
@@ -776,14 +805,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         for (int c = 0; c < LC; ++c) kx[c] = tail_val(p.k, p.tail16, bh, j - p.k.quantized, d0 + c, D);
       } else {
 #pragma unroll
-        for (int c = 0; c < LC; ++c) kx[c] = deq_lane<D, true>(p.k, bh, (int)j, d0 + c, gs);
+        for (int c = 0; c < LC; ++c) kx[c] = deq_lane<D, true, KB>(p.k, bh, (int)j, d0 + c, gs);
       }
       if (j >= p.v.quantized) {
 #pragma unroll
         for (int c = 0; c < LC; ++c) vx[c] = tail_val(p.v, p.tail16, bh, j - p.v.quantized, d0 + c, D);
       } else {
 #pragma unroll
-        for (int c = 0; c < LC; ++c) vx[c] = deq_lane<D, false>(p.v, bh, (int)j, d0 + c, gs);
+        for (int c = 0; c < LC; ++c) vx[c] = deq_lane<D, false, VB>(p.v, bh, (int)j, d0 + c, gs);
       }
       float alpha_mine = 1.f;
 #pragma unroll
