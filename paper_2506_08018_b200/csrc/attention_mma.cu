@@ -102,22 +102,6 @@ __device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, co
                : "r"(smem_u32(row_addr)));
 }
 
-// (a & MASK) | c in one LOP3 (MASK as the immediate, the 0x6400 magic in a register)
-template <uint32_t MASK>
-__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
-  return d;
-}
-
-__device__ __forceinline__ uint32_t h2_sub_magic(uint32_t x) {
-  // (1024 + v_lo, 1024 + v_hi) - 1024 -> exact (v_lo, v_hi)
-  __half2 v = *reinterpret_cast<__half2*>(&x);
-  const __half2 m = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
-  v = __hsub2(v, m);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
 // ---- unpack ---------------------------------------------------------------------------
 // Slots per 16-bit half: 16/B. With the class trick slot position p lives at bit offset
 // off(p) of either w (low positions) or w >> SH (high positions), giving value c * 2^off.
@@ -149,16 +133,15 @@ template <int B, int NS>
 struct Unpacker {
   // class trick valid iff the offset depends on the slot only: NS % SPH == 0
   static constexpr bool kClass = (NS % Cls<B>::SPH) == 0;
-  // exponent of the power of two carried by slot s
+  // exponent of the power of two carried by slot s (the bit offset of its codes)
   __host__ __device__ static constexpr int exp_of_slot(int s) { return kClass ? Cls<B>::off(s % Cls<B>::SPH) : 0; }
-  // slots at offset >= MIN_RAW skip the magic subtraction: A = 1024 + c * 2^off, and the
-  // caller removes 1024 * sum(B) (exact enough once 2^off*c is within ~2^5 of 1024)
-  template <int MIN_RAW>
-  __host__ __device__ static constexpr bool raw_slot(int s) {
-    return B != 3 && kClass && Cls<B>::off(s % Cls<B>::SPH) >= MIN_RAW;
-  }
 
-  template <int MIN_RAW = 99>
+  // Fragment register r at slot s: the two codes masked in place, read by the tensor core
+  // as fp16 SUBNORMALS (exponent field 0), i.e. exactly c * 2^(off - 24). HMMA consumes fp16
+  // subnormal inputs exactly (probed on B200: profiles/probes/hmma_subnormal.cu), so no
+  // magic-number OR / subtraction is needed: one LOP3 per register (plus one shift per
+  // word for the slots above bit 9). The 2^(off - 24) is undone per Key channel (B operand)
+  // and per Value m-tile (accumulator).
   __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
     const int vs = r * NS + s;
     if constexpr (B == 3) {
@@ -169,14 +152,13 @@ struct Unpacker {
         const int p = vs & 7;
         const int o = Cls<3>::off(p);
         const uint32_t lw = p < Cls<3>::split() ? w[vs >> 3] : (w[vs >> 3] >> Cls<3>::sh());
-        const uint32_t lo = lw & (0x00030003u << o);
         const int tgt = o + 2;
         const uint32_t hs = hb >= tgt ? (hw >> (hb - tgt)) : (hw << (tgt - hb));
-        return h2_sub_magic(lo | (hs & (0x00010001u << tgt)) | 0x64006400u);
+        return (lw & (0x00030003u << o)) | (hs & (0x00010001u << tgt));
       } else {
         const uint32_t lo = (w[vs >> 3] >> (2 * (vs & 7))) & 0x00030003u;
         const uint32_t hi = (hw >> hb) & 0x00010001u;
-        return h2_sub_magic(lo | (hi << 2) | 0x64006400u);
+        return lo | (hi << 2);
       }
     } else {
       constexpr int SPH = Cls<B>::SPH;
@@ -185,19 +167,9 @@ struct Unpacker {
       if constexpr (kClass) {
         const int p = vs % SPH;
         const uint32_t src = p < Cls<B>::split() ? word : (word >> Cls<B>::sh());
-        const uint32_t magic = 0x64006400u;
-        uint32_t x;
-        switch (Cls<B>::off(p)) {  // compile-time after unrolling
-          case 0: x = and_or<MASK>(src, magic); break;
-          case 2: x = and_or<(MASK << 2)>(src, magic); break;
-          case 4: x = and_or<(MASK << 4)>(src, magic); break;
-          case 6: x = and_or<(MASK << 6)>(src, magic); break;
-          default: x = and_or<(MASK << 8)>(src, magic); break;
-        }
-        if (Cls<B>::off(p) >= MIN_RAW) return x;
-        return h2_sub_magic(x);
+        return src & (MASK << Cls<B>::off(p));
       } else {
-        return h2_sub_magic(((word >> (B * (vs % SPH))) & MASK) | 0x64006400u);
+        return (word >> (B * (vs % SPH))) & MASK;
       }
     }
   }
@@ -329,8 +301,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   static_assert(!K3 || R <= 2, "3-bit Keys support up to 2 query rows per KV head");
   // bias MMA A operand straight from the staged Value meta rows (16 B = 4 groups per token)
   constexpr bool kMetaRows = GS != 0 && D / (GS ? GS : 1) == 4;
-  constexpr int KRAW = 6;                    // Key slots at offset >= 6 skip the magic subtraction
-  constexpr int VRAW = kMetaRows ? 6 : 99;   // Value m-tiles at offset >= 6 (needs the scale rows)
 
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float s_m[kMmaWarps][R], s_l[kMmaWarps][R];
@@ -436,19 +406,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
 
-  // the k-step of this lane's channels, the power of two its A codes carry, and whether
-  // that k-step is a raw slot (magic offset removed through beta)
+  // the k-step of this lane's channels and the power of two its A codes carry
   float cls_scale = 1.f;
-  bool my_raw = false;
   {
     const int kk = (lane * LC) / 16;
 #pragma unroll
-    for (int x = 0; x < NS; ++x) {
-      if (x == kk) {
-        cls_scale = pow2i(-UK::exp_of_slot(x));
-        my_raw = UK::template raw_slot<KRAW>(x);
-      }
-    }
+    for (int x = 0; x < NS; ++x)
+      if (x == kk) cls_scale = pow2i(-UK::exp_of_slot(x));
   }
 
   int s = 0;
@@ -502,16 +466,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         // sigma = 2^(14 - floor(log2 max|qs|)): max|qs*sigma| in [2^14, 2^15)
         const int e = (int)((mxu >> 23) & 0xffu);
         const int se = min(max(268 - e, 1), 254);
-        const float isg = __int_as_float((254 - se) << 23);
-        inv_sig[r] = isg;
+        inv_sig[r] = __int_as_float((254 + 24 - se) << 23);  // 2^24 / sigma (subnormal A codes)
         const float sgc = __int_as_float(se << 23) * cls_scale;
-        float off = 0.f;  // 1024 * sum(B) of this lane's raw-slot channels
 #pragma unroll
-        for (int c = 0; c < LC; c += 2) {
-          const float x0 = qs[c] * sgc, x1 = qs[c + 1] * sgc;
-          split2(x0, x1, row[c][r], row[c + 1][r]);
-          off += x0 + x1;  // == sum of the hi+lo pairs to ~2^-22
-        }
+        for (int c = 0; c < LC; c += 2) split2(qs[c] * sgc, qs[c + 1] * sgc, row[c][r], row[c + 1][r]);
         if constexpr (K3) {
 #pragma unroll
           for (int c = 0; c < LC; ++c) {
@@ -523,8 +481,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
             for (int xr = 0; xr < 11; ++xr) row[c][R + r * 11 + xr] = tau[c] == xr ? yp : 0u;
           }
         }
-        // beta - (1024 * sum_raw B) / sigma, reduced over the warp in one chain
-        bt -= my_raw ? off * 1024.f * isg : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
         beta[r] = bt;
@@ -580,8 +536,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
           const int acc = NCH == 2 ? (kk & 1) : nb;
 #pragma unroll
           for (int u = 0; u < 2; ++u)
-            mma16816(dk[u][acc], UK::template frag<KRAW>(kw[u], 0, kk), UK::template frag<KRAW>(kw[u], 1, kk),
-                     UK::template frag<KRAW>(kw[u], 2, kk), UK::template frag<KRAW>(kw[u], 3, kk), b0, b1);
+            mma16816(dk[u][acc], UK::frag(kw[u], 0, kk), UK::frag(kw[u], 1, kk), UK::frag(kw[u], 2, kk),
+                     UK::frag(kw[u], 3, kk), b0, b1);
         }
       }
       if constexpr (NCH == 2) {
@@ -721,8 +677,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
 #pragma unroll
           for (int mt = 0; mt < NS; ++mt) {
             const int c = (mt * 16) / GS;
-            mma16816(accv[mt], UV::template frag<VRAW>(vw[u], 0, mt), UV::template frag<VRAW>(vw[u], 1, mt),
-                     UV::template frag<VRAW>(vw[u], 2, mt), UV::template frag<VRAW>(vw[u], 3, mt), bf0[c], bf1[c]);
+            mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
+                     UV::frag(vw[u], 3, mt), bf0[c], bf1[c]);
           }
         } else {
 #pragma unroll
@@ -747,26 +703,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
 
-  // raw Value m-tiles carry 1024 * sum_j B_j(group): taken from the scale rows of the bias
-  // MMA (even rows 2c hold sum_j s_jc p_j, split over the hi/lo columns)
-  if constexpr (kMetaRows) {
-    const float srow = accb[0] + accb[1];
-#pragma unroll
-    for (int mt = 0; mt < NS; ++mt) {
-      if (UV::template raw_slot<VRAW>(mt)) {
-        const int c = (mt * 16) / GS;
-        const float sc = __shfl_sync(0xffffffffu, srow, (2 * c) * 4 + t);  // row 2c, this thread's columns
-        const float o = 1024.f * sc;
-        // the offset sits in the hi column sum; subtract it once from (hi + lo)
-        accv[mt][0] -= o;
-        accv[mt][2] -= o;
-      }
-    }
-  }
-  // undo the per-m-tile power of two carried by the Value codes
+  // undo the per-m-tile 2^(off - 24) carried by the subnormal Value codes
 #pragma unroll
   for (int mt = 0; mt < NS; ++mt) {
-    const float f = pow2i(-UV::exp_of_slot(mt));
+    const float f = pow2i(24 - UV::exp_of_slot(mt));
     accv[mt][0] *= f;
     accv[mt][1] *= f;
     accv[mt][2] *= f;
