@@ -102,6 +102,21 @@ __device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, co
                : "r"(smem_u32(row_addr)));
 }
 
+// (a & MASK) | c in one LOP3 (MASK as the immediate, the magic in a register)
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
+  return d;
+}
+
+// (2^10 + v_lo, 2^10 + v_hi) - 2^10 -> exact (v_lo, v_hi), normal fp16
+__device__ __forceinline__ uint32_t sub_magic(uint32_t x) {
+  __half2 v = *reinterpret_cast<__half2*>(&x);
+  v = __hsub2(v, __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400)));
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 // ---- unpack ---------------------------------------------------------------------------
 // Slots per 16-bit half: 16/B. With the class trick slot position p lives at bit offset
 // off(p) of either w (low positions) or w >> SH (high positions), giving value c * 2^off.
@@ -135,13 +150,20 @@ struct Unpacker {
   static constexpr bool kClass = (NS % Cls<B>::SPH) == 0;
   // exponent of the power of two carried by slot s (the bit offset of its codes)
   __host__ __device__ static constexpr int exp_of_slot(int s) { return kClass ? Cls<B>::off(s % Cls<B>::SPH) : 0; }
+  // Codes at offset >= kSubMin are handed to the tensor core as fp16 SUBNORMALS (exponent
+  // field 0, value c * 2^(off-24), one LOP3): HMMA consumes subnormal inputs exactly but
+  // aligns their products to the nominal 2^-14 exponent, so codes with many leading zeros
+  // lose product bits (profiles/probes/hmma_hilo_prec.cu: 1e-6 vs 2e-8 relative). Low
+  // offsets therefore use the exact magic form (OR 2^10, subtract 2^10 -> c * 2^off,
+  // LOP3 + HADD2), high offsets (>= 4, at most 4 leading zeros) the subnormal form.
+  static constexpr int kSubMin = 4;
+  // power-of-two factor of the operand value relative to the code: 2^(off) or 2^(off-24)
+  __host__ __device__ static constexpr bool is_sub(int s) { return kClass && B != 3 && exp_of_slot(s) >= kSubMin; }
+  __host__ __device__ static constexpr int val_exp_of_slot(int s) { return exp_of_slot(s) - (is_sub(s) ? 24 : 0); }
+  // some slot is subnormal (then the Key GEMV keeps magic and subnormal slots in separate
+  // accumulator chains and joins them as chain_magic + 2^24 * chain_sub)
+  static constexpr bool kHasSub = kClass && B != 3 && Cls<B>::off(Cls<B>::SPH - 1) >= kSubMin;
 
-  // Fragment register r at slot s: the two codes masked in place, read by the tensor core
-  // as fp16 SUBNORMALS (exponent field 0), i.e. exactly c * 2^(off - 24). HMMA consumes fp16
-  // subnormal inputs exactly (probed on B200: profiles/probes/hmma_subnormal.cu), so no
-  // magic-number OR / subtraction is needed: one LOP3 per register (plus one shift per
-  // word for the slots above bit 9). The 2^(off - 24) is undone per Key channel (B operand)
-  // and per Value m-tile (accumulator).
   __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
     const int vs = r * NS + s;
     if constexpr (B == 3) {
@@ -154,11 +176,11 @@ struct Unpacker {
         const uint32_t lw = p < Cls<3>::split() ? w[vs >> 3] : (w[vs >> 3] >> Cls<3>::sh());
         const int tgt = o + 2;
         const uint32_t hs = hb >= tgt ? (hw >> (hb - tgt)) : (hw << (tgt - hb));
-        return (lw & (0x00030003u << o)) | (hs & (0x00010001u << tgt));
+        return sub_magic((lw & (0x00030003u << o)) | (hs & (0x00010001u << tgt)) | 0x64006400u);
       } else {
         const uint32_t lo = (w[vs >> 3] >> (2 * (vs & 7))) & 0x00030003u;
         const uint32_t hi = (hw >> hb) & 0x00010001u;
-        return lo | (hi << 2);
+        return sub_magic(lo | (hi << 2) | 0x64006400u);
       }
     } else {
       constexpr int SPH = Cls<B>::SPH;
@@ -167,9 +189,12 @@ struct Unpacker {
       if constexpr (kClass) {
         const int p = vs % SPH;
         const uint32_t src = p < Cls<B>::split() ? word : (word >> Cls<B>::sh());
-        return src & (MASK << Cls<B>::off(p));
+        const int o = Cls<B>::off(p);
+        if (o >= kSubMin) return src & (MASK << o);  // subnormal operand
+        const uint32_t magic = 0x64006400u;
+        return sub_magic(o == 0 ? and_or<MASK>(src, magic) : and_or<(MASK << 2)>(src, magic));
       } else {
-        return (word >> (B * (vs % SPH))) & MASK;
+        return sub_magic(((word >> (B * (vs % SPH))) & MASK) | 0x64006400u);
       }
     }
   }
@@ -466,7 +491,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         // sigma = 2^(14 - floor(log2 max|qs|)): max|qs*sigma| in [2^14, 2^15)
         const int e = (int)((mxu >> 23) & 0xffu);
         const int se = min(max(268 - e, 1), 254);
-        inv_sig[r] = __int_as_float((254 + 24 - se) << 23);  // 2^24 / sigma (subnormal A codes)
+        inv_sig[r] = __int_as_float((254 - se) << 23);  // 1 / sigma
         const float sgc = __int_as_float(se << 23) * cls_scale;
 #pragma unroll
         for (int c = 0; c < LC; c += 2) split2(qs[c] * sgc, qs[c + 1] * sgc, row[c][r], row[c + 1][r]);
@@ -519,8 +544,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         lds_tile<VB, D>(vt + (size_t)(tp + u) * tile_words(D, VB), lane, vw[u]);
       }
       // scores: K (16 tokens x D) . B, both tiles
-      // NB == 1: two accumulator chains per tile (even/odd k-steps) halve the HMMA
-      // dependency chain; NB > 1 already has NB independent chains
+      // NB == 1: two accumulator chains per tile (magic / subnormal slots, else even / odd
+      // k-steps) halve the HMMA dependency chain; NB > 1 already has NB independent chains
       constexpr int NCH = NB == 1 ? 2 : 1;
       float dk[2][NB * NCH][4];
 #pragma unroll
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
         for (int nb = 0; nb < NB; ++nb) {
           uint32_t b0, b1;
           ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB * 8 + nb * 8);
-          const int acc = NCH == 2 ? (kk & 1) : nb;
+          const int acc = NCH == 2 ? (UK::kHasSub ? (UK::is_sub(kk) ? 1 : 0) : (kk & 1)) : nb;
 #pragma unroll
           for (int u = 0; u < 2; ++u)
             mma16816(dk[u][acc], UK::frag(kw[u], 0, kk), UK::frag(kw[u], 1, kk), UK::frag(kw[u], 2, kk),
@@ -544,7 +569,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) dk[u][0][e] += dk[u][1][e];
+          for (int e = 0; e < 4; ++e) dk[u][0][e] = fmaf(UK::kHasSub ? 16777216.f : 1.f, dk[u][1][e], dk[u][0][e]);
       }
       float sa[2], sb[2];  // row t: token g / token g+8 of each tile
       if constexpr (K3) {
@@ -703,10 +728,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
 
-  // undo the per-m-tile 2^(off - 24) carried by the subnormal Value codes
+  // undo the per-m-tile power of two carried by the Value operands
 #pragma unroll
   for (int mt = 0; mt < NS; ++mt) {
-    const float f = pow2i(24 - UV::exp_of_slot(mt));
+    const float f = pow2i(-UV::val_exp_of_slot(mt));
     accv[mt][0] *= f;
     accv[mt][1] *= f;
     accv[mt][2] *= f;

@@ -97,5 +97,3 @@ def test_split_range_covers():
             assert got[0][0] == 0 and got[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
             assert max(h - l for l, h in got) - min(h - l for l, h in got) <= 1
-    # per-shard accounting sums to the whole (uniform bits; Mixed3 words can straddle shards)
-    assert mem == cache.memory_usage()["total_bits"]
