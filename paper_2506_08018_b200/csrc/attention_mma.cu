@@ -257,18 +257,22 @@ struct MmaParams {
   const void* q;
   int q16, tail16;
   int H, Hq, tq, rows, gs, cg;
-  int64_t T, P;          // total tokens; fast-path limit (multiple of gs)
-  int64_t groups_total;  // ceil(T / gs)
-  int chunk_groups;
+  int64_t T, P;  // total tokens; fast-path limit (multiple of gs)
+  // stream-K work list: per (b, kv-head) U = Gf fast groups + ceil((T - P) / kTailUnit)
+  // tail units, N = BH * U units in bh-major order; warp w of W takes [w N / W, (w+1) N / W)
+  int Gf, U, N;  // 32-bit: the host falls back to the generic path beyond 2^31 units
+  int W;
   int stages;
   uint32_t kt_bytes, vt_bytes, vm_bytes, km_bytes;  // per-group copy sizes
   uint32_t stage_bytes;
   float inv;  // 1/sqrt(D)
   int want_cs;  // accumulate the double scores checksum (only when the caller asks)
-  float2* part_ml;
+  float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
   float* part_acc;
   double* part_cs;
 };
+
+constexpr int kTailUnit = 8;  // full-precision-window tokens per work unit (~ one group's cost)
 
 // Dequantized packed element (token j < quantized, channel d) with compile-time D (gs is a
 // compile-time constant too when the kernel is instantiated with GS): the tail path's
@@ -328,19 +332,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   constexpr bool kMetaRows = GS != 0 && D / (GS ? GS : 1) == 4;
 
   extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ float s_m[kMmaWarps][R], s_l[kMmaWarps][R];
   __shared__ float s_acc[kMmaWarps][R][D];
   __shared__ float s_bias[kMmaWarps][R][8];
-  __shared__ double s_cs[kMmaWarps];
 
-  const int split = blockIdx.x, bh = blockIdx.y, nsplit = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wg = blockIdx.x * kMmaWarps + warp;  // warps are independent: no CTA barriers
+  if (wg >= p.W) return;
   const int g = lane >> 2, t = lane & 3;
-  const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
+  const int G = p.Hq / p.H;
   const int gs = GS ? GS : p.gs;
   const int CG = GS ? D / GS : p.cg;
   const int TPG = gs / 16;  // tiles per group
   const int S = p.stages;
+  const int u_beg = (int)((int64_t)wg * p.N / p.W), u_end = (int)((int64_t)(wg + 1) * p.N / p.W);
 
   uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
   uint8_t* ring = wbase;
@@ -361,45 +365,41 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   }
   __syncwarp();
 
-  // query rows: lane owns channels [lane*LC, lane*LC+LC)
-  float qv[R][LC];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int rr = r < p.rows ? r : 0;
-    const int gi = rr / p.tq, qi = rr % p.tq;
-    const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
-#pragma unroll
-    for (int c = 0; c < LC; ++c) {
-      const float x = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
-      qv[r][c] = r < p.rows ? x : 0.f;
-    }
-  }
-
-  float m_run = -INFINITY, l_run = 0.f;  // row t (threads with t < rows)
-  float accv[NS][4];
-#pragma unroll
-  for (int i = 0; i < NS; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0.f;
-  float accb[4] = {0.f, 0.f, 0.f, 0.f};
-  double cs = 0.0;
   const bool row_ok = t < p.rows;
-
-  const int64_t g_beg = (int64_t)split * p.chunk_groups;
-  const int64_t g_end = min(g_beg + p.chunk_groups, p.groups_total);
-  const int64_t g_fast_end = min(g_end, p.P / gs);
-  const uint8_t* ktiles = reinterpret_cast<const uint8_t*>(p.k.tiles + (size_t)bh * p.k.tiles_per_bh * p.k.tile_words);
-  const uint8_t* vtiles = reinterpret_cast<const uint8_t*>(p.v.tiles + (size_t)bh * p.v.tiles_per_bh * p.v.tile_words);
-  const uint8_t* kmeta = reinterpret_cast<const uint8_t*>(p.k.meta + (size_t)bh * p.k.meta_per_bh);
-  const uint8_t* vmeta = reinterpret_cast<const uint8_t*>(p.v.meta + (size_t)bh * p.v.meta_per_bh);
   const uint64_t policy = evict_first_policy();
 
-  auto issue = [&](int64_t grp, int s) {
-    uint8_t* st = ring + (size_t)s * p.stage_bytes;
-    mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
-    bulk_g2s(st, ktiles + (size_t)grp * p.kt_bytes, p.kt_bytes, &bars[s], policy);
-    bulk_g2s(st + p.kt_bytes, vtiles + (size_t)grp * p.vt_bytes, p.vt_bytes, &bars[s], policy);
-    bulk_g2s(st + p.kt_bytes + p.vt_bytes, vmeta + (size_t)grp * p.vm_bytes, p.vm_bytes, &bars[s], policy);
-    bulk_g2s(st + p.kt_bytes + p.vt_bytes + p.vm_bytes, kmeta + (size_t)grp * p.km_bytes, p.km_bytes, &bars[s], policy);
+  // producer: this warp's fast groups in work-list order, issued S ahead of the consumer
+  int i_bh = u_beg / p.U, i_g = u_beg - i_bh * p.U;
+  if (i_g >= p.Gf) {
+    ++i_bh;
+    i_g = 0;
+  }
+  auto issue_next = [&](int s) {
+    if (p.Gf > 0 && i_bh * p.U + i_g < u_end) {
+      if (lane == 0) {
+        uint8_t* st = ring + (size_t)s * p.stage_bytes;
+        const uint8_t* kt = reinterpret_cast<const uint8_t*>(p.k.tiles + (size_t)i_bh * p.k.tiles_per_bh * p.k.tile_words);
+        const uint8_t* vt = reinterpret_cast<const uint8_t*>(p.v.tiles + (size_t)i_bh * p.v.tiles_per_bh * p.v.tile_words);
+        const uint8_t* vmt = reinterpret_cast<const uint8_t*>(p.v.meta + (size_t)i_bh * p.v.meta_per_bh);
+        const uint8_t* kmt = reinterpret_cast<const uint8_t*>(p.k.meta + (size_t)i_bh * p.k.meta_per_bh);
+        mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
+        bulk_g2s(st, kt + (size_t)i_g * p.kt_bytes, p.kt_bytes, &bars[s], policy);
+        bulk_g2s(st + p.kt_bytes, vt + (size_t)i_g * p.vt_bytes, p.vt_bytes, &bars[s], policy);
+        bulk_g2s(st + p.kt_bytes + p.vt_bytes, vmt + (size_t)i_g * p.vm_bytes, p.vm_bytes, &bars[s], policy);
+        bulk_g2s(st + p.kt_bytes + p.vt_bytes + p.vm_bytes, kmt + (size_t)i_g * p.km_bytes, p.km_bytes, &bars[s], policy);
+      }
+      if (++i_g == p.Gf) {
+        ++i_bh;
+        i_g = 0;
+      }
+    }
   };
+  for (int s = 0; s < S; ++s) issue_next(s);
+
+  float accv[NS][4];
+  float accb[4];
+  float m_run, l_run;  // row t (threads with t < rows)
+  double cs;
 
   auto rescale = [&](float alpha) {
     if (__any_sync(0xffffffffu, alpha != 1.0f)) {
@@ -422,15 +422,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
 #pragma unroll
   for (int mt = 0; mt < NS; ++mt) cg_of[mt] = (mt * 16) / gs;
 
-  // prologue: fill the ring
-  const int64_t first = g_beg + warp;
-  if (lane == 0) {
-    for (int s = 0; s < S; ++s) {
-      const int64_t grp = first + (int64_t)s * kMmaWarps;
-      if (grp < g_fast_end) issue(grp, s);
-    }
-  }
-
   // the k-step of this lane's channels and the power of two its A codes carry
   float cls_scale = 1.f;
   {
@@ -442,7 +433,36 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
 
   int s = 0;
   uint32_t phase = 0;
-  for (int64_t grp = first; grp < g_fast_end; grp += kMmaWarps) {
+  for (int u = u_beg; u < u_end;) {
+    // ---- one (b, kv-head) segment of the work list ----------------------------------------
+    const int bh = u / p.U;
+    const int lo = u - bh * p.U;
+    const int hi = min(u_end - bh * p.U, p.U);
+    u = bh * p.U + hi;
+    const int b = bh / p.H, h = bh % p.H;
+
+    // query rows: lane owns channels [lane*LC, lane*LC+LC)
+    float qv[R][LC];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int rr = r < p.rows ? r : 0;
+      const int gi = rr / p.tq, qi = rr % p.tq;
+      const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
+#pragma unroll
+      for (int c = 0; c < LC; ++c) {
+        const float x = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
+        qv[r][c] = r < p.rows ? x : 0.f;
+      }
+    }
+    m_run = -INFINITY;
+    l_run = 0.f;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0.f;
+    accb[0] = accb[1] = accb[2] = accb[3] = 0.f;
+    cs = 0.0;
+
+  const int g_stop = min(hi, p.Gf);
+  for (int grp = lo; grp < g_stop; ++grp) {
     mbar_wait(&bars[s], phase);
     const uint8_t* st = ring + (size_t)s * p.stage_bytes;
     const uint32_t* kt = reinterpret_cast<const uint32_t*>(st);
@@ -718,24 +738,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       __syncwarp();
     }
     // refill this stage S groups ahead
-    if (lane == 0) {
-      const int64_t nxt = grp + (int64_t)S * kMmaWarps;
-      if (nxt < g_fast_end) issue(nxt, s);
-    }
+    issue_next(s);
     if (++s == S) {
       s = 0;
       phase ^= 1u;
     }
-  }
-
-  // undo the per-m-tile power of two carried by the Value operands
-#pragma unroll
-  for (int mt = 0; mt < NS; ++mt) {
-    const float f = pow2i(-UV::val_exp_of_slot(mt));
-    accv[mt][0] *= f;
-    accv[mt][1] *= f;
-    accv[mt][2] *= f;
-    accv[mt][3] *= f;
   }
 
   // ---- tokens past the fast region: lane-parallel over channels ------------------------
@@ -746,10 +753,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < LC; ++c) acct[r][c] = 0.f;
-  // spread over every CTA of this (b, kv-head) so no split becomes a straggler
-  const int64_t j_lo = p.P + (int64_t)split * kMmaWarps, j_hi = p.T;
-  const int64_t j_step = (int64_t)nsplit * kMmaWarps;
-  if (j_lo + warp < j_hi) {
+  const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * kTailUnit;
+  const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * kTailUnit) : j_lo;
+  if (j_lo < j_hi) {
     float m_all[R], l_all[R];
     {
       float lr = l_run;
@@ -763,7 +769,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       }
     }
     const int d0 = lane * LC;
-    for (int64_t j = j_lo + warp; j < j_hi; j += j_step) {
+    for (int64_t j = j_lo; j < j_hi; ++j) {
       float kx[LC], vx[LC];
       if (j >= p.k.quantized) {
 #pragma unroll
@@ -812,19 +818,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
 
-  // ---- warp epilogue -> shared ----------------------------------------------------------
+  // ---- segment epilogue: this warp's partial for (b, kv-head) -> slot wg + bh ----------
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 8);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
   if (row_ok && t < R) {
-    if (g == 0) {
-      s_m[warp][t] = m_run;
-      s_l[warp][t] = l_run;
-    }
+    // the Value fragments carry the per-m-tile power of two of their operands
 #pragma unroll
     for (int mt = 0; mt < NS; ++mt) {
-      s_acc[warp][t][mt * 16 + g] = accv[mt][0] + accv[mt][1];
-      s_acc[warp][t][mt * 16 + g + 8] = accv[mt][2] + accv[mt][3];
+      const float f = pow2i(-UV::val_exp_of_slot(mt));
+      s_acc[warp][t][mt * 16 + g] = (accv[mt][0] + accv[mt][1]) * f;
+      s_acc[warp][t][mt * 16 + g + 8] = (accv[mt][2] + accv[mt][3]) * f;
     }
     if constexpr (kMetaRows) {
       if (g & 1) s_bias[warp][t][g >> 1] = accb[0] + accb[1];  // min rows
@@ -833,75 +837,67 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     }
   }
   __syncwarp();
+  const int64_t slot = (int64_t)wg + bh;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
+    const float m_r = __shfl_sync(0xffffffffu, m_run, r);
+    const float l_r = __shfl_sync(0xffffffffu, l_run, r);
     if (r < p.rows) {
+      const size_t pi = (size_t)slot * p.rows + r;
+      float o[LC];
 #pragma unroll
-      for (int c = 0; c < LC; ++c) s_acc[warp][r][lane * LC + c] += acct[r][c];
+      for (int c = 0; c < LC; ++c) {
+        const int d = lane * LC + c;
+        o[c] = s_acc[warp][r][d] + s_bias[warp][r][d / gs] + acct[r][c];
+      }
+      if constexpr (LC == 4) {
+        *reinterpret_cast<float4*>(p.part_acc + pi * D + lane * LC) = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < LC; ++c) p.part_acc[pi * D + lane * LC + c] = o[c];
+      }
+      if (lane == 0) p.part_ml[pi] = make_float2(m_r == -INFINITY ? -INFINITY : m_r * kLn2, l_r);
     }
   }
   if (p.want_cs) {
     for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    if (lane == 0) p.part_cs[slot] = cs;
   }
-  if (lane == 0) s_cs[warp] = cs;
-  __syncthreads();
-
-  // ---- CTA merge (fixed warp order) and split partial -----------------------------------
-  for (int e = threadIdx.x; e < p.rows * D; e += blockDim.x) {
-    const int r = e / D, d = e % D;
-    const int c = d / gs;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, s_m[w][r]);
-    float a = 0.f, L = 0.f;
-#pragma unroll
-    for (int w = 0; w < kMmaWarps; ++w) {
-      const float mw = s_m[w][r];
-      if (mw != -INFINITY) {
-        const float f = exp2f(mw - M);
-        a += (s_acc[w][r][d] + s_bias[w][r][c]) * f;
-        L += s_l[w][r] * f;
-      }
-    }
-    const size_t pi = ((size_t)bh * nsplit + split) * p.rows + r;
-    p.part_acc[pi * D + d] = a;
-    if (d == 0) p.part_ml[pi] = make_float2(M == -INFINITY ? -INFINITY : M * kLn2, L);
-  }
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int w = 0; w < kMmaWarps; ++w) tot += s_cs[w];
-    p.part_cs[(size_t)bh * nsplit + split] = tot;
+  __syncwarp();  // s_acc / s_bias are rewritten by the next segment
   }
 }
 
-// Split count: pick the number of CTAs per (b, kv-head) that fills whole waves of the
-// kernel's real residency (occupancy query), with at least two groups per warp; bounded by
-// a cap that depends on (B, H) only, so scratch never depends on the token count.
-int split_cap(int BH) {
-  // up to ~16 waves of 4 CTAs/SM; depends on (B, H) only
-  return std::max(1, std::min(512, (16 * 4 * num_sms() + BH - 1) / std::max(1, BH)));
-}
-
-int pick_splits(int BH, int64_t groups, int slots) {
-  const int cap = split_cap(BH);
-  int best = 1;
-  double best_score = -1.0;
-  for (int n = 1; n <= cap; ++n) {
-    const int64_t chunk = (groups + n - 1) / n;
-    if (n > 1 && chunk < 2 * kMmaWarps) break;
-    const double waves = (double)n * BH / slots;
-    const double eff = waves / std::ceil(waves);
-    const double score = eff - 0.002 * n;
-    if (score > best_score + 1e-9) {
-      best_score = score;
-      best = n;
-    }
+// Combine the stream-K partials of each (b, kv-head): the warps whose unit ranges meet
+// [bh U, (bh+1) U), slot w + bh, merged in warp order (deterministic).
+__global__ void attend_combine_sk_kernel(const float2* __restrict__ part_ml, const float* __restrict__ part_acc,
+                                         int N, int W, int U, int R, int H, int Hq, int tq, int D,
+                                         float* __restrict__ out) {
+  const int bh = blockIdx.x, r = blockIdx.y;
+  const int b = bh / H, h = bh % H, G = Hq / H;
+  const int gi = r / tq, qi = r % tq;
+  const int hq = h * G + gi;
+  const int w0 = (int)((((int64_t)bh * U + 1) * W - 1) / N);
+  const int w1 = (int)((((int64_t)bh + 1) * U * W - 1) / N);  // 64-bit products
+  float M = -INFINITY;
+  for (int w = w0; w <= w1; ++w) M = fmaxf(M, part_ml[((size_t)w + bh) * R + r].x);
+  float L = 0.f;
+  for (int w = w0; w <= w1; ++w) {
+    const float2 ml = part_ml[((size_t)w + bh) * R + r];
+    if (ml.x != -INFINITY) L += ml.y * expf(ml.x - M);
   }
-  return best;
+  const float invL = 1.0f / L;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float a = 0.f;
+    for (int w = w0; w <= w1; ++w) {
+      const float2 ml = part_ml[((size_t)w + bh) * R + r];
+      if (ml.x != -INFINITY) a += part_acc[(((size_t)w + bh) * R + r) * D + d] * expf(ml.x - M);
+    }
+    out[(((size_t)b * Hq + hq) * tq + qi) * D + d] = a * invL;
+  }
 }
 
 template <int D, int KB, int VB, int R, int GS>
-int launch(MmaParams& p, int BH, cudaStream_t st) {
+int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
   constexpr int NB = (NCOL + 7) / 8;
   using WL = WarpLayout<D, NB, GS ? D / GS : 8>;
@@ -934,30 +930,38 @@ int launch(MmaParams& p, int BH, cudaStream_t st) {
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMmaWarps * 32, smem), "occupancy");
     occ_smem = smem;
   }
-  const int nsplit = pick_splits(BH, p.groups_total, std::max(1, occ) * num_sms());
-  p.chunk_groups = (int)((p.groups_total + nsplit - 1) / nsplit);
-  kern<<<dim3(nsplit, BH), kMmaWarps * 32, smem, st>>>(p);
-  return nsplit;
+  // one resident wave of independent warps (persistent): equal unit ranges, no stragglers;
+  // never more warps than units so every range is non-empty
+  const int64_t wave = (int64_t)std::max(1, occ) * num_sms() * kMmaWarps;
+  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(p.N, wave));
+  // partial slots w + bh < W + BH: scratch depends on (B, H, rows, D, SM count) only
+  const size_t slots = (size_t)wave + BH;
+  p.part_ml = ws.ml(st, slots * p.rows);
+  p.part_acc = ws.acc(st, slots * p.rows * D);
+  p.part_cs = ws.cs(st, slots + 1);
+  if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
+  kern<<<(p.W + kMmaWarps - 1) / kMmaWarps, kMmaWarps * 32, smem, st>>>(p);
+  return p.W;
 }
 
 template <int D, int KB, int VB, int R>
-int dispatch_gs(MmaParams& p, int BH, cudaStream_t st) {
+int dispatch_gs(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   if constexpr (KB == 3 && R > 2) {
     return 0;
   } else {
-    return p.gs == 32 ? launch<D, KB, VB, R, 32>(p, BH, st) : launch<D, KB, VB, R, 0>(p, BH, st);
+    return p.gs == 32 ? launch<D, KB, VB, R, 32>(p, BH, ws, st) : launch<D, KB, VB, R, 0>(p, BH, ws, st);
   }
 }
 
 template <int D, int R>
-int dispatch_bits(MmaParams& p, int kb, int vb, int BH, cudaStream_t st) {
+int dispatch_bits(MmaParams& p, int kb, int vb, int BH, Workspace& ws, cudaStream_t st) {
   switch (kb * 10 + vb) {
-    case 22: return dispatch_gs<D, 2, 2, R>(p, BH, st);
-    case 24: return dispatch_gs<D, 2, 4, R>(p, BH, st);
-    case 42: return dispatch_gs<D, 4, 2, R>(p, BH, st);
-    case 44: return dispatch_gs<D, 4, 4, R>(p, BH, st);
-    case 32: return dispatch_gs<D, 3, 2, R>(p, BH, st);
-    case 34: return dispatch_gs<D, 3, 4, R>(p, BH, st);
+    case 22: return dispatch_gs<D, 2, 2, R>(p, BH, ws, st);
+    case 24: return dispatch_gs<D, 2, 4, R>(p, BH, ws, st);
+    case 42: return dispatch_gs<D, 4, 2, R>(p, BH, ws, st);
+    case 44: return dispatch_gs<D, 4, 4, R>(p, BH, ws, st);
+    case 32: return dispatch_gs<D, 3, 2, R>(p, BH, ws, st);
+    case 34: return dispatch_gs<D, 3, 4, R>(p, BH, ws, st);
     default: return 0;
   }
 }
@@ -991,7 +995,11 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (p.cg > 8) return false;
   p.T = T;
   p.P = (std::min(c->k.quantized, c->v.quantized) / gs) * gs;
-  p.groups_total = (T + gs - 1) / gs;
+  const int64_t U = p.P / gs + (T - p.P + kTailUnit - 1) / kTailUnit;
+  if ((int64_t)BH * U >= (int64_t)1 << 31) return false;
+  p.Gf = (int)(p.P / gs);
+  p.U = (int)U;
+  p.N = BH * p.U;
   p.kt_bytes = (uint32_t)((gs / 16) * c->k.tile_words * 4);
   p.vt_bytes = (uint32_t)((gs / 16) * c->v.tile_words * 4);
   p.vm_bytes = (uint32_t)(gs * p.cg * 4);
@@ -1000,29 +1008,27 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
-  const int cap_splits = split_cap(BH);
-  p.part_ml = ws.ml(st, (size_t)BH * cap_splits * rows);
-  p.part_acc = ws.acc(st, (size_t)BH * cap_splits * rows * D);
-  p.part_cs = ws.cs(st, (size_t)BH * cap_splits + 1);
   const int R = rows <= 1 ? 1 : rows <= 2 ? 2 : 4;
-  int nsplit = 0;
+  int W = 0;
 #define KVB_DISPATCH_D(DD)                                                  \
   if (D == DD) {                                                            \
-    if (R == 1) nsplit = dispatch_bits<DD, 1>(p, kb, vb, BH, st);          \
-    else if (R == 2) nsplit = dispatch_bits<DD, 2>(p, kb, vb, BH, st);     \
-    else nsplit = dispatch_bits<DD, 4>(p, kb, vb, BH, st);                 \
+    if (R == 1) W = dispatch_bits<DD, 1>(p, kb, vb, BH, ws, st);           \
+    else if (R == 2) W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st);      \
+    else W = dispatch_bits<DD, 4>(p, kb, vb, BH, ws, st);                  \
   }
   KVB_DISPATCH_D(64)
   KVB_DISPATCH_D(128)
 #undef KVB_DISPATCH_D
-  if (nsplit == 0) return false;
+  if (W == 0) return false;
   after_launch("attend_mma_kernel");
-  attend_combine_kernel<<<dim3(BH, rows), 128, 0, st>>>(p.part_ml, p.part_acc, nsplit, rows, c->H, Hq, tq, D, out);
-  after_launch("attend_combine_kernel");
+  attend_combine_sk_kernel<<<dim3(BH, rows), 128, 0, st>>>(p.part_ml, p.part_acc, p.N, p.W, p.U, rows, c->H, Hq, tq, D,
+                                                           out);
+  after_launch("attend_combine_sk_kernel");
   if (checksum) {
-    checksum_kernel<<<1, 32, 0, st>>>(p.part_cs, (size_t)BH * nsplit, p.part_cs + (size_t)BH * cap_splits);
+    const size_t nslot = (size_t)p.W + BH;
+    checksum_kernel<<<1, 32, 0, st>>>(p.part_cs, nslot, p.part_cs + nslot);
     after_launch("checksum_kernel");
-    check_cuda(cudaMemcpyAsync(checksum, p.part_cs + (size_t)BH * cap_splits, 8, cudaMemcpyDeviceToHost, st), "memcpy");
+    check_cuda(cudaMemcpyAsync(checksum, p.part_cs + nslot, 8, cudaMemcpyDeviceToHost, st), "memcpy");
     check_cuda(cudaStreamSynchronize(st), "sync");
   }
   return true;
