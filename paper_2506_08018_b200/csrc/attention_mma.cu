@@ -261,6 +261,7 @@ struct MmaParams {
   // stream-K work list: per (b, kv-head) U = Gf fast groups + ceil((T - P) / kTailUnit)
   // tail units, N = BH * U units in bh-major order; warp w of W takes [w N / W, (w+1) N / W)
   int Gf, U, N;  // 32-bit: the host falls back to the generic path beyond 2^31 units
+  int Grec;      // group records per (b, kv-head) (bh stride of the record array)
   int W;
   int stages;
   uint32_t kt_bytes, vt_bytes, vm_bytes, km_bytes;  // per-group copy sizes
@@ -279,16 +280,16 @@ constexpr int kTailUnit = 8;  // full-precision-window tokens per work unit (~ o
 // per-element cost without runtime divisions.
 template <int D, bool KEY, int BITS>
 __device__ __forceinline__ float deq_lane(const SideView& s, int bh, int j, int d, int gs) {
-  const uint32_t* tile = s.tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
+  const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
   const uint32_t code = tile_get(tile, KEY ? key_coord(j & 15, d) : value_coord(j & 15, d), D, BITS);
   uint32_t m;
   bool narrow = false;
   if (KEY) {
     const int grp = j / gs;
-    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)grp * D + d];
+    m = s.meta[kmeta_index(s, bh, grp) + d];
     if (BITS == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
   } else {
-    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)j * ((D + gs - 1) / gs) + d / gs];
+    m = s.meta[vmeta_index(s, bh, j) + d / gs];
     if (BITS == 3) narrow = narrow_value(bh, d, D, s.info[j]);
   }
   return decode(code, meta_scale(m), meta_min(m), narrow);
@@ -377,16 +378,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   auto issue_next = [&](int s) {
     if (p.Gf > 0 && i_bh * p.U + i_g < u_end) {
       if (lane == 0) {
-        uint8_t* st = ring + (size_t)s * p.stage_bytes;
-        const uint8_t* kt = reinterpret_cast<const uint8_t*>(p.k.tiles + (size_t)i_bh * p.k.tiles_per_bh * p.k.tile_words);
-        const uint8_t* vt = reinterpret_cast<const uint8_t*>(p.v.tiles + (size_t)i_bh * p.v.tiles_per_bh * p.v.tile_words);
-        const uint8_t* vmt = reinterpret_cast<const uint8_t*>(p.v.meta + (size_t)i_bh * p.v.meta_per_bh);
-        const uint8_t* kmt = reinterpret_cast<const uint8_t*>(p.k.meta + (size_t)i_bh * p.k.meta_per_bh);
+        // the group's record (K tiles | V tiles | V meta | K meta) is one contiguous range
+        const uint32_t* src = p.k.tiles + ((size_t)i_bh * p.Grec + i_g) * (p.stage_bytes / 4);
         mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
-        bulk_g2s(st, kt + (size_t)i_g * p.kt_bytes, p.kt_bytes, &bars[s], policy);
-        bulk_g2s(st + p.kt_bytes, vt + (size_t)i_g * p.vt_bytes, p.vt_bytes, &bars[s], policy);
-        bulk_g2s(st + p.kt_bytes + p.vt_bytes, vmt + (size_t)i_g * p.vm_bytes, p.vm_bytes, &bars[s], policy);
-        bulk_g2s(st + p.kt_bytes + p.vt_bytes + p.vm_bytes, kmt + (size_t)i_g * p.km_bytes, p.km_bytes, &bars[s], policy);
+        bulk_g2s(ring + (size_t)s * p.stage_bytes, src, p.stage_bytes, &bars[s], policy);
       }
       if (++i_g == p.Gf) {
         ++i_bh;
@@ -1005,6 +1000,10 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.vm_bytes = (uint32_t)(gs * p.cg * 4);
   p.km_bytes = (uint32_t)(D * 4);
   p.stage_bytes = p.kt_bytes + p.vt_bytes + p.vm_bytes + p.km_bytes;
+  if ((size_t)p.stage_bytes != c->k.grp_stride * 4 || c->v.tiles != c->k.tiles + (gs / 16) * c->k.tile_words)
+    return false;  // not the group-record layout this kernel streams
+  if (c->k.bh_stride % c->k.grp_stride != 0 || c->k.bh_stride / c->k.grp_stride >= (1u << 31)) return false;
+  p.Grec = (int)(c->k.bh_stride / c->k.grp_stride);
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;

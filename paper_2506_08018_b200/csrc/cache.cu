@@ -105,14 +105,14 @@ struct AppendArgs {
   uint32_t* k_tiles;
   uint32_t* k_meta;
   int2* k_info;
-  size_t k_tiles_per_bh, k_tile_words, k_meta_per_bh;
+  SideView kv;  // addressing of the Key side (group records)
   // values
   int vbits, v_blocks, v_tile0;
   int64_t v_q0, v_n;
   uint32_t* v_tiles;
   uint32_t* v_meta;
   int2* v_info;
-  size_t v_tiles_per_bh, v_tile_words, v_meta_per_bh;
+  SideView vv;
   // tails: staying tokens of the input go to ring slots
   void* k_tail;
   void* v_tail;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
         mx = x > mx ? x : mx;
       }
       const uint32_t m = make_meta(mn, mx, q_max);
-      a.k_meta[(size_t)bh * a.k_meta_per_bh + (size_t)gglob * D + d] = m;
+      a.k_meta[kmeta_index(a.kv, bh, gglob) + d] = m;
       const float sc = meta_scale(m), mnv = meta_min(m);
       // reference stream index inside this segment [B,H,n,D]: (bh*D + d)*n + t_local
       const uint64_t sbase = ((uint64_t)bh * D + d) * (uint64_t)a.k_n + (uint64_t)j0;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     __syncthreads();
     const int64_t tile0 = (a.k_q0 + (int64_t)g * gs) / 16;
     for (int tt = 0; tt < gs / 16; ++tt) {
-      uint32_t* tile = a.k_tiles + (size_t)bh * a.k_tiles_per_bh * a.k_tile_words + (size_t)(tile0 + tt) * a.k_tile_words;
+      uint32_t* tile = a.k_tiles + tile_index(a.kv, bh, tile0 + tt);
       emit_tile(true, D, a.kbits, codes + tt * 16 * D, tile, false, 0, 16);
     }
     return;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       }
       const uint32_t m = make_meta(mn, mx, q_max);
       mrow[i * cg + gi] = m;
-      a.v_meta[(size_t)bh * a.v_meta_per_bh + (size_t)(tile * 16 + i) * cg + gi] = m;
+      a.v_meta[vmeta_index(a.vv, bh, tile * 16 + i) + gi] = m;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < (i_hi - i_lo) * D; e += blockDim.x) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     }
     __syncthreads();
     // only the aged rows' fields: one atomicOr per code into the (zero-initialised) tile
-    uint32_t* tp = a.v_tiles + (size_t)bh * a.v_tiles_per_bh * a.v_tile_words + (size_t)tile * a.v_tile_words;
+    uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, tile);
     for (int e = threadIdx.x; e < (i_hi - i_lo) * D; e += blockDim.x) {
       const int i = i_lo + e / D, d = e % D;
       const uint32_t code = codes[i * D + d];
@@ -293,7 +293,7 @@ __global__ void export_words_kernel(SideView s, bool key, int D, int BH, int64_t
         tl = (int64_t)(tok % n);
       }
       const int64_t j = S + tl;
-      const uint32_t* tile = s.tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
+      const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
       const int i = (int)(j & 15);
       const uint32_t code = tile_get(tile, key ? key_coord(i, d) : value_coord(i, d), D, bits);
       word |= code << field_shift(bits, (uint32_t)k);
@@ -311,13 +311,13 @@ __global__ void export_meta_kernel(SideView s, bool key, int D, int gs, int BH, 
       const size_t c = mi / gpc;
       const int64_t gl = (int64_t)(mi % gpc);
       const int bh = (int)(c / D), d = (int)(c % D);
-      meta[mi] = s.meta[(size_t)bh * s.meta_per_bh + (size_t)(S / gs + gl) * D + d];
+      meta[mi] = s.meta[kmeta_index(s, bh, S / gs + gl) + d];
     } else {
       const size_t tok = mi / cg;
       const int g = (int)(mi % cg);
       const int bh = (int)(tok / n);
       const int64_t tl = (int64_t)(tok % n);
-      meta[mi] = s.meta[(size_t)bh * s.meta_per_bh + (size_t)(S + tl) * cg + g];
+      meta[mi] = s.meta[vmeta_index(s, bh, S + tl) + g];
     }
   }
 }
@@ -358,7 +358,7 @@ __global__ void import_kernel(SideView s, uint32_t* tiles, uint32_t* dmeta, int2
     const uint32_t pos = (uint32_t)(p % cpw);
     const uint32_t code = (words[p / cpw] >> field_shift(bits, pos)) & field_mask(bits, pos);
     const int64_t j = q0 + tl;
-    uint32_t* tile = tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
+    uint32_t* tile = tiles + tile_index(s, bh, j >> 4);
     const TileCoord tc = key ? key_coord((int)(j & 15), d) : value_coord((int)(j & 15), d);
     if (bits == 3) {
       int w, sh;
@@ -373,11 +373,11 @@ __global__ void import_kernel(SideView s, uint32_t* tiles, uint32_t* dmeta, int2
     }
     if (key) {
       if (tl % gs == 0) {
-        dmeta[(size_t)bh * s.meta_per_bh + (size_t)(j / gs) * D + d] = meta[((size_t)bh * D + d) * (n / gs) + tl / gs];
+        dmeta[kmeta_index(s, bh, j / gs) + d] = meta[((size_t)bh * D + d) * (n / gs) + tl / gs];
         if (bh == 0 && d == 0) info[j / gs] = make_int2((int)n, (int)tl);
       }
     } else if (d % gs == 0) {
-      dmeta[(size_t)bh * s.meta_per_bh + (size_t)j * cg + d / gs] = meta[((size_t)bh * n + tl) * cg + d / gs];
+      dmeta[vmeta_index(s, bh, j) + d / gs] = meta[((size_t)bh * n + tl) * cg + d / gs];
       if (bh == 0 && d == 0) info[j] = make_int2((int)n, (int)tl);
     }
   }
@@ -450,9 +450,7 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
   a.k_tiles = K.tiles;
   a.k_meta = K.meta;
   a.k_info = K.info;
-  a.k_tiles_per_bh = K.tiles_per_bh;
-  a.k_tile_words = K.tile_words;
-  a.k_meta_per_bh = K.meta_per_bh;
+  a.kv = view(K);
   a.vbits = V.bits;
   a.v_q0 = V.quantized;
   a.v_n = v_n;
@@ -464,9 +462,7 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
   a.v_tiles = V.tiles;
   a.v_meta = V.meta;
   a.v_info = V.info;
-  a.v_tiles_per_bh = V.tiles_per_bh;
-  a.v_tile_words = V.tile_words;
-  a.v_meta_per_bh = V.meta_per_bh;
+  a.vv = view(V);
   a.k_tail = K.tail;
   a.v_tail = V.tail;
   a.k_cap = K.tail_cap;
@@ -603,9 +599,8 @@ void cache_import_tail(kvmix_cache* c, int side, const float* tail, int64_t t, c
 }
 
 void cache_reset(kvmix_cache* c, cudaStream_t st) {
+  check_cuda(cudaMemsetAsync(c->rec, 0, c->rec_bytes, st), "memset records");
   for (auto* s : {&c->k, &c->v}) {
-    const size_t bytes = (size_t)c->B * c->H * s->tiles_per_bh * s->tile_words * 4;
-    check_cuda(cudaMemsetAsync(s->tiles, 0, bytes, st), "memset tiles");
     s->segs.clear();
     s->quantized = 0;
     s->tail_len = 0;

@@ -5,13 +5,15 @@
 
 #include "common.cuh"
 
-// HBM layout of one layer (bh = b*H + h, all arrays bh-major so one (b, kv-head) stream is
-// contiguous -- the unit attention CTAs and the multi-GPU shards partition):
-//   K tiles  [bh][tile = token/16][tile_words(D, key_bits)]      packed codes, fragment-native
-//   K meta   [bh][group = token/gs][D]        u32 {scale_f16 | min_f16 << 16}
+// HBM layout of one layer (bh = b*H + h, bh-major so one (b, kv-head) stream is contiguous
+// -- the unit the attention work list and the multi-GPU shards partition). The packed store
+// is ONE array of group records, so the attention kernel moves a whole group (Keys, Values
+// and both metas) with a single bulk copy:
+//   rec      [bh][group = token/gs] { K tiles [gs/16][tile_words(D, key_bits)]   fragment-native codes
+//                                     V tiles [gs/16][tile_words(D, value_bits)]
+//                                     V meta  [gs][ceil(D/gs)]  u32 {scale_f16 | min_f16 << 16}
+//                                     K meta  [D] }
 //   K tail   [bh][ring slot][D]               fp32 or fp16 full-precision window (ring)
-//   V tiles  [bh][tile][tile_words(D, value_bits)]
-//   V meta   [bh][token][ceil(D/gs)]          u32
 //   V tail   [bh][ring slot][D]
 //   K info   [group] int2 {segment length, token offset in segment}  (Mixed3 narrow slots)
 //   V info   [token] int2 {segment length, token offset in segment}
@@ -23,11 +25,12 @@ struct kvmix_cache {
     float ratio = 0.1f;
     int64_t tail_cap = 0, tail_start = 0, tail_len = 0, quantized = 0;
     std::vector<int64_t> segs;
-    uint32_t* tiles = nullptr;
+    uint32_t* tiles = nullptr;  // this side's tiles / meta inside the group records
     uint32_t* meta = nullptr;
     void* tail = nullptr;
     int2* info = nullptr;
-    size_t tiles_per_bh = 0, tile_words = 0, meta_per_bh = 0;
+    size_t tile_words = 0, bh_stride = 0, grp_stride = 0;  // words
+    int tpg = 0, mrow = 0;  // tiles per group; meta words per Key group / per Value token
   };
   kvmix_layer_config cfg{};
   int B = 0, H = 0, D = 0;
@@ -35,6 +38,8 @@ struct kvmix_cache {
   kvmix_dtype tail_dtype = KVMIX_F32;
   int device = 0;
   Side k, v;
+  uint32_t* rec = nullptr;  // group records of both sides
+  size_t rec_bytes = 0;
   int cgroups() const { return (D + cfg.group_size - 1) / cfg.group_size; }
   int64_t total() const { return k.quantized + k.tail_len; }
 };
@@ -49,12 +54,29 @@ struct SideView {
   const int2* info;
   int64_t tail_cap, tail_start, tail_len, quantized;
   int bits;
-  size_t tiles_per_bh, tile_words, meta_per_bh;
+  size_t tile_words, bh_stride, grp_stride;
+  int tpg, mrow;
 };
 
 inline SideView view(const kvmix_cache::Side& s) {
   return SideView{s.tiles, s.meta, s.tail, s.info, s.tail_cap, s.tail_start, s.tail_len, s.quantized,
-                  s.bits, s.tiles_per_bh, s.tile_words, s.meta_per_bh};
+                  s.bits, s.tile_words, s.bh_stride, s.grp_stride, s.tpg, s.mrow};
+}
+
+// Word offsets into a side's tiles / meta (group-record layout above).
+__host__ __device__ inline size_t tile_index(const SideView& s, int bh, int64_t tile) {
+  const int64_t gi = tile / s.tpg;
+  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(tile - gi * s.tpg) * s.tile_words;
+}
+// Key meta row of group grp (D words, one per channel)
+__host__ __device__ inline size_t kmeta_index(const SideView& s, int bh, int64_t grp) {
+  return (size_t)bh * s.bh_stride + (size_t)grp * s.grp_stride;
+}
+// Value meta row of token j (ceil(D/gs) words, one per channel group)
+__host__ __device__ inline size_t vmeta_index(const SideView& s, int bh, int64_t j) {
+  const int gs = s.tpg * 16;
+  const int64_t gi = j / gs;
+  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(j - gi * gs) * s.mrow;
 }
 
 template <typename TT>
@@ -78,18 +100,17 @@ __device__ inline bool narrow_value(int bh, int d, int D, int2 info) {
 // Dequantized value of quantized token j (j < s.quantized) of one side, bit-exact.
 __device__ inline float packed_value(bool key, const SideView& s, int bh, int64_t j64, int d, int D, int gs) {
   const int j = (int)j64;
-  const uint32_t* tile = s.tiles + (size_t)bh * s.tiles_per_bh * s.tile_words + (size_t)(j >> 4) * s.tile_words;
+  const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
   const int i = j & 15;
   const uint32_t code = tile_get(tile, key ? key_coord(i, d) : value_coord(i, d), D, s.bits);
   uint32_t m;
   bool narrow = false;
   if (key) {
     const int grp = j / gs;
-    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)grp * D + d];
+    m = s.meta[kmeta_index(s, bh, grp) + d];
     if (s.bits == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
   } else {
-    const int cg = (D + gs - 1) / gs;
-    m = s.meta[(size_t)bh * s.meta_per_bh + (size_t)j * cg + d / gs];
+    m = s.meta[vmeta_index(s, bh, j) + d / gs];
     if (s.bits == 3) narrow = narrow_value(bh, d, D, s.info[j]);
   }
   return decode(code, meta_scale(m), meta_min(m), narrow);

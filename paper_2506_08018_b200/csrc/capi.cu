@@ -57,11 +57,10 @@ void alloc(void** p, size_t bytes) {
 void free_cache(kvmix_cache* c) {
   if (!c) return;
   for (auto* s : {&c->k, &c->v}) {
-    cudaFree(s->tiles);
-    cudaFree(s->meta);
     cudaFree(s->tail);
     cudaFree(s->info);
   }
+  cudaFree(c->rec);
   delete c;
 }
 
@@ -152,7 +151,12 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
     check_cuda(cudaGetDevice(&c->device), "cudaGetDevice");
     const int gs = cfg->group_size;
     const size_t BH = (size_t)batch * heads;
-    const int64_t ntiles = (capacity_tokens + 15) / 16;
+    const int64_t ngroups = (capacity_tokens + gs - 1) / gs;  // group records per (b, kv-head)
+    const int tpg = gs / 16, cg = (head_dim + gs - 1) / gs;
+    const size_t ktw = (size_t)tile_words(head_dim, cfg->key_bits), vtw = (size_t)tile_words(head_dim, cfg->value_bits);
+    const size_t rec_words = tpg * (ktw + vtw) + (size_t)gs * cg + head_dim;  // 16-byte multiple
+    c->rec_bytes = BH * (size_t)ngroups * rec_words * 4;
+    alloc((void**)&c->rec, c->rec_bytes);
     const size_t esz = tail_dtype == KVMIX_F16 ? 2 : 4;
     struct Spec {
       kvmix_cache::Side* s;
@@ -164,21 +168,18 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
       auto& s = *sp.s;
       s.bits = sp.bits;
       s.ratio = sp.r;
-      s.tile_words = (size_t)tile_words(head_dim, sp.bits);
-      s.tiles_per_bh = (size_t)ntiles;
+      s.tile_words = sp.key ? ktw : vtw;
+      s.tpg = tpg;
+      s.grp_stride = rec_words;
+      s.bh_stride = (size_t)ngroups * rec_words;
+      s.tiles = c->rec + (sp.key ? 0 : tpg * ktw);
+      s.meta = c->rec + tpg * (ktw + vtw) + (sp.key ? (size_t)gs * cg : 0);
+      s.mrow = sp.key ? head_dim : cg;
       // window bound: floor(r*cap) (+ gs-1 for whole-group key aging) plus decode slack
       const int64_t bound = (int64_t)std::floor((double)sp.r * (double)capacity_tokens) + (sp.key ? gs : 1);
       s.tail_cap = std::min<int64_t>(capacity_tokens, bound) + 64;
-      alloc((void**)&s.tiles, BH * s.tiles_per_bh * s.tile_words * 4);
-      if (sp.key) {
-        s.meta_per_bh = (size_t)((ntiles * 16 + gs - 1) / gs) * head_dim;
-        alloc((void**)&s.info, sizeof(int2) * (size_t)((capacity_tokens + gs - 1) / gs));
-      } else {
-        // whole tiles of tokens: keeps every (b,h) row 16-byte aligned for bulk copies
-        s.meta_per_bh = (size_t)ntiles * 16 * ((head_dim + gs - 1) / gs);
-        alloc((void**)&s.info, sizeof(int2) * (size_t)capacity_tokens);
-      }
-      alloc((void**)&s.meta, BH * s.meta_per_bh * 4);
+      if (sp.key) alloc((void**)&s.info, sizeof(int2) * (size_t)ngroups);
+      else alloc((void**)&s.info, sizeof(int2) * (size_t)capacity_tokens);
       alloc(&s.tail, BH * (size_t)s.tail_cap * head_dim * esz);
     }
     *out = c;

@@ -9,6 +9,7 @@ import sys
 
 rep, pat = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+by_stall = len(sys.argv) > 4 and sys.argv[4] == "stall"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
                      capture_output=True, text=True).stdout
 lines, fn, hdr, path = [], None, None, None
@@ -34,5 +35,5 @@ for r in csv.reader(io.StringIO(out)):
 tot = sum(x[0] for x in lines) or 1
 tots = sum(x[1] for x in lines) or 1
 print(f"total inst {tot:.4g}")
-for n, s, f, ln, src in sorted(lines, reverse=True)[:top]:
+for n, s, f, ln, src in sorted(lines, key=lambda x: x[1] if by_stall else x[0], reverse=True)[:top]:
     print(f"{100*n/tot:5.1f}% inst {100*s/tots:5.1f}% stall  {f}:{ln:>4}  {src}")
