@@ -1,40 +1,44 @@
-// attention_mma.cu -- fused split-K decode attention on the tensor cores (mma.sync m16n8k16),
-// fed by TMA bulk copies (cp.async.bulk + mbarrier) into a per-warp shared-memory ring.
+// attention_mma.cu -- fused split-K decode attention on the tensor cores, fed by TMA bulk
+// copies (cp.async.bulk + mbarrier) into a per-warp shared-memory ring.
 //
 // Decode is a GEMV per (b, kv-head): scores = K q, out = V^T p. At 2-bit gs32 a K+V element
 // pair is 0.75 B of HBM traffic, so a CUDA-core loop (unpack + dequant + FMA per element)
-// runs out of issue slots before HBM does. Here the codes go straight
-// from shared memory into tensor-core A fragments: the device tile layout (common.cuh) is
-// "fragment-native", so one 128-bit shared load per lane yields that lane's A operands.
-// The dequantization is factored out of the dot products:
+// runs out of issue slots before HBM does. The dequantization is
+// factored out of the dot products
 //     q.k_j  = sum_d (q_d s_gd) c_jd + sum_d q_d m_gd          (Keys, per channel group)
 //     out_d  = sum_j (p_j s_jg) c_jd + sum_j p_j m_jg          (Values, per token group)
-// The B operands (q*s, p*s, p) are split into an fp16 hi part and an fp16 lo remainder in
-// two MMA columns, so products carry ~22 mantissa bits and accumulate in fp32. The Value
-// min term is a second small MMA with A = the binary16 mins (exact in fp16).
+// and the code sums run on integer tensor cores: mma.sync m16n8k32 with the CODES as the
+// u8 A operand straight from the packed words (IMMA layout, common.cuh: one AND per 4
+// codes, each carrying a per-channel power of two 2^(b*class)) and the fp32 factors as the
+// B operand in fixed point, split into four base-256 digits held in four MMA columns
+// (digit n has weight 2^(8n)). Integer products and int32 accumulation are exact, so the
+// only rounding is the fixed-point conversion of the B values (2^-29 of the largest one):
+//   * Keys: B_d = round(q_d s_d 2^-(b class_d) sigma), sigma = 2^(29 - floor(log2 max)),
+//     balanced s8 digits, per group; scores come back per 16-token tile.
+//   * Values: B_j = round(p_j s_jg 2^E), unsigned u8 digits. p <= 1 and the running 2^E
+//     only changes when the largest scale of a block would overflow 2^30, so int32
+//     accumulators persist across blocks and are folded into fp32 (shared memory) only when
+//     the online-softmax max moves, E changes, or 1024 blocks have accumulated.
+//   * The min terms are fp32 FMAs (Keys: one dot product per group; Values: one FMA per
+//     token and channel group).
+// On sm_100a legacy mma.sync issues one MMA per ~8.5 cycles per SM sub-partition for both
+// HMMA m16n8k16 and IMMA m16n8k32 (profiles/probes/imma_rate.cu), so k32 integer MMAs
+// halve the tensor-pipe time as well as the unpack work of the fp16 formulation.
 //
-// Unpack ("scale classes"): a fragment register holds two codes at the same bit offset of
-// the two 16-bit halves. OR-ing the masked word into 0x6400 (fp16 1024) and subtracting
-// 1024 gives the codes exactly, scaled by 2^offset -- so codes at offsets 0..9 need no
-// shift at all. The slot -> offset map only depends on the k-step (Keys) / m-tile
-// (Values), so the power of two is folded into the Key B operand per channel and into the
-// Value accumulator of each m-tile at the end: one LOP3 + one HADD2 per register.
+// Mixed3 (3-bit) Keys keep the fp16 HMMA formulation (HMMA layout): the reference's narrow
+// slots (stream index % 11 == 10) dequantize with scale*7/3; for channel d of a group the
+// narrow tokens are t = tau_d (mod 11), so the correction is 11 extra residue-class B
+// columns (hi/lo fp16 pairs) in the same MMAs.
 //
-// Mixed3 (3-bit) Keys: the reference's narrow slots (stream index % 11 == 10) dequantize
-// with scale*7/3. For channel d of a group the narrow tokens are t = tau_d (mod 11), so the
-// correction sum_d [t == tau_d mod 11] c_td q_d (s'_d - s_d) is 11 extra B columns (one per
-// residue class, hi/lo) in the same MMAs; each token picks the column of its residue.
+// Memory pipeline: every unit of work (one Key group of gs tokens of one (b, kv-head)) is
+// one contiguous record (Key tiles | Value tiles | Value meta | Key meta) copied by one
+// elected lane with cp.async.bulk into a ring of S stages; the warp waits on the stage's
+// mbarrier (complete_tx), computes, and refills the stage S groups ahead.
 //
-// Memory pipeline: every unit of work (one Key group of gs tokens of one (b, kv-head))
-// is four contiguous byte ranges in HBM -- Key tiles, Value tiles, Value meta, Key meta --
-// copied by one elected lane with cp.async.bulk into a ring of S stages; the warp waits on
-// the stage's mbarrier (complete_tx), computes, and refills the stage S groups ahead.
-//
-// CTA = 4 warps over one (b, kv-head) and a chunk of groups (warps interleave groups).
-// Tokens past the last group whose Keys and Values are both packed (the full-precision
-// window, a partially aged Value tile) are processed lane-parallel over channels (each
-// lane owns D/32 channels) with the same online-softmax state. Partials (m, l, acc) go to
-// the split-K combine kernel shared with the generic path.
+// Work distribution (stream-K): a list of per-(b, kv-head) units (fast groups, then tail
+// units of the full-precision window) is cut into equal ranges over one resident wave of
+// independent warps; each warp writes one partial (m, l, acc) per (b, kv-head) segment it
+// touches, merged in warp order by attend_combine_sk_kernel (deterministic).
 #include <algorithm>
 #include <cmath>
 
@@ -45,8 +49,22 @@ namespace kvb {
 namespace {
 
 constexpr int kMmaWarps = 4;
+#ifndef KVB_MIN_CTAS
+#define KVB_MIN_CTAS(KB) ((KB) == 3 ? 3 : 4)  // CTAs per SM the register budget is sized for
+#endif
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kFlushBlocks = 1024;  // Value int32 accumulators: < 2^31 / (32 * 240 * 255)
+// Lazy online-softmax max (log2 units): the reference max m only moves when a block's max
+// exceeds it by more than kLazy, so p = 2^(score - m) <= 2^kLazy and the Value accumulators
+// are rescaled (folded) only a handful of times per segment.
+constexpr int kLazy = 3;
+constexpr int kEHead = 2;  // extra fixed-point headroom bits when the Value exponent is reset
+
+// binary16 pair {scale (lo), min (hi)} of a meta word -> fp32
+__device__ __forceinline__ float2 meta_pair(uint32_t m) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&m));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -96,18 +114,28 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// D += A (u8, 16x32) * B (s8, 32x8), int32 (exact)
+__device__ __forceinline__ void imma_us(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// D += A (u8, 16x32) * B (u8, 32x8), int32 (exact)
+__device__ __forceinline__ void imma_uu(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 __device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, const void* row_addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];\n"
                : "=r"(b0), "=r"(b1)
                : "r"(smem_u32(row_addr)));
-}
-
-// (a & MASK) | c in one LOP3 (MASK as the immediate, the magic in a register)
-template <uint32_t MASK>
-__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
-  return d;
 }
 
 // (2^10 + v_lo, 2^10 + v_hi) - 2^10 -> exact (v_lo, v_hi), normal fp16
@@ -115,121 +143,6 @@ __device__ __forceinline__ uint32_t sub_magic(uint32_t x) {
   __half2 v = *reinterpret_cast<__half2*>(&x);
   v = __hsub2(v, __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400)));
   return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// ---- unpack ---------------------------------------------------------------------------
-// Slots per 16-bit half: 16/B. With the class trick slot position p lives at bit offset
-// off(p) of either w (low positions) or w >> SH (high positions), giving value c * 2^off.
-template <int B>
-struct Cls;
-template <>
-struct Cls<2> {  // positions 0..4 from w (offsets 0,2,..,8), 5..7 from w >> 10
-  static constexpr int SPH = 8;
-  __host__ __device__ static constexpr int split() { return 5; }
-  __host__ __device__ static constexpr int sh() { return 10; }
-  __host__ __device__ static constexpr int off(int p) { return 2 * (p < 5 ? p : p - 5); }
-};
-template <>
-struct Cls<4> {  // positions 0,1 from w (offsets 0,4), 2,3 from w >> 8
-  static constexpr int SPH = 4;
-  __host__ __device__ static constexpr int split() { return 2; }
-  __host__ __device__ static constexpr int sh() { return 8; }
-  __host__ __device__ static constexpr int off(int p) { return 4 * (p < 2 ? p : p - 2); }
-};
-template <>
-struct Cls<3> {  // 2-bit low plane at positions 0..3 of w / w >> 8 (hi bit lands at off+2 <= 8)
-  static constexpr int SPH = 8;
-  __host__ __device__ static constexpr int split() { return 4; }
-  __host__ __device__ static constexpr int sh() { return 8; }
-  __host__ __device__ static constexpr int off(int p) { return 2 * (p < 4 ? p : p - 4); }
-};
-
-template <int B, int NS>
-struct Unpacker {
-  // class trick valid iff the offset depends on the slot only: NS % SPH == 0
-  static constexpr bool kClass = (NS % Cls<B>::SPH) == 0;
-  // exponent of the power of two carried by slot s (the bit offset of its codes)
-  __host__ __device__ static constexpr int exp_of_slot(int s) { return kClass ? Cls<B>::off(s % Cls<B>::SPH) : 0; }
-  // Codes at offset >= kSubMin are handed to the tensor core as fp16 SUBNORMALS (exponent
-  // field 0, value c * 2^(off-24), one LOP3): HMMA consumes subnormal inputs exactly but
-  // aligns their products to the nominal 2^-14 exponent, so codes with many leading zeros
-  // lose product bits (profiles/probes/hmma_hilo_prec.cu: 1e-6 vs 2e-8 relative). Low
-  // offsets therefore use the exact magic form (OR 2^10, subtract 2^10 -> c * 2^off,
-  // LOP3 + HADD2), high offsets (>= 4, at most 4 leading zeros) the subnormal form.
-  static constexpr int kSubMin = 4;
-  // power-of-two factor of the operand value relative to the code: 2^(off) or 2^(off-24)
-  __host__ __device__ static constexpr bool is_sub(int s) { return kClass && B != 3 && exp_of_slot(s) >= kSubMin; }
-  __host__ __device__ static constexpr int val_exp_of_slot(int s) { return exp_of_slot(s) - (is_sub(s) ? 24 : 0); }
-  // some slot is subnormal (then the Key GEMV keeps magic and subnormal slots in separate
-  // accumulator chains and joins them as chain_magic + 2^24 * chain_sub)
-  static constexpr bool kHasSub = kClass && B != 3 && Cls<B>::off(Cls<B>::SPH - 1) >= kSubMin;
-
-  __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
-    const int vs = r * NS + s;
-    if constexpr (B == 3) {
-      // low 2 bits from the 2-bit plane w[0..NS/2), high bit from the 1-bit plane w[NS/2..)
-      const uint32_t hw = w[NS / 2 + (vs >> 4)];
-      const int hb = vs & 15;  // bit of the high plane in each half
-      if constexpr (kClass) {
-        const int p = vs & 7;
-        const int o = Cls<3>::off(p);
-        const uint32_t lw = p < Cls<3>::split() ? w[vs >> 3] : (w[vs >> 3] >> Cls<3>::sh());
-        const int tgt = o + 2;
-        const uint32_t hs = hb >= tgt ? (hw >> (hb - tgt)) : (hw << (tgt - hb));
-        return sub_magic((lw & (0x00030003u << o)) | (hs & (0x00010001u << tgt)) | 0x64006400u);
-      } else {
-        const uint32_t lo = (w[vs >> 3] >> (2 * (vs & 7))) & 0x00030003u;
-        const uint32_t hi = (hw >> hb) & 0x00010001u;
-        return sub_magic(lo | (hi << 2) | 0x64006400u);
-      }
-    } else {
-      constexpr int SPH = Cls<B>::SPH;
-      constexpr uint32_t MASK = B == 2 ? 0x00030003u : 0x000F000Fu;
-      const uint32_t word = w[vs / SPH];
-      if constexpr (kClass) {
-        const int p = vs % SPH;
-        const uint32_t src = p < Cls<B>::split() ? word : (word >> Cls<B>::sh());
-        const int o = Cls<B>::off(p);
-        if (o >= kSubMin) return src & (MASK << o);  // subnormal operand
-        const uint32_t magic = 0x64006400u;
-        return sub_magic(o == 0 ? and_or<MASK>(src, magic) : and_or<(MASK << 2)>(src, magic));
-      } else {
-        return sub_magic(((word >> (B * (vs % SPH))) & MASK) | 0x64006400u);
-      }
-    }
-  }
-};
-
-// Lane's words of one tile in shared memory (layout: plane_addr in common.cuh).
-template <int B, int D>
-__device__ __forceinline__ void lds_tile(const uint32_t* tile, int lane, uint32_t* w) {
-  if constexpr (B == 3) {
-    lds_tile<2, D>(tile, lane, w);
-    lds_tile<1, D>(tile + 32 * (D / 32), lane, w + D / 32);
-  } else {
-    constexpr int WPL = D * B / 64;
-    if constexpr (WPL >= 4) {
-#pragma unroll
-      for (int c = 0; c < WPL / 4; ++c) {
-        const uint4 v = *reinterpret_cast<const uint4*>(tile + c * 128 + lane * 4);
-        w[4 * c] = v.x;
-        w[4 * c + 1] = v.y;
-        w[4 * c + 2] = v.z;
-        w[4 * c + 3] = v.w;
-      }
-    } else if constexpr (WPL == 2) {
-      const uint2 v = *reinterpret_cast<const uint2*>(tile + lane * 2);
-      w[0] = v.x;
-      w[1] = v.y;
-    } else {
-      w[0] = tile[lane];
-    }
-  }
-}
-
-template <int D, int B>
-constexpr int lane_words() {
-  return B == 3 ? D * 3 / 64 : D * B / 64;
 }
 
 __device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }
@@ -241,8 +154,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// (hi, lo) fp16 split of x packed as {hi | lo << 16}: x ~= hi + lo to ~22 bits. Two values
-// at a time through the packed converter (F2FP) instead of four scalar F2F on the XU pipe.
+// (hi, lo) fp16 split of x packed as {hi | lo << 16}: x ~= hi + lo to ~22 bits.
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& p0, uint32_t& p1) {
   const __half2 h = __floats2half2_rn(x0, x1);
   const float2 hf = __half22float2(h);
@@ -250,6 +162,63 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& p0, uint32_
   const uint32_t hu = *reinterpret_cast<const uint32_t*>(&h), lu = *reinterpret_cast<const uint32_t*>(&l);
   p0 = __byte_perm(hu, lu, 0x5410);
   p1 = __byte_perm(hu, lu, 0x7632);
+}
+
+// ---- 3-bit Keys (HMMA layout) --------------------------------------------------------
+// A fragment register = two codes at the same bit offset of the two 16-bit halves; the
+// 2-bit low plane holds positions 0..3 of w / w >> 8 (offsets 0,2,4,6; the high bit from
+// the 1-bit plane lands at offset + 2 <= 8). OR-ing 0x6400 (fp16 1024) and subtracting
+// 1024 gives code * 2^offset exactly; the power of two is folded into the B operand.
+struct K3Unpack {
+  __host__ __device__ static constexpr int off(int p) { return 2 * (p < 4 ? p : p - 4); }
+  template <int NS>
+  __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
+    const int vs = r * NS + s;
+    const uint32_t hw = w[NS / 2 + (vs >> 4)];
+    const int hb = vs & 15;
+    const int p = vs & 7;
+    const int o = off(p);
+    const uint32_t lw = p < 4 ? w[vs >> 3] : (w[vs >> 3] >> 8);
+    const int tgt = o + 2;
+    const uint32_t hs = hb >= tgt ? (hw >> (hb - tgt)) : (hw << (tgt - hb));
+    return sub_magic((lw & (0x00030003u << o)) | (hs & (0x00010001u << tgt)) | 0x64006400u);
+  }
+};
+
+// Lane's words of one tile in shared memory (layout: plane_addr in common.cuh).
+template <int WPL>
+__device__ __forceinline__ void lds_plane(const uint32_t* tile, int lane, uint32_t* w) {
+  if constexpr (WPL >= 4) {
+#pragma unroll
+    for (int c = 0; c < WPL / 4; ++c) {
+      const uint4 v = *reinterpret_cast<const uint4*>(tile + c * 128 + lane * 4);
+      w[4 * c] = v.x;
+      w[4 * c + 1] = v.y;
+      w[4 * c + 2] = v.z;
+      w[4 * c + 3] = v.w;
+    }
+  } else if constexpr (WPL == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(tile + lane * 2);
+    w[0] = v.x;
+    w[1] = v.y;
+  } else {
+    w[0] = tile[lane];
+  }
+}
+
+template <int D, int B>
+__device__ __forceinline__ void lds_tile(const uint32_t* tile, int lane, uint32_t* w) {
+  if constexpr (B == 3) {
+    lds_plane<D * 2 / 64>(tile, lane, w);
+    lds_plane<D / 64>(tile + 32 * (D * 2 / 64), lane, w + D * 2 / 64);
+  } else {
+    lds_plane<D * B / 64>(tile, lane, w);
+  }
+}
+
+template <int D, int B>
+constexpr int lane_words() {
+  return B == 3 ? D * 3 / 64 : D * B / 64;
 }
 
 struct MmaParams {
@@ -275,13 +244,11 @@ struct MmaParams {
 
 constexpr int kTailUnit = 8;  // full-precision-window tokens per work unit (~ one group's cost)
 
-// Dequantized packed element (token j < quantized, channel d) with compile-time D (gs is a
-// compile-time constant too when the kernel is instantiated with GS): the tail path's
-// per-element cost without runtime divisions.
+// Dequantized packed element (token j < quantized, channel d) with compile-time D.
 template <int D, bool KEY, int BITS>
 __device__ __forceinline__ float deq_lane(const SideView& s, int bh, int j, int d, int gs) {
   const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
-  const uint32_t code = tile_get(tile, KEY ? key_coord(j & 15, d) : value_coord(j & 15, d), D, BITS);
+  const uint32_t code = tile_get(tile, KEY, D, BITS, j & 15, d);
   uint32_t m;
   bool narrow = false;
   if (KEY) {
@@ -299,42 +266,47 @@ __device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, i
   return f16 ? tail_at<__half>(s, bh, j, d, D) : tail_at<float>(s, bh, j, d, D);
 }
 
-// Per-warp shared layout (bytes), dynamic:
-//   ring[S][stage_bytes] | bk[D][NB*8] half | bv[2][CGMAX][16][8] half | bp[2][16][8] half |
-//   bars[S] u64. B rows are 16 bytes (8 columns) so ldmatrix.trans yields the fragments.
-template <int D, int NB, int CGMAX>
+// Per-warp dynamic shared layout (bytes):
+//   ring[S][stage_bytes] | kstage | vbs[CGMAX][8][32] u8 | bars[S] u64
+// kstage: IMMA Keys: kbs[8 cols][4 t][NK][2] u32 (digit words of the B fragments);
+//         3-bit Keys: bk[D][NB*8] half (B rows for ldmatrix.trans).
+template <int D, int KB, int R>
 struct WarpLayout {
-  static constexpr int kBk = D * NB * 8 * 2;
-  static constexpr int kBv = 2 * CGMAX * 16 * 8 * 2;
-  static constexpr int kBp = 2 * 16 * 8 * 2;
-  static constexpr int kPV = kBv + kBp;
+  static constexpr int NCOL3 = 2 * R + 22 * R;
+  static constexpr int NB3 = (NCOL3 + 7) / 8;
+  static constexpr int kK = KB == 3 ? D * NB3 * 8 * 2 : 8 * 4 * (D / 32) * 2 * 4;
+  static constexpr int kV = (D / 32) * 8 * 32;
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
-    const size_t n = (size_t)stages * stage_bytes + kBk + kPV + (size_t)stages * 8;
+    const size_t n = (size_t)stages * stage_bytes + kK + kV + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
   }
 };
 
-// GS: 0 = runtime group size, else compile-time (32 is the KVmix default).
+// GS: 0 = runtime group size (a multiple of 32), else compile-time (32 is the KVmix default).
 template <int D, int KB, int VB, int R, int GS>
-__global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams p) {
-  constexpr int NS = D / 16;                   // k-steps (Keys) / m-tiles (Values)
+__global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_kernel(MmaParams p) {
+  static_assert(D == 64 || D == 128, "IMMA attention handles D in {64, 128}");
+  static_assert(VB == 2 || VB == 4, "Values: 2 or 4 bits");
+  static_assert(R == 1 || R == 2, "one or two query rows per KV head");
+  constexpr bool K3 = KB == 3;
+  static_assert(!K3 || D == 128, "3-bit Keys: D = 128");
+  constexpr int NK = D / 32;                   // Key k-steps (32 channels)
+  constexpr int NM = D / 16;                   // Value m-tiles (16 channels)
+  constexpr int NS3 = D / 16;                  // 3-bit Keys: HMMA k-steps
   constexpr int KW = lane_words<D, KB>();      // words per lane, Key tile
   constexpr int VW = lane_words<D, VB>();      // words per lane, Value tile
-  constexpr int LC = D / 32;                   // channels per lane for meta / q / tail
-  constexpr bool K3 = KB == 3;
-  constexpr int NCOL = 2 * R + (K3 ? 22 * R : 0);
-  constexpr int NB = (NCOL + 7) / 8;           // 8-column MMA blocks for the Key GEMV
-  constexpr int CGMAX = GS ? D / GS : 8;       // channel groups held in the P.V staging
-  using WL = WarpLayout<D, NB, CGMAX>;
-  using UK = Unpacker<KB, NS>;
-  using UV = Unpacker<VB, NS>;
-  static_assert(!K3 || R <= 2, "3-bit Keys support up to 2 query rows per KV head");
-  // bias MMA A operand straight from the staged Value meta rows (16 B = 4 groups per token)
-  constexpr bool kMetaRows = GS != 0 && D / (GS ? GS : 1) == 4;
+  constexpr int CK = K3 ? 1 : 8 / KB;          // classes per byte
+  constexpr int CV = 8 / VB;
+  constexpr uint32_t KMASK = KB == 4 ? 0x0F0F0F0Fu : 0x03030303u;
+  constexpr uint32_t VMASK = VB == 4 ? 0x0F0F0F0Fu : 0x03030303u;
+  constexpr int LC = D / 32;                   // channels per lane (tail path / epilogue)
+  constexpr int QL = D / 4;                    // lanes with a distinct Key channel quad
+  constexpr int CGMAX = D / 32;                // channel groups of a token (gs >= 32)
+  using WL = WarpLayout<D, KB, R>;
+  constexpr int NB3 = WL::NB3;
 
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float s_acc[kMmaWarps][R][D];
-  __shared__ float s_bias[kMmaWarps][R][8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wg = blockIdx.x * kMmaWarps + warp;  // warps are independent: no CTA barriers
@@ -343,22 +315,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   const int G = p.Hq / p.H;
   const int gs = GS ? GS : p.gs;
   const int CG = GS ? D / GS : p.cg;
-  const int TPG = gs / 16;  // tiles per group
+  const int NBLK = gs / 32;  // 32-token blocks per group
   const int S = p.stages;
   const int u_beg = (int)((int64_t)wg * p.N / p.W), u_end = (int)((int64_t)(wg + 1) * p.N / p.W);
 
   uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
   uint8_t* ring = wbase;
-  __half* bk = reinterpret_cast<__half*>(ring + (size_t)S * p.stage_bytes);            // [D][NB*8]
-  uint8_t* pv = reinterpret_cast<uint8_t*>(bk) + WL::kBk;
-  uint4(*bv)[CGMAX][16] = reinterpret_cast<uint4(*)[CGMAX][16]>(pv);          // [tile][cg][token] -> 8 cols
-  uint4(*bp)[16] = reinterpret_cast<uint4(*)[16]>(pv + WL::kBv);              // [tile][token] -> 8 cols
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pv + WL::kPV);
+  uint8_t* kstage = ring + (size_t)S * p.stage_bytes;
+  uint32_t* kbs = reinterpret_cast<uint32_t*>(kstage);
+  __half* bk = reinterpret_cast<__half*>(kstage);
+  uint8_t* vbs = kstage + WL::kK;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vbs + WL::kV);
 
-  // zero the B staging (columns of absent query rows must stay 0)
+  // zero the B staging (columns of absent query rows / digits must stay 0)
   {
-    uint4* z = reinterpret_cast<uint4*>(bk);
-    for (int i = lane; i < (WL::kBk + WL::kPV) / 16; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    uint4* z = reinterpret_cast<uint4*>(kstage);
+    for (int i = lane; i < (WL::kK + WL::kV) / 16; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -366,65 +338,56 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
   }
   __syncwarp();
 
-  const bool row_ok = t < p.rows;
+  // this lane's softmax row: lanes t = 2r, 2r+1 hold row r (IMMA score columns 4r .. 4r+3)
+  const int my_r = t >> 1;
+  const bool row_ok = my_r < p.rows;
   const uint64_t policy = evict_first_policy();
 
   // producer: this warp's fast groups in work-list order, issued S ahead of the consumer
-  int i_bh = u_beg / p.U, i_g = u_beg - i_bh * p.U;
-  if (i_g >= p.Gf) {
-    ++i_bh;
-    i_g = 0;
+  // (running record pointer, groups left in the current (b, kv-head), groups left to issue)
+  const uint8_t* src_rec;
+  int left_bh, left_all;
+  {
+    int i_bh = u_beg / p.U, i_g = u_beg - i_bh * p.U;
+    if (i_g >= p.Gf) {
+      ++i_bh;
+      i_g = 0;
+    }
+    src_rec = reinterpret_cast<const uint8_t*>(p.k.tiles) + ((size_t)i_bh * p.Grec + i_g) * p.stage_bytes;
+    left_bh = p.Gf - i_g;
+    // fast groups of [u_beg, u_end): whole (b, kv-head) ranges clipped at both ends
+    const int bh0 = u_beg / p.U, bh1 = (u_end - 1) / p.U;
+    int n = 0;
+    for (int x = bh0; x <= bh1; ++x) {
+      const int a = max(u_beg - x * p.U, 0), z = min(u_end - x * p.U, p.Gf);
+      n += max(z - a, 0);
+    }
+    left_all = n;
   }
+  const size_t skip_bytes = (size_t)(p.Grec - p.Gf) * p.stage_bytes;
   auto issue_next = [&](int s) {
-    if (p.Gf > 0 && i_bh * p.U + i_g < u_end) {
+    if (left_all > 0) {
       if (lane == 0) {
-        // the group's record (K tiles | V tiles | V meta | K meta) is one contiguous range
-        const uint32_t* src = p.k.tiles + ((size_t)i_bh * p.Grec + i_g) * (p.stage_bytes / 4);
         mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
-        bulk_g2s(ring + (size_t)s * p.stage_bytes, src, p.stage_bytes, &bars[s], policy);
+        bulk_g2s(ring + (size_t)s * p.stage_bytes, src_rec, p.stage_bytes, &bars[s], policy);
       }
-      if (++i_g == p.Gf) {
-        ++i_bh;
-        i_g = 0;
+      --left_all;
+      src_rec += p.stage_bytes;
+      if (--left_bh == 0) {
+        src_rec += skip_bytes;
+        left_bh = p.Gf;
       }
     }
   };
   for (int s = 0; s < S; ++s) issue_next(s);
 
-  float accv[NS][4];
-  float accb[4];
-  float m_run, l_run;  // row t (threads with t < rows)
-  double cs;
-
-  auto rescale = [&](float alpha) {
-    if (__any_sync(0xffffffffu, alpha != 1.0f)) {
-#pragma unroll
-      for (int i = 0; i < NS; ++i) {
-        accv[i][0] *= alpha;
-        accv[i][1] *= alpha;
-        accv[i][2] *= alpha;
-        accv[i][3] *= alpha;
-      }
-      accb[0] *= alpha;
-      accb[1] *= alpha;
-      accb[2] *= alpha;
-      accb[3] *= alpha;
-    }
-  };
-
-  // channel group of each Value m-tile
-  int cg_of[NS];
-#pragma unroll
-  for (int mt = 0; mt < NS; ++mt) cg_of[mt] = (mt * 16) / gs;
-
-  // the k-step of this lane's channels and the power of two its A codes carry
-  float cls_scale = 1.f;
-  {
-    const int kk = (lane * LC) / 16;
-#pragma unroll
-    for (int x = 0; x < NS; ++x)
-      if (x == kk) cls_scale = pow2i(-UK::exp_of_slot(x));
-  }
+  // Key B-build mapping: lane owns channels 4*Lq .. 4*Lq+3 (IMMA: one B register's k rows)
+  const int Lq = lane % QL;
+  const bool qdup = lane >= QL;  // D = 64: lanes 16..31 mirror 0..15
+  const int kkL = Lq >> 3, hL = (Lq & 7) >> 2, tL = Lq & 3;
+  const float clsL = K3 ? 1.f : pow2i(-KB * ((kkL + NK * hL) % CK));
+  // 3-bit Keys: power of two of this lane's k-step slot (HMMA layout)
+  const float cls3 = K3 ? pow2i(-K3Unpack::off(((lane * LC) / 16) % 8)) : 1.f;
 
   int s = 0;
   uint32_t phase = 0;
@@ -436,321 +399,455 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
     u = bh * p.U + hi;
     const int b = bh / p.H, h = bh % p.H;
 
-    // query rows: lane owns channels [lane*LC, lane*LC+LC)
-    float qv[R][LC];
+    // query rows at this lane's Key channels
+    float qv[R][4];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int rr = r < p.rows ? r : 0;
       const int gi = rr / p.tq, qi = rr % p.tq;
-      const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
+      const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + 4 * Lq;
 #pragma unroll
-      for (int c = 0; c < LC; ++c) {
+      for (int c = 0; c < 4; ++c) {
         const float x = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
         qv[r][c] = r < p.rows ? x : 0.f;
       }
     }
-    m_run = -INFINITY;
-    l_run = 0.f;
+    float qc[R][4];  // q * 2^-(b class) of this lane's Key channels
 #pragma unroll
-    for (int i = 0; i < NS; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0.f;
-    accb[0] = accb[1] = accb[2] = accb[3] = 0.f;
-    cs = 0.0;
-
-  const int g_stop = min(hi, p.Gf);
-  for (int grp = lo; grp < g_stop; ++grp) {
-    mbar_wait(&bars[s], phase);
-    const uint8_t* st = ring + (size_t)s * p.stage_bytes;
-    const uint32_t* kt = reinterpret_cast<const uint32_t*>(st);
-    const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + p.kt_bytes);
-    const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes);
-    const uint32_t* km = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes + p.vm_bytes);
-
-    // ---- Key group: B operand (q*s split hi/lo, pre-scaled by 2^(e - class) per row) ----
-    float beta[R], inv_sig[R];
-    {
-      float sc[LC], mn[LC];
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int c = 0; c < LC; ++c) {
-        const uint32_t m = km[lane * LC + c];
-        sc[c] = meta_scale(m);
-        mn[c] = meta_min(m);
-      }
-      int tau[LC];
-      if constexpr (K3) {
-        const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
-        const int nmod = inf.x % 11, omod = inf.y % 11;
+      for (int c = 0; c < 4; ++c) qc[r][c] = qv[r][c] * clsL;
+    float m_run = -INFINITY, l_run = 0.f;  // row my_r (lazy reference max, log2 units)
+    double cs = 0.0;
+    int accv[NM][4];
 #pragma unroll
-        for (int c = 0; c < LC; ++c) {
-          const int cmod = (int)(((unsigned)bh * D + lane * LC + c) % 11u);
-          const int phi = (cmod * nmod + omod) % 11;  // stream index % 11 of the group's first token
-          tau[c] = (21 - phi) % 11;                   // narrow tokens: t = tau (mod 11)
-        }
-      }
-      uint32_t row[LC][NB * 4];  // this lane's B rows (channel-major), packed half2
+    for (int i = 0; i < NM; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0;
+    float bias[R][CGMAX];
 #pragma unroll
-      for (int c = 0; c < LC; ++c)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int j = 0; j < NB * 4; ++j) row[c][j] = 0u;
+      for (int c = 0; c < CGMAX; ++c) bias[r][c] = 0.f;
+    int e_cur = 0;      // Value fixed-point exponent
+    int nacc = 0;       // blocks in the int32 Value accumulators
+    bool dirty = false;  // s_acc / accumulators / bias hold something
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float qs[LC], mx = 0.f, bt = 0.f;
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int c = 0; c < LC; ++c) {
-          qs[c] = qv[r][c] * sc[c];
-          mx = fmaxf(mx, fabsf(qs[c]));
-          bt = fmaf(qv[r][c], mn[c], bt);
-          if constexpr (K3) mx = fmaxf(mx, fabsf(qv[r][c] * (wide_scale(sc[c]) - sc[c])));
-        }
-        // max over the warp on the (non-negative) float bits: one REDUX
-        const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
-        // sigma = 2^(14 - floor(log2 max|qs|)): max|qs*sigma| in [2^14, 2^15)
-        const int e = (int)((mxu >> 23) & 0xffu);
-        const int se = min(max(268 - e, 1), 254);
-        inv_sig[r] = __int_as_float((254 - se) << 23);  // 1 / sigma
-        const float sgc = __int_as_float(se << 23) * cls_scale;
-#pragma unroll
-        for (int c = 0; c < LC; c += 2) split2(qs[c] * sgc, qs[c + 1] * sgc, row[c][r], row[c + 1][r]);
-        if constexpr (K3) {
-#pragma unroll
-          for (int c = 0; c < LC; ++c) {
-            const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc;
-            const __half yh = __float2half_rn(y);
-            const __half yl = __float2half_rn(y - __half2float(yh));
-            const uint32_t yp = (uint32_t)__half_as_ushort(yh) | ((uint32_t)__half_as_ushort(yl) << 16);
-#pragma unroll
-            for (int xr = 0; xr < 11; ++xr) row[c][R + r * 11 + xr] = tau[c] == xr ? yp : 0u;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
-        beta[r] = bt;
-      }
-      __syncwarp();  // previous group's ldmatrix reads of bk are done
-#pragma unroll
-      for (int c = 0; c < LC; ++c) {
-        uint32_t* dst = reinterpret_cast<uint32_t*>(bk + (size_t)(lane * LC + c) * NB * 8);
-        if constexpr (K3) {
-#pragma unroll
-          for (int j = 0; j < NB; ++j)
-            reinterpret_cast<uint4*>(dst)[j] = make_uint4(row[c][4 * j], row[c][4 * j + 1], row[c][4 * j + 2], row[c][4 * j + 3]);
-        } else {
-          // columns of absent rows stay zero from the kernel prologue
-#pragma unroll
-          for (int j = 0; j < R; ++j) dst[j] = row[c][j];
-        }
-      }
-    }
+      for (int c = 0; c < LC; ++c) s_acc[warp][r][lane * LC + c] = 0.f;
     __syncwarp();
-    float my_beta = beta[0], my_isig = inv_sig[0];
-#pragma unroll
-    for (int r = 1; r < R; ++r) {
-      if (t == r) {
-        my_beta = beta[r];
-        my_isig = inv_sig[r];
-      }
-    }
 
-    // ---- the group's tiles, two at a time (independent MMA chains, one softmax round) ----
-    for (int tp = 0; tp < TPG; tp += 2) {
-      uint32_t kw[2][KW], vw[2][VW];
+    // Fold the int32 Value accumulators into s_acc (fp32): s_acc = (s_acc + acc 2^-E) alpha.
+    // Lane (g, t) holds digit columns 2t, 2t+1 (row t >> 1) of channels 16 mt + g (+8).
+    auto flush = [&](float alpha) {
+      const float w0 = pow2i(16 * (t & 1) - e_cur);
+      const float w1 = w0 * 256.f;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        lds_tile<KB, D>(kt + (size_t)(tp + u) * tile_words(D, KB), lane, kw[u]);
-        lds_tile<VB, D>(vt + (size_t)(tp + u) * tile_words(D, VB), lane, vw[u]);
-      }
-      // scores: K (16 tokens x D) . B, both tiles
-      // NB == 1: two accumulator chains per tile (magic / subnormal slots, else even / odd
-      // k-steps) halve the HMMA dependency chain; NB > 1 already has NB independent chains
-      constexpr int NCH = NB == 1 ? 2 : 1;
-      float dk[2][NB * NCH][4];
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int nb = 0; nb < NB * NCH; ++nb) dk[u][nb][0] = dk[u][nb][1] = dk[u][nb][2] = dk[u][nb][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < NS; ++kk) {
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          uint32_t b0, b1;
-          ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB * 8 + nb * 8);
-          const int acc = NCH == 2 ? (UK::kHasSub ? (UK::is_sub(kk) ? 1 : 0) : (kk & 1)) : nb;
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            mma16816(dk[u][acc], UK::frag(kw[u], 0, kk), UK::frag(kw[u], 1, kk), UK::frag(kw[u], 2, kk),
-                     UK::frag(kw[u], 3, kk), b0, b1);
+      for (int mt = 0; mt < NM; ++mt) {
+        const float c0 = pow2i(-VB * (mt % CV)), c1 = pow2i(-VB * ((mt + NM) % CV));
+        float f0 = fmaf((float)accv[mt][1], w1, (float)accv[mt][0] * w0) * c0;
+        float f1 = fmaf((float)accv[mt][3], w1, (float)accv[mt][2] * w0) * c1;
+        f0 += __shfl_xor_sync(0xffffffffu, f0, 1);
+        f1 += __shfl_xor_sync(0xffffffffu, f1, 1);
+        if ((t & 1) == 0 && my_r < R) {
+          float* a = &s_acc[warp][my_r][16 * mt + g];
+          a[0] = (a[0] + f0) * alpha;  // accumulated with the old max
+          a[8] = (a[8] + f1) * alpha;
         }
+        accv[mt][0] = accv[mt][1] = accv[mt][2] = accv[mt][3] = 0;
       }
-      if constexpr (NCH == 2) {
+      nacc = 0;
+    };
+
+    const int g_stop = min(hi, p.Gf);
+    for (int grp = lo; grp < g_stop; ++grp) {
+      mbar_wait(&bars[s], phase);
+      const uint8_t* st = ring + (size_t)s * p.stage_bytes;
+      const uint32_t* kt = reinterpret_cast<const uint32_t*>(st);
+      const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + p.kt_bytes);
+      const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes);
+      const uint32_t* km = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes + p.vm_bytes);
+
+      // ---- Key group: B operand ---------------------------------------------------------
+      float betaL;       // sum_d q_d m_d of row my_r, scaled to log2 units
+      float wsc0, wsc1;  // IMMA: weights of this lane's two score columns (log2 units)
+      uint32_t kb[NK][2];
+      float isig3[R], beta3[R];
+      {
+        const uint4 m4 = *reinterpret_cast<const uint4*>(km + 4 * Lq);
+        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+        float sc[4], mn[4];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int c = 0; c < 4; ++c) {
+          const float2 f = meta_pair(mw[c]);
+          sc[c] = f.x;
+          mn[c] = f.y;
+        }
+        float beta[R], isig[R];
+        if constexpr (!K3) {
+          __syncwarp();  // previous group's reads of kbs are done
 #pragma unroll
-          for (int e = 0; e < 4; ++e) dk[u][0][e] = fmaf(UK::kHasSub ? 16777216.f : 1.f, dk[u][1][e], dk[u][0][e]);
-      }
-      float sa[2], sb[2];  // row t: token g / token g+8 of each tile
-      if constexpr (K3) {
-        // residue-class corrections without shared memory: for token row x the column pair
-        // of residue class (tile*16 + row) % 11 lives in lane (row, t_src); every lane of
-        // row `g` computes the same source, so the source lane itself knows which register
-        // block to expose, and one shuffle per (row, query row) delivers it.
+          for (int r = 0; r < R; ++r) {
+            float x[4], mx = 0.f, bt = 0.f;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+            for (int c = 0; c < 4; ++c) {
+              x[c] = qc[r][c] * sc[c];
+              mx = fmaxf(mx, fabsf(x[c]));
+              bt = fmaf(qv[r][c], mn[c], bt);
+            }
+            if (qdup) bt = 0.f;
+            // sigma = 2^(29 - floor(log2 max|x|)): max|x sigma| in [2^29, 2^30)
+            const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+            const int e = (int)((mxu >> 23) & 0xffu);
+            const int se = min(max(283 - e, 1), 254);
+            isig[r] = __int_as_float((254 - se) << 23);
+            const float sg = __int_as_float(se << 23);
+            uint32_t uu[4];
 #pragma unroll
-          for (int hlf = 0; hlf < 2; ++hlf) {  // token g, then token g+8
-            const int x = ((tp + u) * 16 + g + 8 * hlf) % 11;
-            float tot = 0.f;
+            for (int c = 0; c < 4; ++c) uu[c] = ((uint32_t)__float2int_rn(x[c] * sg) + 0x80808080u) ^ 0x80808080u;
+            // 4x4 byte transpose: word n = digit n of the four channels (balanced s8)
+            const uint32_t lo01 = __byte_perm(uu[0], uu[1], 0x5140), hi01 = __byte_perm(uu[0], uu[1], 0x7362);
+            const uint32_t lo23 = __byte_perm(uu[2], uu[3], 0x5140), hi23 = __byte_perm(uu[2], uu[3], 0x7362);
+            if (!qdup) {
+              uint32_t* dst = kbs + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL;
+              dst[0] = __byte_perm(lo01, lo23, 0x5410);
+              dst[4 * 2 * NK] = __byte_perm(lo01, lo23, 0x7632);
+              dst[8 * 2 * NK] = __byte_perm(hi01, hi23, 0x5410);
+              dst[12 * 2 * NK] = __byte_perm(hi01, hi23, 0x7632);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
+            beta[r] = bt;
+          }
+          __syncwarp();
+          // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column g (digit g%4 of row g/4)
+          const uint32_t* src = kbs + (g * 4 + t) * (2 * NK);
+#pragma unroll
+          for (int kk = 0; kk < NK; kk += 2) {
+            const uint4 v = *reinterpret_cast<const uint4*>(src + 2 * kk);
+            kb[kk][0] = v.x;
+            kb[kk][1] = v.y;
+            kb[kk + 1][0] = v.z;
+            kb[kk + 1][1] = v.w;
+          }
+          const int rr = my_r < R ? my_r : 0;
+          float is = isig[0], bb = beta[0];
+#pragma unroll
+          for (int r = 1; r < R; ++r)
+            if (rr == r) {
+              is = isig[r];
+              bb = beta[r];
+            }
+          wsc0 = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
+          wsc1 = wsc0 * 256.f;
+          betaL = bb * p.inv * kLog2e;
+        } else {
+          // 3-bit Keys: fp16 hi/lo B rows (pre-scaled by 2^(e - class)) + residue columns
+          int tau[4];
+          {
+            const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
+            const int nmod = inf.x % 11, omod = inf.y % 11;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int cmod = (int)(((unsigned)bh * D + lane * 4 + c) % 11u);
+              const int phi = (cmod * nmod + omod) % 11;  // stream index % 11 of the group's first token
+              tau[c] = (21 - phi) % 11;                   // narrow tokens: t = tau (mod 11)
+            }
+          }
+          float sgc[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float mx = 0.f, bt = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              mx = fmaxf(mx, fabsf(qv[r][c] * sc[c]));
+              mx = fmaxf(mx, fabsf(qv[r][c] * (wide_scale(sc[c]) - sc[c])));
+              bt = fmaf(qv[r][c], mn[c], bt);
+            }
+            const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+            const int e = (int)((mxu >> 23) & 0xffu);
+            const int se = min(max(268 - e, 1), 254);  // max|qs*sigma| in [2^14, 2^15)
+            isig3[r] = __int_as_float((254 - se) << 23);
+            sgc[r] = __int_as_float(se << 23) * cls3;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
+            beta3[r] = bt;
+          }
+          __syncwarp();  // previous group's ldmatrix reads of bk are done
+          // B row of channel lane*4 + c: {hi | lo << 16} of q s sigma per row, then the
+          // residue-class columns (only column tau_c is non-zero)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t row[NB3 * 4];
+#pragma unroll
+            for (int jj = 0; jj < NB3 * 4; ++jj) row[jj] = 0u;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              const int col = 2 * R + (r * 11 + x) * 2;     // even: hi, odd: lo
-              const int nb = col >> 3, tsrc = (col & 7) >> 1;
-              float mine = 0.f;                              // this lane's (hi+lo) in block nb
+              const float x = qv[r][c] * sc[c] * sgc[r];
+              const __half xh = __float2half_rn(x);
+              const __half xl = __float2half_rn(x - __half2float(xh));
+              row[r] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(xl) << 16);
+              const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc[r];
+              const __half yh = __float2half_rn(y);
+              const __half yl = __float2half_rn(y - __half2float(yh));
+              const uint32_t yp = (uint32_t)__half_as_ushort(yh) | ((uint32_t)__half_as_ushort(yl) << 16);
 #pragma unroll
-              for (int q = 0; q < NB; ++q)
-                if (q == nb) mine = dk[u][q][2 * hlf] + dk[u][q][2 * hlf + 1];
-              const float corr = __shfl_sync(0xffffffffu, mine, g * 4 + tsrc);
-              if (r == t) tot = corr;
+              for (int xr = 0; xr < 11; ++xr) row[R + r * 11 + xr] = tau[c] == xr ? yp : 0u;
             }
-            const float mainv = dk[u][0][2 * hlf] + dk[u][0][2 * hlf + 1];
-            if (hlf == 0) sa[u] = mainv + tot;
-            else sb[u] = mainv + tot;
+            uint4* dst = reinterpret_cast<uint4*>(bk + (size_t)(lane * 4 + c) * NB3 * 8);
+#pragma unroll
+            for (int jj = 0; jj < NB3; ++jj) dst[jj] = make_uint4(row[4 * jj], row[4 * jj + 1], row[4 * jj + 2], row[4 * jj + 3]);
           }
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          sa[u] = dk[u][0][0] + dk[u][0][1];
-          sb[u] = dk[u][0][2] + dk[u][0][3];
+          __syncwarp();
+          wsc0 = wsc1 = 0.f;
+          betaL = 0.f;
         }
       }
-      float la[2], lb[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        sa[u] = (sa[u] * my_isig + my_beta) * p.inv;
-        sb[u] = (sb[u] * my_isig + my_beta) * p.inv;
-        la[u] = sa[u] * kLog2e;
-        lb[u] = sb[u] * kLog2e;
-      }
-      if (p.want_cs && row_ok) cs += (double)((sa[0] + sb[0]) + (sa[1] + sb[1]));
-      float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-      const float m_new = fmaxf(m_run, tmax);
-      const float alpha = fast_exp2(m_run - m_new);
-      float pa[2], pb[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        pa[u] = row_ok ? fast_exp2(la[u] - m_new) : 0.f;
-        pb[u] = row_ok ? fast_exp2(lb[u] - m_new) : 0.f;
-      }
-      l_run = l_run * alpha + ((pa[0] + pb[0]) + (pa[1] + pb[1]));
-      m_run = m_new;
-      rescale(alpha);
 
-      // ---- P.V B operands: lane j -> token j of the 32 (tile j/16, row-in-tile j%16) ----
-      // each (token, group) row is 8 fp16 columns {hi_r, lo_r}: one 16-byte store per row
-      {
-        const int u = lane >> 4, i = lane & 15;
-        const uint32_t* vmt = vm + (size_t)(tp * 16 + lane) * CG;  // this token's Value meta
-        float vsc[CGMAX];
-        if constexpr (kMetaRows) {
-          const uint4 q4 = *reinterpret_cast<const uint4*>(vmt);
-          vsc[0] = meta_scale(q4.x);
-          vsc[1] = meta_scale(q4.y);
-          vsc[2] = meta_scale(q4.z);
-          vsc[3] = meta_scale(q4.w);
-        } else {
+      // ---- the group's 32-token blocks: 2 Key tiles + one Value k-step each ---------------
+      for (int blk = 0; blk < NBLK; ++blk) {
+        const uint32_t* kt2 = kt + (size_t)(2 * blk) * tile_words(D, KB);
+        const uint32_t* vt2 = vt + (size_t)(2 * blk) * tile_words(D, VB);
+        const uint32_t* vm2 = vm + (size_t)(32 * blk) * CG;
+        float la[2], lb[2];  // scores (log2 units) of tokens g / g+8 of tile u, row my_r
+        if constexpr (!K3) {
+          uint32_t kw[2][KW];
+          lds_tile<D, KB>(kt2, lane, kw[0]);
+          lds_tile<D, KB>(kt2 + tile_words(D, KB), lane, kw[1]);
+          int dk[2][4];
 #pragma unroll
-          for (int c = 0; c < CGMAX; ++c) vsc[c] = (GS || c < CG) ? meta_scale(vmt[c]) : 0.f;
-        }
-        uint32_t prow[4] = {0u, 0u, 0u, 0u};
-        uint32_t vrow[CGMAX][4];
+          for (int u2 = 0; u2 < 2; ++u2) dk[u2][0] = dk[u2][1] = dk[u2][2] = dk[u2][3] = 0;
 #pragma unroll
-        for (int c = 0; c < CGMAX; ++c) vrow[c][0] = vrow[c][1] = vrow[c][2] = vrow[c][3] = 0u;
+          for (int kk = 0; kk < NK; ++kk) {
+            const int q0 = kk, q1 = kk + NK;  // channel halves h = 0 / 1
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int src = (i & 7) * 4 + r;
-          const float x0 = __shfl_sync(0xffffffffu, pa[0], src);
-          const float x1 = __shfl_sync(0xffffffffu, pb[0], src);
-          const float x2 = __shfl_sync(0xffffffffu, pa[1], src);
-          const float x3 = __shfl_sync(0xffffffffu, pb[1], src);
-          const float pj = u == 0 ? (i < 8 ? x0 : x1) : (i < 8 ? x2 : x3);  // 0 for absent rows
-          float xs[CGMAX + 1];
-          xs[0] = pj;
-#pragma unroll
-          for (int c = 0; c < CGMAX; ++c) xs[c + 1] = pj * vsc[c];
-          uint32_t pk[CGMAX + 2];
-#pragma unroll
-          for (int c = 0; c < CGMAX + 1; c += 2) split2(xs[c], c + 1 <= CGMAX ? xs[c + 1] : 0.f, pk[c], pk[c + 1]);
-          prow[r] = pk[0];
-#pragma unroll
-          for (int c = 0; c < CGMAX; ++c) vrow[c][r] = pk[c + 1];
-        }
-        bp[u][i] = make_uint4(prow[0], prow[1], prow[2], prow[3]);
-#pragma unroll
-        for (int c = 0; c < CGMAX; ++c)
-          if (GS || c < CG) bv[u][c][i] = make_uint4(vrow[c][0], vrow[c][1], vrow[c][2], vrow[c][3]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        uint32_t pb0, pb1;
-        ldmatrix_x2_trans(pb0, pb1, &bp[u][lane & 15]);
-        // bias MMA: A rows = per-token meta halves, B = p
-        uint32_t a0 = 0u, a2 = 0u;
-        if constexpr (kMetaRows) {
-          // rows = {s0, m0, s1, m1, s2, m2, s3, m3} of the 16 tokens (ldmatrix.trans of the
-          // staged 16-byte meta rows): odd rows give sum_j m_jg p_j, even rows sum_j s_jg p_j
-          ldmatrix_x2_trans(a0, a2, vm + (size_t)((tp + u) * 16 + (lane & 15)) * CG);
-        } else {
-          const uint32_t* vmt = vm + (size_t)(tp + u) * 16 * CG;  // [16][CG]
-          if (g < CG) {
-            a0 = __byte_perm(vmt[(2 * t) * CG + g], vmt[(2 * t + 1) * CG + g], 0x7632);
-            a2 = __byte_perm(vmt[(2 * t + 8) * CG + g], vmt[(2 * t + 9) * CG + g], 0x7632);
+            for (int u2 = 0; u2 < 2; ++u2) {
+              const uint32_t a0 = kw[u2][(q0 / CK) * 2 + 0] & (KMASK << (KB * (q0 % CK)));
+              const uint32_t a1 = kw[u2][(q0 / CK) * 2 + 1] & (KMASK << (KB * (q0 % CK)));
+              const uint32_t a2 = kw[u2][(q1 / CK) * 2 + 0] & (KMASK << (KB * (q1 % CK)));
+              const uint32_t a3 = kw[u2][(q1 / CK) * 2 + 1] & (KMASK << (KB * (q1 % CK)));
+              imma_us(dk[u2], a0, a1, a2, a3, kb[kk][0], kb[kk][1]);
+            }
           }
-        }
-        mma16816(accb, a0, 0u, a2, 0u, pb0, pb1);
-        if constexpr (GS != 0) {
-          constexpr int CGC = D / GS;
-          uint32_t bf0[CGC], bf1[CGC];
 #pragma unroll
-          for (int c = 0; c < CGC; ++c) ldmatrix_x2_trans(bf0[c], bf1[c], &bv[u][c][lane & 15]);
-#pragma unroll
-          for (int mt = 0; mt < NS; ++mt) {
-            const int c = (mt * 16) / GS;
-            mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
-                     UV::frag(vw[u], 3, mt), bf0[c], bf1[c]);
+          for (int u2 = 0; u2 < 2; ++u2) {
+            float pa = fmaf((float)dk[u2][1], wsc1, (float)dk[u2][0] * wsc0);
+            float pb = fmaf((float)dk[u2][3], wsc1, (float)dk[u2][2] * wsc0);
+            pa += __shfl_xor_sync(0xffffffffu, pa, 1);
+            pb += __shfl_xor_sync(0xffffffffu, pb, 1);
+            la[u2] = pa + betaL;
+            lb[u2] = pb + betaL;
           }
         } else {
+          uint32_t kw[2][KW];
+          lds_tile<D, KB>(kt2, lane, kw[0]);
+          lds_tile<D, KB>(kt2 + tile_words(D, KB), lane, kw[1]);
+          // one tile at a time (the residue columns make the accumulator set wide)
+          float sa[2], sb[2];
+          float my_isig = isig3[0], my_beta = beta3[0];
 #pragma unroll
-          for (int mt = 0; mt < NS; ++mt) {
-            uint32_t b0, b1;
-            ldmatrix_x2_trans(b0, b1, &bv[u][cg_of[mt]][lane & 15]);
-            mma16816(accv[mt], UV::frag(vw[u], 0, mt), UV::frag(vw[u], 1, mt), UV::frag(vw[u], 2, mt),
-                     UV::frag(vw[u], 3, mt), b0, b1);
+          for (int r = 1; r < R; ++r)
+            if (t == r) {
+              my_isig = isig3[r];
+              my_beta = beta3[r];
+            }
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            float dk[NB3][4];
+#pragma unroll
+            for (int nb = 0; nb < NB3; ++nb) dk[nb][0] = dk[nb][1] = dk[nb][2] = dk[nb][3] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < NS3; ++kk) {
+              const uint32_t a0 = K3Unpack::frag<NS3>(kw[u2], 0, kk), a1 = K3Unpack::frag<NS3>(kw[u2], 1, kk);
+              const uint32_t a2 = K3Unpack::frag<NS3>(kw[u2], 2, kk), a3 = K3Unpack::frag<NS3>(kw[u2], 3, kk);
+#pragma unroll
+              for (int nb = 0; nb < NB3; ++nb) {
+                uint32_t b0, b1;
+                ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB3 * 8 + nb * 8);
+                mma16816(dk[nb], a0, a1, a2, a3, b0, b1);
+              }
+            }
+            // rows of lane t (HMMA column pairs), residue-class corrections by shuffle
+#pragma unroll
+            for (int hlf = 0; hlf < 2; ++hlf) {  // token g, then token g+8
+              const int x = ((2 * blk + u2) * 16 + g + 8 * hlf) % 11;
+              float tot = 0.f;
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const int col = 2 * R + (r * 11 + x) * 2;  // even: hi, odd: lo
+                const int nb = col >> 3, tsrc = (col & 7) >> 1;
+                float mine = 0.f;
+#pragma unroll
+                for (int qq = 0; qq < NB3; ++qq)
+                  if (qq == nb) mine = dk[qq][2 * hlf] + dk[qq][2 * hlf + 1];
+                const float corr = __shfl_sync(0xffffffffu, mine, g * 4 + tsrc);
+                if (r == t) tot = corr;
+              }
+              const float v = ((dk[0][2 * hlf] + dk[0][2 * hlf + 1] + tot) * my_isig + my_beta) * p.inv * kLog2e;
+              if (hlf == 0) sa[u2] = v;
+              else sb[u2] = v;
+            }
+          }
+          // to the IMMA convention: row r in lanes t = 2r, 2r+1
+          const int src = g * 4 + (my_r < R ? my_r : 0);
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            la[u2] = __shfl_sync(0xffffffffu, sa[u2], src);
+            lb[u2] = __shfl_sync(0xffffffffu, sb[u2], src);
           }
         }
-      }
-      __syncwarp();
-    }
-    // refill this stage S groups ahead
-    issue_next(s);
-    if (++s == S) {
-      s = 0;
-      phase ^= 1u;
-    }
-  }
+        if (p.want_cs && row_ok && (t & 1) == 0) cs += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);
 
-  // ---- tokens past the fast region: lane-parallel over channels ------------------------
-  // Every lane tracks all R rows (identical values across lanes); the Value contribution
-  // accumulates per lane for its LC channels and joins the fragments in the epilogue.
-  float acct[R][LC];
+        // ---- online softmax (row my_r) -----------------------------------------------------
+        float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+        const float m_new = tmax > m_run + (float)kLazy ? tmax : m_run;
+        const float alpha = fast_exp2(m_run - m_new);
+        float pa[2], pb[2];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+        for (int u2 = 0; u2 < 2; ++u2) {
+          pa[u2] = row_ok ? fast_exp2(la[u2] - m_new) : 0.f;
+          pb[u2] = row_ok ? fast_exp2(lb[u2] - m_new) : 0.f;
+        }
+        l_run = l_run * alpha + ((pa[0] + pb[0]) + (pa[1] + pb[1]));
+        m_run = m_new;
+
+        // ---- Value block: lane (g, t) owns token j = g + 8t of the 32 ---------------------
+        const int j = g + 8 * t;
+        float pr[R];  // p of token j for every row
+        {
+          const float mine = (t & 1) ? ((t >> 1) ? pb[1] : pb[0]) : ((t >> 1) ? pa[1] : pa[0]);
+          const float other = (t & 1) ? ((t >> 1) ? pb[0] : pb[1]) : ((t >> 1) ? pa[0] : pa[1]);
+          const float recv = __shfl_xor_sync(0xffffffffu, other, 2);  // partner t^2's token, my row
 #pragma unroll
-    for (int c = 0; c < LC; ++c) acct[r][c] = 0.f;
-  const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * kTailUnit;
-  const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * kTailUnit) : j_lo;
-  if (j_lo < j_hi) {
+          for (int r = 0; r < R; ++r) pr[r] = (r == my_r) ? mine : recv;
+        }
+        float sv[CGMAX], mv[CGMAX];
+        {
+          const uint32_t* vmt = vm2 + (size_t)j * CG;
+          if constexpr (GS != 0 && D / (GS ? GS : 1) == 4) {
+            const uint4 q4 = *reinterpret_cast<const uint4*>(vmt);
+            const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float2 f = meta_pair(w4[c]);
+              sv[c] = f.x;
+              mv[c] = f.y;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < CGMAX; ++c) {
+              const float2 f = meta_pair(c < CG ? vmt[c] : 0u);
+              sv[c] = f.x;
+              mv[c] = f.y;
+            }
+          }
+        }
+        // fixed-point exponent: max scale of the block * 2^E < 2^30 (p <= 1)
+        float smax = sv[0];
+#pragma unroll
+        for (int c = 1; c < CGMAX; ++c) smax = fmaxf(smax, sv[c]);
+        const uint32_t smu = __reduce_max_sync(0xffffffffu, __float_as_uint(smax));
+        // (p <= 2^kLazy): y = p s 2^E < 2^30 for E <= e_blk
+        const int e_blk = min(156 - kLazy - (int)((smu >> 23) & 0xffu), 100);
+        if (!dirty) {
+          e_cur = e_blk - kEHead;
+        } else {
+          const bool moved = __any_sync(0xffffffffu, row_ok && alpha != 1.0f);
+          if (moved || e_cur > e_blk || nacc >= kFlushBlocks) {
+            flush(alpha);
+            if (moved) {
+              const float ax = __shfl_xor_sync(0xffffffffu, alpha, 2);
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < CGMAX; ++c) bias[r][c] *= (r == my_r) ? alpha : ax;
+            }
+            e_cur = e_blk - kEHead;
+          }
+        }
+        dirty = true;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int c = 0; c < CGMAX; ++c) bias[r][c] = fmaf(pr[r], mv[c], bias[r][c]);
+        // B digits of y = p s 2^E (u8, four columns per row) -> vbs[c][4r + n][pos(j)]
+        {
+          const float pe = pow2i(e_cur);
+          float ppe[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) ppe[r] = pr[r] * pe;
+          const int pos = ((g >> 2) + 2 * (t & 1)) * 8 + (t >> 1) * 4 + (g & 3);
+#pragma unroll
+          for (int c = 0; c < CGMAX; ++c) {
+            if (GS == 0 && c >= CG) break;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const uint32_t v = (uint32_t)__float2int_rn(ppe[r] * sv[c]);
+              uint8_t* dst = vbs + c * 256 + (4 * r) * 32 + pos;
+              dst[0] = (uint8_t)v;
+              dst[32] = (uint8_t)(v >> 8);
+              dst[64] = (uint8_t)(v >> 16);
+              dst[96] = (uint8_t)(v >> 24);
+            }
+          }
+        }
+        __syncwarp();
+        {
+          uint32_t vw0[VW], vw1[VW];
+          lds_tile<D, VB>(vt2, lane, vw0);
+          lds_tile<D, VB>(vt2 + tile_words(D, VB), lane, vw1);
+          uint32_t vb[CGMAX][2];
+          if constexpr (GS != 0) {
+#pragma unroll
+            for (int c = 0; c < CGMAX; ++c) {
+              if (c < D / (GS ? GS : 1)) {
+                const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
+                vb[c][0] = x.x;
+                vb[c][1] = x.y;
+              }
+            }
+          }
+#pragma unroll
+          for (int mt = 0; mt < NM; ++mt) {
+            const int q0 = mt, q1 = mt + NM;
+            const uint32_t a0 = vw0[q0 / CV] & (VMASK << (VB * (q0 % CV)));
+            const uint32_t a1 = vw0[q1 / CV] & (VMASK << (VB * (q1 % CV)));
+            const uint32_t a2 = vw1[q0 / CV] & (VMASK << (VB * (q0 % CV)));
+            const uint32_t a3 = vw1[q1 / CV] & (VMASK << (VB * (q1 % CV)));
+            if constexpr (GS != 0) {
+              const int c = (mt * 16) / (GS ? GS : 1);
+              imma_uu(accv[mt], a0, a1, a2, a3, vb[c][0], vb[c][1]);
+            } else {
+              const int c = (mt * 16) / gs;
+              const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
+              imma_uu(accv[mt], a0, a1, a2, a3, x.x, x.y);
+            }
+          }
+        }
+        ++nacc;
+        __syncwarp();  // vbs is rewritten by the next block
+      }
+      // refill this stage S groups ahead
+      issue_next(s);
+      if (++s == S) {
+        s = 0;
+        phase ^= 1u;
+      }
+    }
+
+    // ---- end of the fast region: fold accumulators, gather the softmax state ------------
+    if (dirty) flush(1.0f);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < CGMAX; ++c) {
+        float x = bias[r][c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        bias[r][c] = x;
+      }
     float m_all[R], l_all[R];
     {
       float lr = l_run;
@@ -759,106 +856,121 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 4) attend_mma_kernel(MmaParams
       lr += __shfl_xor_sync(0xffffffffu, lr, 16);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        m_all[r] = __shfl_sync(0xffffffffu, m_run, r);  // lane r = (g 0, t r)
-        l_all[r] = __shfl_sync(0xffffffffu, lr, r);
+        m_all[r] = __shfl_sync(0xffffffffu, m_run, 2 * r);  // lane (g 0, t 2r)
+        l_all[r] = __shfl_sync(0xffffffffu, lr, 2 * r);
       }
     }
-    const int d0 = lane * LC;
-    for (int64_t j = j_lo; j < j_hi; ++j) {
-      float kx[LC], vx[LC];
-      if (j >= p.k.quantized) {
+    __syncwarp();
+    // lane-parallel accumulators over channels lane*LC .. lane*LC+LC-1
+    float acct[R][LC];
 #pragma unroll
-        for (int c = 0; c < LC; ++c) kx[c] = tail_val(p.k, p.tail16, bh, j - p.k.quantized, d0 + c, D);
-      } else {
-#pragma unroll
-        for (int c = 0; c < LC; ++c) kx[c] = deq_lane<D, true, KB>(p.k, bh, (int)j, d0 + c, gs);
-      }
-      if (j >= p.v.quantized) {
-#pragma unroll
-        for (int c = 0; c < LC; ++c) vx[c] = tail_val(p.v, p.tail16, bh, j - p.v.quantized, d0 + c, D);
-      } else {
-#pragma unroll
-        for (int c = 0; c < LC; ++c) vx[c] = deq_lane<D, false, VB>(p.v, bh, (int)j, d0 + c, gs);
-      }
-      float alpha_mine = 1.f;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float x = 0.f;
-#pragma unroll
-        for (int c = 0; c < LC; ++c) x = fmaf(qv[r][c], kx[c], x);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (r < p.rows) {
-          const float sc = x * p.inv;
-          if (p.want_cs && lane == 0) cs += (double)sc;
-          const float ls = sc * kLog2e;
-          const float m_new = fmaxf(m_all[r], ls);
-          const float alpha = exp2f(m_all[r] - m_new);
-          const float pj = exp2f(ls - m_new);
-          l_all[r] = l_all[r] * alpha + pj;
-          m_all[r] = m_new;
-#pragma unroll
-          for (int c = 0; c < LC; ++c) acct[r][c] = acct[r][c] * alpha + pj * vx[c];
-          if (t == r) alpha_mine = alpha;
-        }
-      }
-      rescale(alpha_mine);
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (t == r) {
-        m_run = m_all[r];
-        l_run = g == 0 ? l_all[r] : 0.f;
-      }
-    }
-  }
-
-  // ---- segment epilogue: this warp's partial for (b, kv-head) -> slot wg + bh ----------
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 8);
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
-  if (row_ok && t < R) {
-    // the Value fragments carry the per-m-tile power of two of their operands
-#pragma unroll
-    for (int mt = 0; mt < NS; ++mt) {
-      const float f = pow2i(-UV::val_exp_of_slot(mt));
-      s_acc[warp][t][mt * 16 + g] = (accv[mt][0] + accv[mt][1]) * f;
-      s_acc[warp][t][mt * 16 + g + 8] = (accv[mt][2] + accv[mt][3]) * f;
-    }
-    if constexpr (kMetaRows) {
-      if (g & 1) s_bias[warp][t][g >> 1] = accb[0] + accb[1];  // min rows
-    } else {
-      s_bias[warp][t][g] = accb[0] + accb[1];
-    }
-  }
-  __syncwarp();
-  const int64_t slot = (int64_t)wg + bh;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const float m_r = __shfl_sync(0xffffffffu, m_run, r);
-    const float l_r = __shfl_sync(0xffffffffu, l_run, r);
-    if (r < p.rows) {
-      const size_t pi = (size_t)slot * p.rows + r;
-      float o[LC];
+    for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
         const int d = lane * LC + c;
-        o[c] = s_acc[warp][r][d] + s_bias[warp][r][d / gs] + acct[r][c];
-      }
-      if constexpr (LC == 4) {
-        *reinterpret_cast<float4*>(p.part_acc + pi * D + lane * LC) = make_float4(o[0], o[1], o[2], o[3]);
-      } else {
+        float bsel = bias[r][0];
 #pragma unroll
-        for (int c = 0; c < LC; ++c) p.part_acc[pi * D + lane * LC + c] = o[c];
+        for (int cc = 1; cc < CGMAX; ++cc)
+          if (cc == d / gs) bsel = bias[r][cc];
+        acct[r][c] = s_acc[warp][r][d] + bsel;
       }
-      if (lane == 0) p.part_ml[pi] = make_float2(m_r == -INFINITY ? -INFINITY : m_r * kLn2, l_r);
+
+    // ---- tokens past the fast region: lane-parallel over channels ------------------------
+    const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * kTailUnit;
+    const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * kTailUnit) : j_lo;
+    if (j_lo < j_hi) {
+      const int d0 = lane * LC;
+      float qt[R][LC];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int rr = r < p.rows ? r : 0;
+        const int gi = rr / p.tq, qi = rr % p.tq;
+        const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + d0;
+#pragma unroll
+        for (int c = 0; c < LC; ++c)
+          qt[r][c] = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
+      }
+      // four tokens per round: all loads issued first, the four reductions interleaved
+      constexpr int TB = 4;
+      for (int64_t j0 = j_lo; j0 < j_hi; j0 += TB) {
+        float kx[TB][LC], vx[TB][LC];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          const int64_t jj = min(j0 + i, j_hi - 1);
+          if (jj >= p.k.quantized) {
+#pragma unroll
+            for (int c = 0; c < LC; ++c) kx[i][c] = tail_val(p.k, p.tail16, bh, jj - p.k.quantized, d0 + c, D);
+          } else {
+#pragma unroll
+            for (int c = 0; c < LC; ++c) kx[i][c] = deq_lane<D, true, KB>(p.k, bh, (int)jj, d0 + c, gs);
+          }
+          if (jj >= p.v.quantized) {
+#pragma unroll
+            for (int c = 0; c < LC; ++c) vx[i][c] = tail_val(p.v, p.tail16, bh, jj - p.v.quantized, d0 + c, D);
+          } else {
+#pragma unroll
+            for (int c = 0; c < LC; ++c) vx[i][c] = deq_lane<D, false, VB>(p.v, bh, (int)jj, d0 + c, gs);
+          }
+        }
+        float x[TB][R];
+#pragma unroll
+        for (int i = 0; i < TB; ++i)
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float a = 0.f;
+#pragma unroll
+            for (int c = 0; c < LC; ++c) a = fmaf(qt[r][c], kx[i][c], a);
+            x[i][r] = a;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < TB; ++i)
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[i][r] += __shfl_xor_sync(0xffffffffu, x[i][r], o);
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          if (j0 + i >= j_hi) break;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (r < p.rows) {
+              const float sc = x[i][r] * p.inv;
+              if (p.want_cs && lane == 0) cs += (double)sc;
+              const float ls = sc * kLog2e;
+              const float m_new = fmaxf(m_all[r], ls);
+              const float alpha = exp2f(m_all[r] - m_new);
+              const float pj = exp2f(ls - m_new);
+              l_all[r] = l_all[r] * alpha + pj;
+              m_all[r] = m_new;
+#pragma unroll
+              for (int c = 0; c < LC; ++c) acct[r][c] = acct[r][c] * alpha + pj * vx[i][c];
+            }
+          }
+        }
+      }
     }
-  }
-  if (p.want_cs) {
-    for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-    if (lane == 0) p.part_cs[slot] = cs;
-  }
-  __syncwarp();  // s_acc / s_bias are rewritten by the next segment
+
+    // ---- segment epilogue: this warp's partial for (b, kv-head) -> slot wg + bh ----------
+    const int64_t slot = (int64_t)wg + bh;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < p.rows) {
+        const size_t pi = (size_t)slot * p.rows + r;
+        if constexpr (LC == 4) {
+          *reinterpret_cast<float4*>(p.part_acc + pi * D + lane * LC) =
+              make_float4(acct[r][0], acct[r][1], acct[r][2], acct[r][3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < LC; ++c) p.part_acc[pi * D + lane * LC + c] = acct[r][c];
+        }
+        if (lane == 0) p.part_ml[pi] = make_float2(m_all[r] == -INFINITY ? -INFINITY : m_all[r] * kLn2, l_all[r]);
+      }
+    }
+    if (p.want_cs) {
+      for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+      if (lane == 0) p.part_cs[slot] = cs;
+    }
+    __syncwarp();  // s_acc is rewritten by the next segment
   }
 }
 
@@ -893,9 +1005,7 @@ __global__ void attend_combine_sk_kernel(const float2* __restrict__ part_ml, con
 
 template <int D, int KB, int VB, int R, int GS>
 int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
-  constexpr int NCOL = 2 * R + (KB == 3 ? 22 * R : 0);
-  constexpr int NB = (NCOL + 7) / 8;
-  using WL = WarpLayout<D, NB, GS ? D / GS : 8>;
+  using WL = WarpLayout<D, KB, R>;
   auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
   // ring depth: as many stages (2..4) as fit while keeping the highest CTA residency
   // the registers allow (4, else 3, else 2 CTAs per SM)
@@ -941,8 +1051,8 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
 
 template <int D, int KB, int VB, int R>
 int dispatch_gs(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
-  if constexpr (KB == 3 && R > 2) {
-    return 0;
+  if constexpr (KB == 3 && (D != 128 || R != 1)) {
+    return 0;  // 3-bit Keys with two rows: the residue columns spill; generic path
   } else {
     return p.gs == 32 ? launch<D, KB, VB, R, 32>(p, BH, ws, st) : launch<D, KB, VB, R, 0>(p, BH, ws, st);
   }
@@ -963,16 +1073,16 @@ int dispatch_bits(MmaParams& p, int kb, int vb, int BH, Workspace& ws, cudaStrea
 
 }  // namespace
 
-
 bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
                 Workspace& ws, cudaStream_t st) {
   const int rows = (Hq / c->H) * tq;
-  if (rows > 4) return false;
+  if (rows > 2) return false;
   const int kb = c->k.bits, vb = c->v.bits;
-  if (vb == 3 || (kb == 3 && rows > 2)) return false;
+  if (vb == 3) return false;
   const int D = c->D, gs = c->cfg.group_size;
-  if (gs % 32 != 0) return false;  // groups are processed two tiles at a time
+  if (gs % 32 != 0) return false;  // groups are processed in 32-token blocks
   if (D != 64 && D != 128) return false;
+  if (kb == 3 && (D != 128 || rows != 1)) return false;
   const int BH = c->B * c->H;
   const int64_t T = c->total();
   MmaParams p{};
@@ -987,7 +1097,6 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.rows = rows;
   p.gs = gs;
   p.cg = c->cgroups();
-  if (p.cg > 8) return false;
   p.T = T;
   p.P = (std::min(c->k.quantized, c->v.quantized) / gs) * gs;
   const int64_t U = p.P / gs + (T - p.P + kTailUnit - 1) / kTailUnit;
@@ -1007,13 +1116,12 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
-  const int R = rows <= 1 ? 1 : rows <= 2 ? 2 : 4;
+  const int R = rows <= 1 ? 1 : 2;
   int W = 0;
 #define KVB_DISPATCH_D(DD)                                                  \
   if (D == DD) {                                                            \
     if (R == 1) W = dispatch_bits<DD, 1>(p, kb, vb, BH, ws, st);           \
-    else if (R == 2) W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st);      \
-    else W = dispatch_bits<DD, 4>(p, kb, vb, BH, ws, st);                  \
+    else W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st);                  \
   }
   KVB_DISPATCH_D(64)
   KVB_DISPATCH_D(128)

@@ -45,8 +45,8 @@ struct Src {
   }
 };
 
-// Inverse of key_coord/value_coord: element (token-in-tile i, channel d) of the field
-// (lane, w, half, sl) of a b-bit plane.
+// Inverse of key_coord/value_coord (3-bit HMMA layout): element (token-in-tile i,
+// channel d) of the field (lane, w, half, sl) of a b-bit plane.
 __device__ inline void field_element(bool key, int D, int b, int lane, int w, int half, int sl, int* i, int* d) {
   const int sph = 16 / b;
   const int vs = w * sph + sl;
@@ -66,10 +66,30 @@ __device__ inline void field_element(bool key, int D, int b, int lane, int w, in
 // [i_lo, i_hi) contribute and words are OR-merged.
 __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes, uint32_t* tile, bool atomic,
                                  int i_lo, int i_hi) {
-  const int planes = bits == 3 ? 2 : 1;
+  if (bits != 3) {  // IMMA layout: 4 bytes x C classes per word
+    const int wpl = plane_wpl(D, bits), cw = wpl < 4 ? wpl : 4;
+    const int nf = 32 / bits;
+    for (int pw = threadIdx.x; pw < 32 * wpl; pw += blockDim.x) {
+      const int chunk = pw / (32 * cw), within = pw % (32 * cw);
+      const int lane = within / cw, w = chunk * cw + within % cw;
+      uint32_t word = 0;
+      for (int f = 0; f < nf; ++f) {
+        int i, d, sh;
+        imma_element(key, D, bits, lane, w, f, &i, &d, &sh);
+        if (i < i_lo || i >= i_hi) continue;
+        word |= (uint32_t)codes[i * D + d] << sh;
+      }
+      if (atomic) {
+        if (word) atomicOr(tile + pw, word);
+      } else {
+        tile[pw] = word;
+      }
+    }
+    return;
+  }
   int off = 0;
-  for (int pl = 0; pl < planes; ++pl) {
-    const int b = bits == 3 ? (pl == 0 ? 2 : 1) : bits;
+  for (int pl = 0; pl < 2; ++pl) {
+    const int b = pl == 0 ? 2 : 1;
     const int wpl = plane_wpl(D, b);
     const int cw = wpl < 4 ? wpl : 4;
     const int sph = 16 / b;
@@ -83,7 +103,7 @@ __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes
           field_element(key, D, b, lane, w, half, sl, &i, &d);
           if (i < i_lo || i >= i_hi) continue;
           uint32_t code = codes[i * D + d];
-          if (bits == 3) code = pl == 0 ? (code & 3u) : (code >> 2);
+          code = pl == 0 ? (code & 3u) : (code >> 2);
           word |= code << (half * 16 + sl * b);
         }
       }
@@ -218,18 +238,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     for (int e = threadIdx.x; e < (i_hi - i_lo) * D; e += blockDim.x) {
       const int i = i_lo + e / D, d = e % D;
       const uint32_t code = codes[i * D + d];
-      if (code == 0) continue;
-      const TileCoord tc = value_coord(i, d);
-      int w, sh;
-      if (a.vbits == 3) {
-        plane_field(tc, D, 2, &w, &sh);
-        if (code & 3u) atomicOr(tp + w, (code & 3u) << sh);
-        plane_field(tc, D, 1, &w, &sh);
-        if (code >> 2) atomicOr(tp + 32 * plane_wpl(D, 2) + w, (code >> 2) << sh);
-      } else {
-        plane_field(tc, D, a.vbits, &w, &sh);
-        atomicOr(tp + w, code << sh);
-      }
+      tile_or(tp, false, D, a.vbits, i, d, code);
     }
     return;
   }
@@ -295,7 +304,7 @@ __global__ void export_words_kernel(SideView s, bool key, int D, int BH, int64_t
       const int64_t j = S + tl;
       const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
       const int i = (int)(j & 15);
-      const uint32_t code = tile_get(tile, key ? key_coord(i, d) : value_coord(i, d), D, bits);
+      const uint32_t code = tile_get(tile, key, D, bits, i, d);
       word |= code << field_shift(bits, (uint32_t)k);
     }
     words[w] = word;
@@ -359,18 +368,7 @@ __global__ void import_kernel(SideView s, uint32_t* tiles, uint32_t* dmeta, int2
     const uint32_t code = (words[p / cpw] >> field_shift(bits, pos)) & field_mask(bits, pos);
     const int64_t j = q0 + tl;
     uint32_t* tile = tiles + tile_index(s, bh, j >> 4);
-    const TileCoord tc = key ? key_coord((int)(j & 15), d) : value_coord((int)(j & 15), d);
-    if (bits == 3) {
-      int w, sh;
-      plane_field(tc, D, 2, &w, &sh);
-      if (code & 3u) atomicOr(tile + w, (code & 3u) << sh);
-      plane_field(tc, D, 1, &w, &sh);
-      if (code >> 2) atomicOr(tile + 32 * plane_wpl(D, 2) + w, (code >> 2) << sh);
-    } else {
-      int w, sh;
-      plane_field(tc, D, bits, &w, &sh);
-      if (code) atomicOr(tile + w, code << sh);
-    }
+    tile_or(tile, key, D, bits, (int)(j & 15), d, code);
     if (key) {
       if (tl % gs == 0) {
         dmeta[kmeta_index(s, bh, j / gs) + d] = meta[((size_t)bh * D + d) * (n / gs) + tl / gs];

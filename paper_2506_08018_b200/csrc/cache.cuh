@@ -9,7 +9,7 @@
 // -- the unit the attention work list and the multi-GPU shards partition). The packed store
 // is ONE array of group records, so the attention kernel moves a whole group (Keys, Values
 // and both metas) with a single bulk copy:
-//   rec      [bh][group = token/gs] { K tiles [gs/16][tile_words(D, key_bits)]   fragment-native codes
+//   rec      [bh][group = token/gs] { K tiles [gs/16][tile_words(D, key_bits)]   fragment-native codes (common.cuh)
 //                                     V tiles [gs/16][tile_words(D, value_bits)]
 //                                     V meta  [gs][ceil(D/gs)]  u32 {scale_f16 | min_f16 << 16}
 //                                     K meta  [D] }
@@ -102,7 +102,7 @@ __device__ inline float packed_value(bool key, const SideView& s, int bh, int64_
   const int j = (int)j64;
   const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
   const int i = j & 15;
-  const uint32_t code = tile_get(tile, key ? key_coord(i, d) : value_coord(i, d), D, s.bits);
+  const uint32_t code = tile_get(tile, key, D, s.bits, i, d);
   uint32_t m;
   bool narrow = false;
   if (key) {

@@ -101,15 +101,29 @@ __host__ __device__ inline size_t words_for(size_t n, int bits) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Device cache tile layout ("fragment-native"). A tile is 16 tokens x D channels of
-// b-bit codes, arranged so that each lane of a warp owns exactly the operands of an
-// mma.sync m16n8k16 A fragment (rows g, g+8; cols 2t,2t+1, 2t+8,2t+9; g=lane/4,
-// t=lane%4). Keys use A = [token][channel] (k-step kk = d/16), Values use
-// A = [channel][token] (m-tile mt = d/16). Register r of the fragment holds the pair
-// (lo half = first element, hi half = second element). Within a lane, fragment register
-// r at slot s lives at virtual slot vs = r*(D/16) + s of a per-half bit stream with
-// 16/b slots per 16-bit half. 3-bit codes are stored as a 2-bit plane (low bits) followed
-// by a 1-bit plane (high bit). D must be a multiple of 64.
+// Device cache tile layouts. A tile is 16 tokens x D channels of b-bit codes (D % 64 == 0),
+// stored as 32 lanes x wpl words (wpl = D*b/64), in chunks of <= 4 words per lane so a
+// warp's 128-bit loads are contiguous (plane_addr). The layouts are "fragment-native": lane
+// l of a warp reads exactly the tensor-core A operands it owns, with no shuffles.
+//
+// 2- and 4-bit codes (both sides) -- IMMA layout, mma.sync m16n8k32 u8 A fragments
+// (g = lane/4, t = lane%4; a0 = row g, k 4t..4t+3; a1 = row g+8; a2/a3 = k 16+4t..16+4t+3).
+// A fragment register holds 4 codes, one per byte; a byte holds C = 8/b codes of
+// different registers at bit offsets b*class, so one AND with 0x03030303 << 2*class
+// (0x0F0F0F0F << 4*class) yields a register of u8 values code * 2^(b*class).
+//   Keys (A = [token][channel], one k-step per 32 channels, NK = D/32): token i, channel
+//     d = 32 kk + 16 h + 4 t + e, i = g + 8 rb: lane 4g+t, q = kk + NK h, word (q/C)*2 + rb,
+//     bit 8e + b (q%C). The class depends on the channel only (folded into the B operand).
+//   Values (A = [channel][token], one k-step per 32-token block = tiles 2m, 2m+1, one
+//     m-tile per 16 channels, NM = D/16): token i = 4t + e of the tile, channel
+//     d = 16 mt + 8 rh + g: lane 4g+t, q = mt + NM rh, word q/C, bit 8e + b (q%C). Tile 2m
+//     holds a0/a1 (tokens 0..15 of the block), tile 2m+1 holds a2/a3; the class depends on
+//     the channel only (undone per accumulator row).
+// 3-bit codes -- HMMA layout, mma.sync m16n8k16 f16 A fragments (rows g, g+8; cols 2t,2t+1,
+// 2t+8,2t+9). Keys use A = [token][channel] (k-step kk = d/16), Values A = [channel][token]
+// (m-tile mt = d/16). Register r holds a pair (lo half = first element); within a lane,
+// register r at slot s lives at virtual slot vs = r*(D/16) + s of a per-half bit stream with
+// 16/b slots per half. Stored as a 2-bit plane (low bits) followed by a 1-bit plane.
 // ---------------------------------------------------------------------------------------
 struct TileCoord {
   int lane, r, slot, half;
@@ -148,7 +162,7 @@ __host__ __device__ inline int plane_addr(int lane, int w, int wpl) {
   return (w / cw) * (32 * cw) + lane * cw + (w % cw);
 }
 
-// Location (word offset within tile, bit shift) of a b-bit field of one plane.
+// Location (word offset within tile, bit shift) of a b-bit field of one HMMA-layout plane.
 __host__ __device__ inline void plane_field(const TileCoord& c, int D, int b, int* word, int* shift) {
   const int sph = 16 / b;
   const int vs = c.r * (D >> 4) + c.slot;
@@ -157,19 +171,85 @@ __host__ __device__ inline void plane_field(const TileCoord& c, int D, int b, in
   *word = plane_addr(c.lane, w, plane_wpl(D, b));
 }
 
-// Read a code from a tile (bits in {2,3,4}).
-__device__ inline uint32_t tile_get(const uint32_t* tile, const TileCoord& c, int D, int bits) {
-  if (bits == 3) {
-    int w, s;
-    plane_field(c, D, 2, &w, &s);
-    uint32_t lo = (tile[w] >> s) & 3u;
-    plane_field(c, D, 1, &w, &s);
-    uint32_t hi = (tile[32 * plane_wpl(D, 2) + w] >> s) & 1u;
-    return lo | (hi << 2);
+// IMMA layout (b in {2, 4}): word offset / bit shift of (token-in-tile i, channel d).
+__host__ __device__ inline void imma_field(bool key, int D, int b, int i, int d, int* word, int* shift) {
+  const int C = 8 / b;
+  int lane, w, bit;
+  if (key) {
+    const int NK = D >> 5, kk = d >> 5, dc = d & 31, h = dc >> 4, t = (dc & 15) >> 2, e = dc & 3;
+    const int q = kk + NK * h;
+    lane = 4 * (i & 7) + t;
+    w = (q / C) * 2 + (i >> 3);
+    bit = 8 * e + b * (q % C);
+  } else {
+    const int NM = D >> 4, mt = d >> 4, dc = d & 15, rh = dc >> 3, g = dc & 7, t = i >> 2, e = i & 3;
+    const int q = mt + NM * rh;
+    lane = 4 * g + t;
+    w = q / C;
+    bit = 8 * e + b * (q % C);
   }
-  int w, s;
-  plane_field(c, D, bits, &w, &s);
-  return (tile[w] >> s) & ((1u << bits) - 1u);
+  *word = plane_addr(lane, w, plane_wpl(D, b));
+  *shift = bit;
+}
+
+// Inverse of imma_field: the (i, d) of field f (0 .. 32/b-1; byte e = f / C, class f % C)
+// of word w of lane `lane`.
+__host__ __device__ inline void imma_element(bool key, int D, int b, int lane, int w, int f, int* i, int* d,
+                                             int* shift) {
+  const int C = 8 / b, e = f / C, cls = f % C;
+  const int g = lane >> 2, t = lane & 3;
+  *shift = 8 * e + b * cls;
+  if (key) {
+    const int NK = D >> 5;
+    const int q = (w >> 1) * C + cls, rb = w & 1;
+    const int kk = q % NK, h = q / NK;
+    *i = g + 8 * rb;
+    *d = 32 * kk + 16 * h + 4 * t + e;
+  } else {
+    const int NM = D >> 4;
+    const int q = w * C + cls;
+    const int mt = q % NM, rh = q / NM;
+    *i = 4 * t + e;
+    *d = 16 * mt + 8 * rh + g;
+  }
+}
+
+// Every code of a tile is one field (bits 2/4) or two (bits 3: low 2 bits, high bit).
+struct CodeLoc {
+  int w0, s0;       // field of the code (bits 2/4) or of its low 2 bits (bits 3)
+  int w1, s1;       // bits 3: field of the high bit (word offset includes the 2-bit plane)
+};
+
+__host__ __device__ inline CodeLoc code_loc(bool key, int D, int bits, int i, int d) {
+  CodeLoc c{0, 0, -1, 0};
+  if (bits == 3) {
+    const TileCoord tc = key ? key_coord(i, d) : value_coord(i, d);
+    plane_field(tc, D, 2, &c.w0, &c.s0);
+    plane_field(tc, D, 1, &c.w1, &c.s1);
+    c.w1 += 32 * plane_wpl(D, 2);
+  } else {
+    imma_field(key, D, bits, i, d, &c.w0, &c.s0);
+  }
+  return c;
+}
+
+// Read a code from a tile (bits in {2,3,4}).
+__device__ inline uint32_t tile_get(const uint32_t* tile, bool key, int D, int bits, int i, int d) {
+  const CodeLoc c = code_loc(key, D, bits, i, d);
+  if (bits == 3) return ((tile[c.w0] >> c.s0) & 3u) | (((tile[c.w1] >> c.s1) & 1u) << 2);
+  return (tile[c.w0] >> c.s0) & ((1u << bits) - 1u);
+}
+
+// OR a code into a zero-initialised field (global or shared memory).
+__device__ inline void tile_or(uint32_t* tile, bool key, int D, int bits, int i, int d, uint32_t code) {
+  if (code == 0) return;
+  const CodeLoc c = code_loc(key, D, bits, i, d);
+  if (bits == 3) {
+    if (code & 3u) atomicOr(tile + c.w0, (code & 3u) << c.s0);
+    if (code >> 2) atomicOr(tile + c.w1, (code >> 2) << c.s1);
+  } else {
+    atomicOr(tile + c.w0, code << c.s0);
+  }
 }
 
 // Mixed3 narrow-slot test from a segment-relative stream index (quant.cpp:39, :77-84).
