@@ -175,6 +175,9 @@ kvmix_status kvmix_reference_attend(const kvmix_cache* cache, const void* q, kvm
 /* Number of kernels this library has launched in this process (instrumentation for
  * the benchmark's gpu_launches count). */
 uint64_t kvmix_launch_count(void);
+/* Launches of one kernel by name ("attend_mma_kernel", "attend_generic_kernel", ...):
+ * lets tests assert which device path served a call. */
+uint64_t kvmix_launch_count_of(const char* kernel);
 
 #ifdef __cplusplus
 }

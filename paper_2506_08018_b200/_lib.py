@@ -73,6 +73,7 @@ def _declare(L):
         "kvmix_last_error": (C.c_char_p, []),
         "kvmix_abi_version": (i, []),
         "kvmix_launch_count": (u64, []),
+        "kvmix_launch_count_of": (u64, [C.c_char_p]),
         "kvmix_packed_word_count": (sz, [sz, i]),
         "kvmix_feat_per_word": (i, [i, C.POINTER(C.c_int)]),
         "kvmix_pack": (i, [vp, sz, i, vp, vp]),
@@ -133,3 +134,8 @@ def check(status: int) -> None:
 
 def launch_count() -> int:
     return int(lib().kvmix_launch_count())
+
+
+def launch_count_of(kernel: str) -> int:
+    """Launches of one device kernel by name (which path served a call)."""
+    return int(lib().kvmix_launch_count_of(kernel.encode()))

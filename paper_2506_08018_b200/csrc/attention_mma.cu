@@ -41,6 +41,7 @@
 // touches, merged in warp order by attend_combine_sk_kernel (deterministic).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "attention.cuh"
 
@@ -55,6 +56,7 @@ constexpr int kMmaWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kFlushBlocks = 1024;  // Value int32 accumulators: < 2^31 / (32 * 240 * 255)
+// (KVMIX_TEST_FLUSH_BLOCKS lowers it so the parity tests reach the forced-fold path)
 // Lazy online-softmax max (log2 units): the reference max m only moves when a block's max
 // exceeds it by more than kLazy, so p = 2^(score - m) <= 2^kLazy and the Value accumulators
 // are rescaled (folded) only a handful of times per segment.
@@ -237,6 +239,7 @@ struct MmaParams {
   uint32_t stage_bytes;
   float inv;  // 1/sqrt(D)
   int want_cs;  // accumulate the double scores checksum (only when the caller asks)
+  int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
   float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
   float* part_acc;
   double* part_cs;
@@ -755,7 +758,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           e_cur = e_blk - kEHead;
         } else {
           const bool moved = __any_sync(0xffffffffu, row_ok && alpha != 1.0f);
-          if (moved || e_cur > e_blk || nacc >= kFlushBlocks) {
+          if (moved || e_cur > e_blk || nacc >= p.flush_blocks) {
             flush(alpha);
             if (moved) {
               const float ax = __shfl_xor_sync(0xffffffffu, alpha, 2);
@@ -1116,6 +1119,8 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
+  p.flush_blocks = kFlushBlocks;
+  if (const char* e = getenv("KVMIX_TEST_FLUSH_BLOCKS")) p.flush_blocks = std::max(1, std::min(kFlushBlocks, atoi(e)));
   const int R = rows <= 1 ? 1 : 2;
   int W = 0;
 #define KVB_DISPATCH_D(DD)                                                  \

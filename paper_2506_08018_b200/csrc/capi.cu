@@ -5,12 +5,29 @@
 #include <cstring>
 #include <string>
 
+#include <map>
+#include <mutex>
+#include <string>
+
 #include "attention.cuh"
 
 namespace kvb {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_names_mu;
+std::map<std::string, uint64_t>& kernel_names() {
+  static std::map<std::string, uint64_t> m;
+  return m;
+}
+}  // namespace
+
+void count_kernel(const char* name) {
+  std::lock_guard<std::mutex> lk(g_names_mu);
+  ++kernel_names()[name];
+}
 
 void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int H, int T, int D, int bits, int gs,
               uint32_t* words, uint16_t* meta, cudaStream_t st);
@@ -78,6 +95,13 @@ extern "C" {
 const char* kvmix_last_error(void) { return g_err.c_str(); }
 int kvmix_abi_version(void) { return KVMIX_B200_ABI_VERSION; }
 uint64_t kvmix_launch_count(void) { return g_launches.load(); }
+
+uint64_t kvmix_launch_count_of(const char* kernel) {
+  std::lock_guard<std::mutex> lk(kvb::g_names_mu);
+  auto& m = kvb::kernel_names();
+  auto it = m.find(kernel ? kernel : "");
+  return it == m.end() ? 0 : it->second;
+}
 
 size_t kvmix_packed_word_count(size_t n, int bits) { return words_for(n, bits); }
 

@@ -30,8 +30,10 @@ inline void check_cuda(cudaError_t e, const char* what) {
 [[noreturn]] inline void invalid(const std::string& m) { throw Error(KVMIX_INVALID_ARGUMENT, m); }
 
 void count_launch(int n = 1);
+void count_kernel(const char* name);  // per-kernel-name tally (kvmix_launch_count_of)
 inline void after_launch(const char* what) {
   count_launch();
+  count_kernel(what);
   check_cuda(cudaGetLastError(), what);
 }
 

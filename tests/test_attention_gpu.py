@@ -43,7 +43,7 @@ def abs_score_sum(q, ks, G=1):
     return float(np.abs(np.einsum("bhtd,bhjd->bhtj", qr, ks.astype(np.float64))).sum() / np.sqrt(D))
 
 
-def check_attend(dev, ora, q, G=1):
+def check_attend(dev, ora, q, G=1, expect_mma=None):
     ks, vs = ora.snapshot()
     l1 = abs_score_sum(q, ks, G)
     if G > 1:  # GQA: KV head h serves query heads h*G .. h*G+G-1 (= reference t=G rows)
@@ -55,8 +55,14 @@ def check_attend(dev, ora, q, G=1):
     else:
         o64, cs64 = O.attend_f64(q, ks, vs)
         o32, cs32 = O.attend_f32(q, ks, vs)
+    n_mma, n_gen = K.launch_count_of("attend_mma_kernel"), K.launch_count_of("attend_generic_kernel")
     res = K.attend(torch.from_numpy(q).cuda(), dev)
     out = res.output.cpu().numpy()
+    used_mma = K.launch_count_of("attend_mma_kernel") - n_mma
+    used_gen = K.launch_count_of("attend_generic_kernel") - n_gen
+    assert used_mma + used_gen == 1
+    if expect_mma is not None:
+        assert used_mma == int(expect_mma), "tensor-core path expected" if expect_mma else "generic path expected"
     vmax = float(np.abs(vs).max())
     e64 = float(np.abs(out - o64).max()) / vmax
     e32 = float(np.abs(out - o32).max()) / vmax
@@ -82,19 +88,19 @@ def test_attend_long_context_config1(cuda, sigma):
     """Config 1: B1, H32, D128, K2/V2 gs32 r=0.1, 4096 tokens (prefill + decode steps)."""
     dev, ora = build(2, 2, 0.1, 0.1, 32, 1, 32, 128, [4032] + [1] * 64, seed=7, cap=4200)
     q = O.random_h16(5, (1, 32, 1, 128), sigma=sigma)
-    check_attend(dev, ora, q)
+    check_attend(dev, ora, q, expect_mma=True)
 
 
 def test_attend_right_after_prefill(cuda):
     dev, ora = build(2, 2, 0.1, 0.1, 32, 1, 8, 128, [4096], seed=3, cap=4200)
     assert dev.key_tail_tokens() == 416 and dev.value_tail_tokens() == 409
-    check_attend(dev, ora, O.random_h16(6, (1, 8, 1, 128)))
+    check_attend(dev, ora, O.random_h16(6, (1, 8, 1, 128)), expect_mma=True)
 
 
 def test_attend_mixed_tier_fp16(cuda):
     dev, ora = build(3, 4, 0.2, 0.2, 32, 2, 4, 128, [2000] + [1] * 40, seed=11, tail_dtype=torch.float16)
     q = O.random_h16(8, (2, 4, 1, 128))
-    check_attend(dev, ora, q)
+    check_attend(dev, ora, q, expect_mma=True)
     # fp16 queries give the same result as their fp32 copy
     a = K.attend(torch.from_numpy(q).cuda(), dev).output
     b = K.attend(torch.from_numpy(q).cuda().half(), dev).output
@@ -105,13 +111,49 @@ def test_attend_mixed_tier_fp16(cuda):
 def test_attend_gqa(cuda, G):
     dev, ora = build(2, 2, 0.1, 0.1, 32, 2, 4, 128, [1500] + [1] * 33, seed=21)
     q = O.random_h16(12, (2, 4 * G, 1, 128), sigma=2.0)
-    check_attend(dev, ora, q, G=G)
+    check_attend(dev, ora, q, G=G, expect_mma=G <= 2)
 
 
 @pytest.mark.parametrize("gs", [64, 128])
 def test_attend_group_sizes(cuda, gs):
     dev, ora = build(2, 4, 0.1, 0.1, gs, 1, 4, 128, [1200, 1, 1, 300] + [1] * 20, seed=31)
-    check_attend(dev, ora, O.random_h16(13, (1, 4, 2, 128)))
+    check_attend(dev, ora, O.random_h16(13, (1, 4, 2, 128)), expect_mma=True)
+
+
+def test_attend_scale_ramp(cuda):
+    """Magnitudes growing 1000x along the context and a late dominant key: the Value
+    fixed-point exponent and the lazy softmax reference move several times per segment."""
+    B, H, D, T = 2, 4, 128, 3000
+    ramp = np.exp(np.linspace(0.0, np.log(1000.0), T)).astype(np.float32)[None, None, :, None]
+    k = (O.random_h16(41, (B, H, T, D)) * ramp).astype(np.float16).astype(np.float32)
+    v = (O.random_h16(42, (B, H, T, D)) * ramp).astype(np.float16).astype(np.float32)
+    q = O.random_h16(43, (B, H, 1, D), sigma=0.01)
+    k[:, :, 2500] = (q[:, :, 0] * 50.0).astype(np.float16).astype(np.float32)
+    for kb, vb in ((2, 2), (4, 4), (2, 4)):
+        dev = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, 0.05, 0.05, 32), B, H, D, capacity_tokens=T + 16)
+        ora = O.CacheOracle(kb, vb, 0.05, 0.05, 32, B, H, D)
+        for a, z in ((0, 2900), (2900, 3000)):
+            dev.append(k[:, :, a:z], v[:, :, a:z])
+            ora.append(np.ascontiguousarray(k[:, :, a:z]), np.ascontiguousarray(v[:, :, a:z]))
+        check_attend(dev, ora, q, expect_mma=True)
+
+
+def test_attend_forced_folds(cuda, monkeypatch):
+    """The int32 Value accumulators are folded every N blocks (N = 1024 in production,
+    lowered here so that path runs): same result within the stated tolerance."""
+    dev, ora = build(2, 2, 0.1, 0.1, 32, 1, 2, 128, [2000] + [1] * 5, seed=17)
+    q = O.random_h16(18, (1, 2, 1, 128), sigma=2.0)
+    for n in ("1", "3"):
+        monkeypatch.setenv("KVMIX_TEST_FLUSH_BLOCKS", n)
+        check_attend(dev, ora, q, expect_mma=True)
+
+
+def test_attend_d64_two_rows(cuda):
+    """IMMA path at D = 64 (lanes 16..31 mirror the Key channel quads) with two query rows."""
+    dev, ora = build(4, 2, 0.1, 0.1, 32, 2, 4, 64, [900] + [1] * 9, seed=19)
+    check_attend(dev, ora, O.random_h16(20, (2, 4, 2, 64), sigma=1.5), expect_mma=True)
+    dev, ora = build(2, 4, 0.1, 0.1, 32, 1, 3, 64, [700, 3, 1], seed=23)
+    check_attend(dev, ora, O.random_h16(24, (1, 6, 1, 64)), G=2, expect_mma=True)
 
 
 def test_full_precision_cache_exact_dot(cuda):
