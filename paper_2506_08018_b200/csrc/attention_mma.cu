@@ -240,12 +240,16 @@ struct MmaParams {
   float inv;  // 1/sqrt(D)
   int want_cs;  // accumulate the double scores checksum (only when the caller asks)
   int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
+  int tail_unit;     // window tokens per work unit
   float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
   float* part_acc;
   double* part_cs;
 };
 
-constexpr int kTailUnit = 8;  // full-precision-window tokens per work unit (~ one group's cost)
+// Full-precision-window tokens per work unit. A window token costs several times a packed
+// token (lane-parallel dequantization of partially aged Values, no TMA staging), so units
+// are small to keep the stream-K ranges balanced (KVMIX_TAIL_UNIT overrides, for tuning).
+constexpr int kTailUnit = 1;
 
 // Dequantized packed element (token j < quantized, channel d) with compile-time D.
 template <int D, bool KEY, int BITS>
@@ -879,8 +883,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       }
 
     // ---- tokens past the fast region: lane-parallel over channels ------------------------
-    const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * kTailUnit;
-    const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * kTailUnit) : j_lo;
+    const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * p.tail_unit;
+    const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * p.tail_unit) : j_lo;
     if (j_lo < j_hi) {
       const int d0 = lane * LC;
       float qt[R][LC];
@@ -893,6 +897,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         for (int c = 0; c < LC; ++c)
           qt[r][c] = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
       }
+      // IMMA Value layout of this lane's channels: word offset at t = 0 and bit shift at e = 0
+      constexpr int VWPL = D * VB / 64, VCW = VWPL < 4 ? VWPL : 4;
+      int vbase[LC], vsh[LC];
+#pragma unroll
+      for (int c = 0; c < LC; ++c) {
+        const int d = d0 + c, dc = d & 15;
+        const int q = (d >> 4) + NM * (dc >> 3);
+        vbase[c] = plane_addr(4 * (dc & 7), q / CV, VWPL);
+        vsh[c] = VB * (q % CV);
+      }
       // four tokens per round: all loads issued first, the four reductions interleaved
       constexpr int TB = 4;
       for (int64_t j0 = j_lo; j0 < j_hi; j0 += TB) {
@@ -901,8 +915,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         for (int i = 0; i < TB; ++i) {
           const int64_t jj = min(j0 + i, j_hi - 1);
           if (jj >= p.k.quantized) {
+            if (p.tail16 && LC == 4) {  // this lane's 4 channels: one 8-byte load from the ring
+              int64_t slot = p.k.tail_start + (jj - p.k.quantized);
+              if (slot >= p.k.tail_cap) slot -= p.k.tail_cap;
+              const uint2 hv = __ldg(reinterpret_cast<const uint2*>(static_cast<const __half*>(p.k.tail) +
+                                                                    ((size_t)bh * p.k.tail_cap + (size_t)slot) * D + d0));
+              const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&hv.x));
+              const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hv.y));
+              kx[i][0] = f0.x;
+              kx[i][1] = f0.y;
+              kx[i][2 % LC] = f1.x;
+              kx[i][3 % LC] = f1.y;
+            } else {
 #pragma unroll
-            for (int c = 0; c < LC; ++c) kx[i][c] = tail_val(p.k, p.tail16, bh, jj - p.k.quantized, d0 + c, D);
+              for (int c = 0; c < LC; ++c) kx[i][c] = tail_val(p.k, p.tail16, bh, jj - p.k.quantized, d0 + c, D);
+            }
           } else {
 #pragma unroll
             for (int c = 0; c < LC; ++c) kx[i][c] = deq_lane<D, true, KB>(p.k, bh, (int)jj, d0 + c, gs);
@@ -911,8 +938,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
             for (int c = 0; c < LC; ++c) vx[i][c] = tail_val(p.v, p.tail16, bh, jj - p.v.quantized, d0 + c, D);
           } else {
+            // packed Value of a window token (IMMA layout): shared token address math, one
+            // meta word for the lane's channels (same channel group), per-channel word/shift
+            const int j32 = (int)jj;
+            const uint32_t* tile = p.v.tiles + tile_index(p.v, bh, j32 >> 4);
+            const int ti = (j32 & 15) >> 2, te = j32 & 3;
+            const float2 sm = meta_pair(__ldg(p.v.meta + vmeta_index(p.v, bh, j32) + d0 / gs));
 #pragma unroll
-            for (int c = 0; c < LC; ++c) vx[i][c] = deq_lane<D, false, VB>(p.v, bh, (int)jj, d0 + c, gs);
+            for (int c = 0; c < LC; ++c) {
+              const uint32_t w = __ldg(tile + vbase[c] + ti * VCW);
+              const uint32_t code = (w >> (vsh[c] + 8 * te)) & ((1u << VB) - 1u);
+              vx[i][c] = fmaf((float)code, sm.x, sm.y);
+            }
           }
         }
         float x[TB][R];
@@ -978,31 +1015,49 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 }
 
 // Combine the stream-K partials of each (b, kv-head): the warps whose unit ranges meet
-// [bh U, (bh+1) U), slot w + bh, merged in warp order (deterministic).
-__global__ void attend_combine_sk_kernel(const float2* __restrict__ part_ml, const float* __restrict__ part_acc,
-                                         int N, int W, int U, int R, int H, int Hq, int tq, int D,
-                                         float* __restrict__ out) {
-  const int bh = blockIdx.x, r = blockIdx.y;
+// [bh U, (bh+1) U), slot w + bh, merged in warp order (deterministic). One warp per
+// (b, kv-head, row), lanes over channels. (A programmatic-dependent launch that overlaps
+// this kernel with the attention kernel's tail measured bimodal step times; not used.)
+constexpr int kCombineWarps = 4;
+__global__ void __launch_bounds__(kCombineWarps * 32) attend_combine_sk_kernel(
+    const float2* __restrict__ part_ml, const float* __restrict__ part_acc, int N, int W, int U, int R, int BH, int H,
+    int Hq, int tq, int D, float* __restrict__ out) {
+  const int item = blockIdx.x * kCombineWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (item >= BH * R) return;
+  const int bh = item / R, r = item % R;
   const int b = bh / H, h = bh % H, G = Hq / H;
   const int gi = r / tq, qi = r % tq;
   const int hq = h * G + gi;
   const int w0 = (int)((((int64_t)bh * U + 1) * W - 1) / N);
   const int w1 = (int)((((int64_t)bh + 1) * U * W - 1) / N);  // 64-bit products
   float M = -INFINITY;
-  for (int w = w0; w <= w1; ++w) M = fmaxf(M, part_ml[((size_t)w + bh) * R + r].x);
+  for (int w = w0 + lane; w <= w1; w += 32) M = fmaxf(M, part_ml[((size_t)w + bh) * R + r].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float L = 0.f;
-  for (int w = w0; w <= w1; ++w) {
+  for (int w = w0 + lane; w <= w1; w += 32) {
     const float2 ml = part_ml[((size_t)w + bh) * R + r];
     if (ml.x != -INFINITY) L += ml.y * expf(ml.x - M);
   }
+  // fixed-order sum over lanes (deterministic: same shuffle tree every call)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
   const float invL = 1.0f / L;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float a = 0.f;
+  for (int d0 = lane * 4; d0 < D; d0 += 128) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int w = w0; w <= w1; ++w) {
-      const float2 ml = part_ml[((size_t)w + bh) * R + r];
-      if (ml.x != -INFINITY) a += part_acc[(((size_t)w + bh) * R + r) * D + d] * expf(ml.x - M);
+      const size_t pi = ((size_t)w + bh) * R + r;
+      const float2 ml = part_ml[pi];
+      if (ml.x == -INFINITY) continue;
+      const float f = expf(ml.x - M);
+      const float4 x = *reinterpret_cast<const float4*>(part_acc + pi * D + d0);
+      a.x += x.x * f;
+      a.y += x.y * f;
+      a.z += x.z * f;
+      a.w += x.w * f;
     }
-    out[(((size_t)b * Hq + hq) * tq + qi) * D + d] = a * invL;
+    *reinterpret_cast<float4*>(out + (((size_t)b * Hq + hq) * tq + qi) * D + d0) =
+        make_float4(a.x * invL, a.y * invL, a.z * invL, a.w * invL);
   }
 }
 
@@ -1102,7 +1157,9 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.cg = c->cgroups();
   p.T = T;
   p.P = (std::min(c->k.quantized, c->v.quantized) / gs) * gs;
-  const int64_t U = p.P / gs + (T - p.P + kTailUnit - 1) / kTailUnit;
+  p.tail_unit = kTailUnit;
+  if (const char* e = getenv("KVMIX_TAIL_UNIT")) p.tail_unit = std::max(1, std::min(64, atoi(e)));
+  const int64_t U = p.P / gs + (T - p.P + p.tail_unit - 1) / p.tail_unit;
   if ((int64_t)BH * U >= (int64_t)1 << 31) return false;
   p.Gf = (int)(p.P / gs);
   p.U = (int)U;
@@ -1133,8 +1190,11 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
 #undef KVB_DISPATCH_D
   if (W == 0) return false;
   after_launch("attend_mma_kernel");
-  attend_combine_sk_kernel<<<dim3(BH, rows), 128, 0, st>>>(p.part_ml, p.part_acc, p.N, p.W, p.U, rows, c->H, Hq, tq, D,
-                                                           out);
+  {
+    const int items = BH * rows;
+    attend_combine_sk_kernel<<<(items + kCombineWarps - 1) / kCombineWarps, kCombineWarps * 32, 0, st>>>(
+        p.part_ml, p.part_acc, p.N, p.W, p.U, rows, BH, c->H, Hq, tq, D, out);
+  }
   after_launch("attend_combine_sk_kernel");
   if (checksum) {
     const size_t nslot = (size_t)p.W + BH;
