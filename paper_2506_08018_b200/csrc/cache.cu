@@ -128,6 +128,7 @@ struct AppendArgs {
   SideView kv;  // addressing of the Key side (group records)
   // values
   int vbits, v_blocks, v_tile0;
+  int v_warp;  // decode-sized age-out: one warp per (aged token, bh), lanes over channels
   int64_t v_q0, v_n;
   uint32_t* v_tiles;
   uint32_t* v_meta;
@@ -159,11 +160,15 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     uint8_t* codes = sm;  // [gs][D]
     const int q_max = q_max_for_bits(a.kbits);
     const int64_t gglob = a.k_q0 / gs + g;
+    float* xs = reinterpret_cast<float*>(sm + (size_t)gs * D);  // [gs][D] staged column values
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       const int64_t j0 = (int64_t)g * gs;
-      float mn = src.at(bh, j0, d, D), mx = mn;
+      // stage the channel's gs values with the loads in flight together, then reduce
+#pragma unroll 8
+      for (int jj = 0; jj < gs; ++jj) xs[jj * D + d] = src.at(bh, j0 + jj, d, D);
+      float mn = xs[d], mx = mn;
       for (int jj = 1; jj < gs; ++jj) {
-        const float x = src.at(bh, j0 + jj, d, D);
+        const float x = xs[jj * D + d];
         mn = x < mn ? x : mn;
         mx = x > mx ? x : mx;
       }
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       // reference stream index inside this segment [B,H,n,D]: (bh*D + d)*n + t_local
       const uint64_t sbase = ((uint64_t)bh * D + d) * (uint64_t)a.k_n + (uint64_t)j0;
       for (int jj = 0; jj < gs; ++jj) {
-        const float x = src.at(bh, j0 + jj, d, D);
+        const float x = xs[jj * D + d];
         codes[jj * D + d] = (uint8_t)encode(x, sc, mnv, a.kbits, is_narrow(a.kbits, sbase + jj));
       }
     }
@@ -188,6 +193,44 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
   }
   blk -= n_k_blocks;
 
+  if (blk < n_v_blocks && a.v_warp) {
+    // ---- value age-out, few tokens: one warp per (token, bh); lanes own D/32 channels,
+    // channel-group min/max by shuffles over the group's lanes, codes OR-ed into the tile.
+    constexpr int kW = kAppendThreads / 32;
+    const int item = blk * kW + (int)(threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (item >= a.v_n * a.BH) return;
+    const int bh = item % a.BH;
+    const int64_t tl = item / a.BH;  // token index inside the segment
+    const int64_t j = a.v_q0 + tl;   // global token index
+    Src<TI, TT> src{static_cast<const TT*>(a.v_tail), a.v_cap, a.v_start, a.v_L, vin, a.t};
+    const int LC = D / 32;           // 2 or 4 (host checks)
+    const int q_max = q_max_for_bits(a.vbits);
+    float x[4];
+    for (int c = 0; c < LC; ++c) x[c] = src.at(bh, tl, lane * LC + c, D);
+    float mn = x[0], mx = x[0];
+    for (int c = 1; c < LC; ++c) {
+      mn = x[c] < mn ? x[c] : mn;
+      mx = x[c] > mx ? x[c] : mx;
+    }
+    const int glanes = min(gs, D) / LC;  // lanes per channel group (power of two)
+    for (int o = 1; o < glanes; o <<= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mn, o), ox = __shfl_xor_sync(0xffffffffu, mx, o);
+      mn = om < mn ? om : mn;
+      mx = ox > mx ? ox : mx;
+    }
+    const uint32_t m = make_meta(mn, mx, q_max);
+    const int g0 = lane * LC / gs;
+    if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + g0] = m;
+    if (bh == 0 && lane == 0) a.v_info[j] = make_int2((int)a.v_n, (int)tl);
+    const float sc = meta_scale(m), mnv = meta_min(m);
+    uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
+    for (int c = 0; c < LC; ++c) {
+      const int d = lane * LC + c;
+      const uint64_t si = ((uint64_t)bh * a.v_n + (uint64_t)tl) * D + d;
+      tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
+    }
+    return;
+  }
   if (blk < n_v_blocks) {
     // ---- value age-out: one 16-token tile window for one bh ---------------------------
     const int bh = blk % a.BH, w = blk / a.BH;
@@ -261,6 +304,56 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     const TI* in = is_k ? kin : vin;
     TT* tail = static_cast<TT*>(is_k ? a.k_tail : a.v_tail);
     tail[((size_t)bh * cap + (size_t)slot) * D + d] = from_f<TT>(ld_f<TI>(in + r));
+  }
+}
+
+// Decode-step append (t = 1, no Key group ages): one warp per (b, kv-head). The Key token
+// goes to its ring slot; the Value side either ages one token (the oldest window token or
+// the new one) -- channel-group min/max by shuffles, codes OR-ed into the tile -- and/or
+// stores the new token in its ring. A small kernel: the general append kernel's size costs
+// instruction-cache misses that dominate a 1-token step.
+template <typename TI, typename TT>
+__global__ void __launch_bounds__(kAppendThreads) append_decode_kernel(AppendArgs a, const TI* __restrict__ kin,
+                                                                       const TI* __restrict__ vin) {
+  const int bh = blockIdx.x * (kAppendThreads / 32) + (int)(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (bh >= a.BH) return;
+  const int D = a.D, gs = a.gs, LC = D / 32;
+  // Key: the new token stays (k_n == 0)
+  {
+    TT* ring = static_cast<TT*>(a.k_tail) + ((size_t)bh * a.k_cap + (size_t)((a.k_start + a.k_L) % a.k_cap)) * D;
+    for (int c = 0; c < LC; ++c) ring[lane * LC + c] = from_f<TT>(ld_f<TI>(kin + (size_t)bh * D + lane * LC + c));
+  }
+  if (a.v_n == 1) {
+    Src<TI, TT> src{static_cast<const TT*>(a.v_tail), a.v_cap, a.v_start, a.v_L, vin, 1};
+    const int64_t j = a.v_q0;
+    const int q_max = q_max_for_bits(a.vbits);
+    float x[4];
+    for (int c = 0; c < LC; ++c) x[c] = src.at(bh, 0, lane * LC + c, D);
+    float mn = x[0], mx = x[0];
+    for (int c = 1; c < LC; ++c) {
+      mn = x[c] < mn ? x[c] : mn;
+      mx = x[c] > mx ? x[c] : mx;
+    }
+    const int glanes = min(gs, D) / LC;
+    for (int o = 1; o < glanes; o <<= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mn, o), ox = __shfl_xor_sync(0xffffffffu, mx, o);
+      mn = om < mn ? om : mn;
+      mx = ox > mx ? ox : mx;
+    }
+    const uint32_t m = make_meta(mn, mx, q_max);
+    if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + lane * LC / gs] = m;
+    if (bh == 0 && lane == 0) a.v_info[j] = make_int2(1, 0);
+    const float sc = meta_scale(m), mnv = meta_min(m);
+    uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
+    for (int c = 0; c < LC; ++c) {
+      const int d = lane * LC + c;
+      const uint64_t si = (uint64_t)bh * D + d;  // segment [B,H,1,D]
+      tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
+    }
+  }
+  if (a.v_stay0 == 0) {  // the new Value token stays in the window
+    TT* ring = static_cast<TT*>(a.v_tail) + ((size_t)bh * a.v_cap + (size_t)((a.v_start + a.v_L) % a.v_cap)) * D;
+    for (int c = 0; c < LC; ++c) ring[lane * LC + c] = from_f<TT>(ld_f<TI>(vin + (size_t)bh * D + lane * LC + c));
   }
 }
 
@@ -456,6 +549,12 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
     a.v_tile0 = (int)(V.quantized / 16);
     const int64_t tile_end = (V.quantized + v_n + 15) / 16;
     a.v_blocks = (int)(tile_end - a.v_tile0) * BH;
+    // decode-sized age-outs: warp per (token, bh) (channel groups of a power-of-two lane count)
+    const int gl = std::min(gs, D) / std::max(1, D / 32);
+    if (v_n <= 16 && (D == 64 || D == 128) && gl >= 1 && (gl & (gl - 1)) == 0 && gs % (D / 32) == 0) {
+      a.v_warp = 1;
+      a.v_blocks = (int)((v_n * BH + kAppendThreads / 32 - 1) / (kAppendThreads / 32));
+    }
   }
   a.v_tiles = V.tiles;
   a.v_meta = V.meta;
@@ -475,7 +574,7 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
   const bool any_stay = a.k_stay0 < t || a.v_stay0 < t;
   a.tail_blocks = any_stay ? grid_for((size_t)2 * BH * t * D, kAppendThreads) : 0;
 
-  const size_t smem_k = a.k_blocks ? (size_t)gs * D : 0;
+  const size_t smem_k = a.k_blocks ? (size_t)gs * D + (size_t)gs * D * 4 : 0;  // codes + staged values
   const size_t smem_v = a.v_blocks ? (size_t)16 * D + (size_t)16 * (D + 1) * 4 + (size_t)16 * c->cgroups() * 4 : 0;
   const size_t smem = std::max(smem_k, smem_v);
   // ring hazard: new tail slots could alias aged slots still being read only if L + t > cap
@@ -488,7 +587,22 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
     else if (in16 && !tail16) launch_append<__half, float>(args, blocks, smem, k, v, st);
     else launch_append<__half, __half>(args, blocks, smem, k, v, st);
   };
-  if (fused) {
+  const int gl = std::min(gs, D) / std::max(1, D / 32);
+  const bool decode = t == 1 && a.k_n == 0 && v_n <= 1 && fused && (D == 64 || D == 128) && (gl & (gl - 1)) == 0 &&
+                      gs % (D / 32) == 0;
+  if (decode) {
+    const bool in16 = dt == KVMIX_F16, tail16 = c->tail_dtype == KVMIX_F16;
+    const int blocks = (BH + kAppendThreads / 32 - 1) / (kAppendThreads / 32);
+    if (!in16 && !tail16)
+      append_decode_kernel<float, float><<<blocks, kAppendThreads, 0, st>>>(a, (const float*)k, (const float*)v);
+    else if (!in16 && tail16)
+      append_decode_kernel<float, __half><<<blocks, kAppendThreads, 0, st>>>(a, (const float*)k, (const float*)v);
+    else if (in16 && !tail16)
+      append_decode_kernel<__half, float><<<blocks, kAppendThreads, 0, st>>>(a, (const __half*)k, (const __half*)v);
+    else
+      append_decode_kernel<__half, __half><<<blocks, kAppendThreads, 0, st>>>(a, (const __half*)k, (const __half*)v);
+    after_launch("append_decode_kernel");
+  } else if (fused) {
     a.phase = 0;
     launch(a, a.k_blocks + a.v_blocks + a.tail_blocks);
   } else {
