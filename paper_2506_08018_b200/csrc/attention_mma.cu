@@ -51,7 +51,7 @@ namespace {
 
 constexpr int kMmaWarps = 4;
 #ifndef KVB_MIN_CTAS
-#define KVB_MIN_CTAS(KB) ((KB) == 3 ? 3 : 4)  // CTAs per SM the register budget is sized for
+#define KVB_MIN_CTAS(KB) 4  // CTAs per SM the register budget is sized for
 #endif
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -107,15 +107,6 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   return p;
 }
 
-__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
 // D += A (u8, 16x32) * B (s8, 32x8), int32 (exact)
 __device__ __forceinline__ void imma_us(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                         uint32_t b1) {
@@ -134,19 +125,6 @@ __device__ __forceinline__ void imma_uu(int (&d)[4], uint32_t a0, uint32_t a1, u
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, const void* row_addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];\n"
-               : "=r"(b0), "=r"(b1)
-               : "r"(smem_u32(row_addr)));
-}
-
-// (2^10 + v_lo, 2^10 + v_hi) - 2^10 -> exact (v_lo, v_hi), normal fp16
-__device__ __forceinline__ uint32_t sub_magic(uint32_t x) {
-  __half2 v = *reinterpret_cast<__half2*>(&x);
-  v = __hsub2(v, __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400)));
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
 __device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }
 
 // 2^x via MUFU.EX2 without the denormal fix-up (x <= 0 here; 2^x < 2^-126 flushes to 0)
@@ -156,36 +134,22 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// (hi, lo) fp16 split of x packed as {hi | lo << 16}: x ~= hi + lo to ~22 bits.
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& p0, uint32_t& p1) {
-  const __half2 h = __floats2half2_rn(x0, x1);
-  const float2 hf = __half22float2(h);
-  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
-  const uint32_t hu = *reinterpret_cast<const uint32_t*>(&h), lu = *reinterpret_cast<const uint32_t*>(&l);
-  p0 = __byte_perm(hu, lu, 0x5410);
-  p1 = __byte_perm(hu, lu, 0x7632);
+// inverse of n modulo 11 (n in 1..10)
+__device__ __forceinline__ int inv11(int n) {
+  // 1 1, 2 6, 3 4, 4 3, 5 9, 6 2, 7 8, 8 7, 9 5, 10 10
+  return (int)((0xA578293461ull >> (4 * (n - 1))) & 0xFu);
 }
 
-// ---- 3-bit Keys (HMMA layout) --------------------------------------------------------
-// A fragment register = two codes at the same bit offset of the two 16-bit halves; the
-// 2-bit low plane holds positions 0..3 of w / w >> 8 (offsets 0,2,4,6; the high bit from
-// the 1-bit plane lands at offset + 2 <= 8). OR-ing 0x6400 (fp16 1024) and subtracting
-// 1024 gives code * 2^offset exactly; the power of two is folded into the B operand.
-struct K3Unpack {
-  __host__ __device__ static constexpr int off(int p) { return 2 * (p < 4 ? p : p - 4); }
-  template <int NS>
-  __device__ __forceinline__ static uint32_t frag(const uint32_t* w, int r, int s) {
-    const int vs = r * NS + s;
-    const uint32_t hw = w[NS / 2 + (vs >> 4)];
-    const int hb = vs & 15;
-    const int p = vs & 7;
-    const int o = off(p);
-    const uint32_t lw = p < 4 ? w[vs >> 3] : (w[vs >> 3] >> 8);
-    const int tgt = o + 2;
-    const uint32_t hs = hb >= tgt ? (hw >> (hb - tgt)) : (hw << (tgt - hb));
-    return sub_magic((lw & (0x00030003u << o)) | (hs & (0x00010001u << tgt)) | 0x64006400u);
-  }
-};
+// Four channels' balanced s8 digit words (byte n of uu[c] = digit n of channel c) -> digit
+// planes: dst[n * stride] = {digit n of channels 0..3} (4x4 byte transpose).
+__device__ __forceinline__ void store_digits(uint32_t* dst, int stride, const uint32_t (&uu)[4]) {
+  const uint32_t lo01 = __byte_perm(uu[0], uu[1], 0x5140), hi01 = __byte_perm(uu[0], uu[1], 0x7362);
+  const uint32_t lo23 = __byte_perm(uu[2], uu[3], 0x5140), hi23 = __byte_perm(uu[2], uu[3], 0x7362);
+  dst[0] = __byte_perm(lo01, lo23, 0x5410);
+  dst[stride] = __byte_perm(lo01, lo23, 0x7632);
+  dst[2 * stride] = __byte_perm(hi01, hi23, 0x5410);
+  dst[3 * stride] = __byte_perm(hi01, hi23, 0x7632);
+}
 
 // Lane's words of one tile in shared memory (layout: plane_addr in common.cuh).
 template <int WPL>
@@ -275,13 +239,13 @@ __device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, i
 
 // Per-warp dynamic shared layout (bytes):
 //   ring[S][stage_bytes] | kstage | vbs[CGMAX][8][32] u8 | bars[S] u64
-// kstage: IMMA Keys: kbs[8 cols][4 t][NK][2] u32 (digit words of the B fragments);
-//         3-bit Keys: bk[D][NB*8] half (B rows for ldmatrix.trans).
+// kstage: kbs[planes][8 cols][4 t][NK][2] u32 (digit words of the Key B fragments; 3-bit
+//         Keys have a second plane), then for 3-bit Keys ytab[D] f32 (narrow-slot factors)
+//         and ntab[D] u32 (word offset | shift << 16 of each channel's low 2 bits at row 0).
 template <int D, int KB, int R>
 struct WarpLayout {
-  static constexpr int NCOL3 = 2 * R + 22 * R;
-  static constexpr int NB3 = (NCOL3 + 7) / 8;
-  static constexpr int kK = KB == 3 ? D * NB3 * 8 * 2 : 8 * 4 * (D / 32) * 2 * 4;
+  static constexpr int kKB = 8 * 4 * (D / 32) * 2 * 4;
+  static constexpr int kK = KB == 3 ? 2 * kKB + 2 * D * 4 : kKB;
   static constexpr int kV = (D / 32) * 8 * 32;
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
     const size_t n = (size_t)stages * stage_bytes + kK + kV + (size_t)stages * 8;
@@ -299,18 +263,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   static_assert(!K3 || D == 128, "3-bit Keys: D = 128");
   constexpr int NK = D / 32;                   // Key k-steps (32 channels)
   constexpr int NM = D / 16;                   // Value m-tiles (16 channels)
-  constexpr int NS3 = D / 16;                  // 3-bit Keys: HMMA k-steps
   constexpr int KW = lane_words<D, KB>();      // words per lane, Key tile
   constexpr int VW = lane_words<D, VB>();      // words per lane, Value tile
-  constexpr int CK = K3 ? 1 : 8 / KB;          // classes per byte
+  constexpr int KB2 = K3 ? 2 : KB;             // bits of the Key plane in the 2/4-bit layout
+  constexpr int CK = 8 / KB2;                  // classes per byte
   constexpr int CV = 8 / VB;
-  constexpr uint32_t KMASK = KB == 4 ? 0x0F0F0F0Fu : 0x03030303u;
+  constexpr uint32_t KMASK = KB2 == 4 ? 0x0F0F0F0Fu : 0x03030303u;
   constexpr uint32_t VMASK = VB == 4 ? 0x0F0F0F0Fu : 0x03030303u;
   constexpr int LC = D / 32;                   // channels per lane (tail path / epilogue)
   constexpr int QL = D / 4;                    // lanes with a distinct Key channel quad
   constexpr int CGMAX = D / 32;                // channel groups of a token (gs >= 32)
   using WL = WarpLayout<D, KB, R>;
-  constexpr int NB3 = WL::NB3;
 
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float s_acc[kMmaWarps][R][D];
@@ -330,7 +293,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   uint8_t* ring = wbase;
   uint8_t* kstage = ring + (size_t)S * p.stage_bytes;
   uint32_t* kbs = reinterpret_cast<uint32_t*>(kstage);
-  __half* bk = reinterpret_cast<__half*>(kstage);
+  float* ytab = reinterpret_cast<float*>(kstage + 2 * WL::kKB);
+  uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + 2 * WL::kKB + D * 4);
   uint8_t* vbs = kstage + WL::kK;
   uint64_t* bars = reinterpret_cast<uint64_t*>(vbs + WL::kV);
 
@@ -392,9 +356,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   const int Lq = lane % QL;
   const bool qdup = lane >= QL;  // D = 64: lanes 16..31 mirror 0..15
   const int kkL = Lq >> 3, hL = (Lq & 7) >> 2, tL = Lq & 3;
-  const float clsL = K3 ? 1.f : pow2i(-KB * ((kkL + NK * hL) % CK));
-  // 3-bit Keys: power of two of this lane's k-step slot (HMMA layout)
-  const float cls3 = K3 ? pow2i(-K3Unpack::off(((lane * LC) / 16) % 8)) : 1.f;
+  const float clsL = pow2i(-KB2 * ((kkL + NK * hL) % CK));
+  // 3-bit Keys: 4 * 2^-class of the high-bit plane (class q for D = 128), channel offset
+  // of this (b, kv-head) in the Mixed3 stream mod 11, and the channel -> field table
+  const float clsH = K3 ? 4.f * pow2i(-((kkL + NK * hL) & 7)) : 0.f;
+  if constexpr (K3) {
+    for (int d = lane; d < D; d += 32) {
+      int w, sh;
+      imma_field(true, D, 2, 0, d, &w, &sh);
+      ntab[d] = (uint32_t)w | ((uint32_t)sh << 16);
+    }
+    __syncwarp();
+  }
 
   int s = 0;
   uint32_t phase = 0;
@@ -405,6 +378,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     const int hi = min(u_end - bh * p.U, p.U);
     u = bh * p.U + hi;
     const int b = bh / p.H, h = bh % p.H;
+    const int cb11 = (int)(((unsigned)bh * (unsigned)D) % 11u);
+    (void)cb11;
 
     // query rows at this lane's Key channels
     float qv[R][4];
@@ -475,10 +450,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       const uint32_t* km = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes + p.vm_bytes);
 
       // ---- Key group: B operand ---------------------------------------------------------
+      // Fixed-point B = round(q s 2^-(b class) sigma) in four balanced s8 digits; 3-bit Keys
+      // add the high-bit plane's B = round(4 q s 2^-class_hi sigma) (same sigma, so both
+      // planes accumulate into the same int32 scores) and the narrow-slot table
+      // ytab[d] = q_d (wide_scale(s_d) - s_d) for the Mixed3 correction.
       float betaL;       // sum_d q_d m_d of row my_r, scaled to log2 units
-      float wsc0, wsc1;  // IMMA: weights of this lane's two score columns (log2 units)
-      uint32_t kb[NK][2];
-      float isig3[R], beta3[R];
+      float wsc0, wsc1;  // weights of this lane's two score columns (log2 units)
+      uint32_t kb[NK][2], kbh[K3 ? NK : 1][2];
+      int nmod = 0, omod = 0;  // 3-bit Keys: segment length / group offset mod 11
       {
         const uint4 m4 = *reinterpret_cast<const uint4*>(km + 4 * Lq);
         const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
@@ -489,44 +468,57 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           sc[c] = f.x;
           mn[c] = f.y;
         }
+        if constexpr (K3) {
+          const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
+          nmod = inf.x % 11;
+          omod = inf.y % 11;
+        }
         float beta[R], isig[R];
-        if constexpr (!K3) {
-          __syncwarp();  // previous group's reads of kbs are done
+        __syncwarp();  // previous group's reads of kbs / ytab are done
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            float x[4], mx = 0.f, bt = 0.f;
+        for (int r = 0; r < R; ++r) {
+          float x[4], xh[4], mx = 0.f, bt = 0.f;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              x[c] = qc[r][c] * sc[c];
-              mx = fmaxf(mx, fabsf(x[c]));
-              bt = fmaf(qv[r][c], mn[c], bt);
+          for (int c = 0; c < 4; ++c) {
+            x[c] = qc[r][c] * sc[c];
+            mx = fmaxf(mx, fabsf(x[c]));
+            if constexpr (K3) {
+              xh[c] = qv[r][c] * clsH * sc[c];  // 4 q s 2^-class_hi
+              mx = fmaxf(mx, fabsf(xh[c]));
             }
-            if (qdup) bt = 0.f;
-            // sigma = 2^(29 - floor(log2 max|x|)): max|x sigma| in [2^29, 2^30)
-            const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
-            const int e = (int)((mxu >> 23) & 0xffu);
-            const int se = min(max(283 - e, 1), 254);
-            isig[r] = __int_as_float((254 - se) << 23);
-            const float sg = __int_as_float(se << 23);
-            uint32_t uu[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) uu[c] = ((uint32_t)__float2int_rn(x[c] * sg) + 0x80808080u) ^ 0x80808080u;
-            // 4x4 byte transpose: word n = digit n of the four channels (balanced s8)
-            const uint32_t lo01 = __byte_perm(uu[0], uu[1], 0x5140), hi01 = __byte_perm(uu[0], uu[1], 0x7362);
-            const uint32_t lo23 = __byte_perm(uu[2], uu[3], 0x5140), hi23 = __byte_perm(uu[2], uu[3], 0x7362);
-            if (!qdup) {
-              uint32_t* dst = kbs + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL;
-              dst[0] = __byte_perm(lo01, lo23, 0x5410);
-              dst[4 * 2 * NK] = __byte_perm(lo01, lo23, 0x7632);
-              dst[8 * 2 * NK] = __byte_perm(hi01, hi23, 0x5410);
-              dst[12 * 2 * NK] = __byte_perm(hi01, hi23, 0x7632);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
-            beta[r] = bt;
+            bt = fmaf(qv[r][c], mn[c], bt);
           }
-          __syncwarp();
-          // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column g (digit g%4 of row g/4)
+          if (qdup) bt = 0.f;
+          // sigma = 2^(29 - floor(log2 max|x|)): max|x sigma| in [2^29, 2^30)
+          const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+          const int e = (int)((mxu >> 23) & 0xffu);
+          const int se = min(max(283 - e, 1), 254);
+          isig[r] = __int_as_float((254 - se) << 23);
+          const float sg = __int_as_float(se << 23);
+          uint32_t uu[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) uu[c] = ((uint32_t)__float2int_rn(x[c] * sg) + 0x80808080u) ^ 0x80808080u;
+          if (!qdup) store_digits(kbs + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL, 4 * 2 * NK, uu);
+          if constexpr (K3) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) uu[c] = ((uint32_t)__float2int_rn(xh[c] * sg) + 0x80808080u) ^ 0x80808080u;
+            store_digits(kbs + 8 * 4 * 2 * NK + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL, 4 * 2 * NK, uu);
+            if (r == 0) {  // narrow-slot correction table (one query row: the host routes R = 1)
+              float4 y;
+              y.x = qv[0][0] * (wide_scale(sc[0]) - sc[0]);
+              y.y = qv[0][1] * (wide_scale(sc[1]) - sc[1]);
+              y.z = qv[0][2] * (wide_scale(sc[2]) - sc[2]);
+              y.w = qv[0][3] * (wide_scale(sc[3]) - sc[3]);
+              *reinterpret_cast<float4*>(ytab + 4 * lane) = y;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
+          beta[r] = bt;
+        }
+        __syncwarp();
+        // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column g (digit g%4 of row g/4)
+        {
           const uint32_t* src = kbs + (g * 4 + t) * (2 * NK);
 #pragma unroll
           for (int kk = 0; kk < NK; kk += 2) {
@@ -536,78 +528,28 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             kb[kk + 1][0] = v.z;
             kb[kk + 1][1] = v.w;
           }
-          const int rr = my_r < R ? my_r : 0;
-          float is = isig[0], bb = beta[0];
+          if constexpr (K3) {
 #pragma unroll
-          for (int r = 1; r < R; ++r)
-            if (rr == r) {
-              is = isig[r];
-              bb = beta[r];
-            }
-          wsc0 = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
-          wsc1 = wsc0 * 256.f;
-          betaL = bb * p.inv * kLog2e;
-        } else {
-          // 3-bit Keys: fp16 hi/lo B rows (pre-scaled by 2^(e - class)) + residue columns
-          int tau[4];
-          {
-            const int2 inf = __ldg(p.k.info + grp);  // {segment length, token offset of the group}
-            const int nmod = inf.x % 11, omod = inf.y % 11;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int cmod = (int)(((unsigned)bh * D + lane * 4 + c) % 11u);
-              const int phi = (cmod * nmod + omod) % 11;  // stream index % 11 of the group's first token
-              tau[c] = (21 - phi) % 11;                   // narrow tokens: t = tau (mod 11)
+            for (int kk = 0; kk < NK; kk += 2) {
+              const uint4 v = *reinterpret_cast<const uint4*>(src + 8 * 4 * 2 * NK + 2 * kk);
+              kbh[kk][0] = v.x;
+              kbh[kk][1] = v.y;
+              kbh[kk + 1][0] = v.z;
+              kbh[kk + 1][1] = v.w;
             }
           }
-          float sgc[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            float mx = 0.f, bt = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              mx = fmaxf(mx, fabsf(qv[r][c] * sc[c]));
-              mx = fmaxf(mx, fabsf(qv[r][c] * (wide_scale(sc[c]) - sc[c])));
-              bt = fmaf(qv[r][c], mn[c], bt);
-            }
-            const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
-            const int e = (int)((mxu >> 23) & 0xffu);
-            const int se = min(max(268 - e, 1), 254);  // max|qs*sigma| in [2^14, 2^15)
-            isig3[r] = __int_as_float((254 - se) << 23);
-            sgc[r] = __int_as_float(se << 23) * cls3;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
-            beta3[r] = bt;
-          }
-          __syncwarp();  // previous group's ldmatrix reads of bk are done
-          // B row of channel lane*4 + c: {hi | lo << 16} of q s sigma per row, then the
-          // residue-class columns (only column tau_c is non-zero)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t row[NB3 * 4];
-#pragma unroll
-            for (int jj = 0; jj < NB3 * 4; ++jj) row[jj] = 0u;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const float x = qv[r][c] * sc[c] * sgc[r];
-              const __half xh = __float2half_rn(x);
-              const __half xl = __float2half_rn(x - __half2float(xh));
-              row[r] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(xl) << 16);
-              const float y = qv[r][c] * (wide_scale(sc[c]) - sc[c]) * sgc[r];
-              const __half yh = __float2half_rn(y);
-              const __half yl = __float2half_rn(y - __half2float(yh));
-              const uint32_t yp = (uint32_t)__half_as_ushort(yh) | ((uint32_t)__half_as_ushort(yl) << 16);
-#pragma unroll
-              for (int xr = 0; xr < 11; ++xr) row[R + r * 11 + xr] = tau[c] == xr ? yp : 0u;
-            }
-            uint4* dst = reinterpret_cast<uint4*>(bk + (size_t)(lane * 4 + c) * NB3 * 8);
-#pragma unroll
-            for (int jj = 0; jj < NB3; ++jj) dst[jj] = make_uint4(row[4 * jj], row[4 * jj + 1], row[4 * jj + 2], row[4 * jj + 3]);
-          }
-          __syncwarp();
-          wsc0 = wsc1 = 0.f;
-          betaL = 0.f;
         }
+        const int rr = my_r < R ? my_r : 0;
+        float is = isig[0], bb = beta[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+          if (rr == r) {
+            is = isig[r];
+            bb = beta[r];
+          }
+        wsc0 = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
+        wsc1 = wsc0 * 256.f;
+        betaL = bb * p.inv * kLog2e;
       }
 
       // ---- the group's 32-token blocks: 2 Key tiles + one Value k-step each ---------------
@@ -616,7 +558,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         const uint32_t* vt2 = vt + (size_t)(2 * blk) * tile_words(D, VB);
         const uint32_t* vm2 = vm + (size_t)(32 * blk) * CG;
         float la[2], lb[2];  // scores (log2 units) of tokens g / g+8 of tile u, row my_r
-        if constexpr (!K3) {
+        {
           uint32_t kw[2][KW];
           lds_tile<D, KB>(kt2, lane, kw[0]);
           lds_tile<D, KB>(kt2 + tile_words(D, KB), lane, kw[1]);
@@ -628,11 +570,51 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             const int q0 = kk, q1 = kk + NK;  // channel halves h = 0 / 1
 #pragma unroll
             for (int u2 = 0; u2 < 2; ++u2) {
-              const uint32_t a0 = kw[u2][(q0 / CK) * 2 + 0] & (KMASK << (KB * (q0 % CK)));
-              const uint32_t a1 = kw[u2][(q0 / CK) * 2 + 1] & (KMASK << (KB * (q0 % CK)));
-              const uint32_t a2 = kw[u2][(q1 / CK) * 2 + 0] & (KMASK << (KB * (q1 % CK)));
-              const uint32_t a3 = kw[u2][(q1 / CK) * 2 + 1] & (KMASK << (KB * (q1 % CK)));
+              const uint32_t a0 = kw[u2][(q0 / CK) * 2 + 0] & (KMASK << (KB2 * (q0 % CK)));
+              const uint32_t a1 = kw[u2][(q0 / CK) * 2 + 1] & (KMASK << (KB2 * (q0 % CK)));
+              const uint32_t a2 = kw[u2][(q1 / CK) * 2 + 0] & (KMASK << (KB2 * (q1 % CK)));
+              const uint32_t a3 = kw[u2][(q1 / CK) * 2 + 1] & (KMASK << (KB2 * (q1 % CK)));
               imma_us(dk[u2], a0, a1, a2, a3, kb[kk][0], kb[kk][1]);
+              if constexpr (K3) {  // high-bit plane: words (q + 2 NK rb) / 8, class q (D = 128)
+                constexpr int HW = D * 2 / 64;  // first word of the 1-bit plane
+                const uint32_t h0 = kw[u2][HW + 0] & (0x01010101u << q0);
+                const uint32_t h1 = kw[u2][HW + 1] & (0x01010101u << q0);
+                const uint32_t h2 = kw[u2][HW + 0] & (0x01010101u << q1);
+                const uint32_t h3 = kw[u2][HW + 1] & (0x01010101u << q1);
+                imma_us(dk[u2], h0, h1, h2, h3, kbh[kk][0], kbh[kk][1]);
+              }
+            }
+          }
+          float corr[4] = {0.f, 0.f, 0.f, 0.f};  // Mixed3 narrow corrections of tokens g, g+8, 16+g, 24+g
+          float fac[4] = {1.f, 1.f, 1.f, 1.f};
+          if constexpr (K3) {
+            // lane (g, t) corrects token jt = g + 8t of the block: narrow channels d = d0 + 11k
+            const int jt = g + 8 * t, tg = 32 * blk + jt;
+            const int rres = ((10 - omod - tg) % 11 + 11) % 11;
+            float dlt = 0.f;
+            if (nmod != 0) {
+              const int d0 = ((rres * inv11(nmod) - cb11) % 11 + 11) % 11;
+              const uint32_t* tile = kt2 + (t >> 1) * tile_words(D, KB);
+              const int ib = jt & 15, rowoff = 16 * (ib & 7) + (ib >> 3);
+#pragma unroll
+              for (int k = 0; k < (D + 10) / 11; ++k) {
+                const int d = d0 + 11 * k;
+                if (d < D) {
+                  const uint32_t tb = ntab[d];  // {word offset at row 0 | shift << 16}
+                  const uint32_t code = (tile[(tb & 0xffffu) + rowoff] >> (tb >> 16)) & 3u;
+                  dlt = fmaf((float)code, ytab[d], dlt);
+                }
+              }
+            }
+            const float wsn = p.inv * kLog2e;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) corr[x] = __shfl_sync(0xffffffffu, dlt, 4 * g + x) * wsn;
+            if (nmod == 0) {  // every channel of the tokens with (omod + tg) % 11 == 10 is narrow
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const int tgx = 32 * blk + g + 8 * x;
+                if ((omod + tgx) % 11 == 10) fac[x] = 7.0f / 3.0f;
+              }
             }
           }
 #pragma unroll
@@ -641,65 +623,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             float pb = fmaf((float)dk[u2][3], wsc1, (float)dk[u2][2] * wsc0);
             pa += __shfl_xor_sync(0xffffffffu, pa, 1);
             pb += __shfl_xor_sync(0xffffffffu, pb, 1);
-            la[u2] = pa + betaL;
-            lb[u2] = pb + betaL;
-          }
-        } else {
-          uint32_t kw[2][KW];
-          lds_tile<D, KB>(kt2, lane, kw[0]);
-          lds_tile<D, KB>(kt2 + tile_words(D, KB), lane, kw[1]);
-          // one tile at a time (the residue columns make the accumulator set wide)
-          float sa[2], sb[2];
-          float my_isig = isig3[0], my_beta = beta3[0];
-#pragma unroll
-          for (int r = 1; r < R; ++r)
-            if (t == r) {
-              my_isig = isig3[r];
-              my_beta = beta3[r];
-            }
-#pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            float dk[NB3][4];
-#pragma unroll
-            for (int nb = 0; nb < NB3; ++nb) dk[nb][0] = dk[nb][1] = dk[nb][2] = dk[nb][3] = 0.f;
-#pragma unroll
-            for (int kk = 0; kk < NS3; ++kk) {
-              const uint32_t a0 = K3Unpack::frag<NS3>(kw[u2], 0, kk), a1 = K3Unpack::frag<NS3>(kw[u2], 1, kk);
-              const uint32_t a2 = K3Unpack::frag<NS3>(kw[u2], 2, kk), a3 = K3Unpack::frag<NS3>(kw[u2], 3, kk);
-#pragma unroll
-              for (int nb = 0; nb < NB3; ++nb) {
-                uint32_t b0, b1;
-                ldmatrix_x2_trans(b0, b1, bk + (size_t)(16 * kk + (lane & 15)) * NB3 * 8 + nb * 8);
-                mma16816(dk[nb], a0, a1, a2, a3, b0, b1);
-              }
-            }
-            // rows of lane t (HMMA column pairs), residue-class corrections by shuffle
-#pragma unroll
-            for (int hlf = 0; hlf < 2; ++hlf) {  // token g, then token g+8
-              const int x = ((2 * blk + u2) * 16 + g + 8 * hlf) % 11;
-              float tot = 0.f;
-#pragma unroll
-              for (int r = 0; r < R; ++r) {
-                const int col = 2 * R + (r * 11 + x) * 2;  // even: hi, odd: lo
-                const int nb = col >> 3, tsrc = (col & 7) >> 1;
-                float mine = 0.f;
-#pragma unroll
-                for (int qq = 0; qq < NB3; ++qq)
-                  if (qq == nb) mine = dk[qq][2 * hlf] + dk[qq][2 * hlf + 1];
-                const float corr = __shfl_sync(0xffffffffu, mine, g * 4 + tsrc);
-                if (r == t) tot = corr;
-              }
-              const float v = ((dk[0][2 * hlf] + dk[0][2 * hlf + 1] + tot) * my_isig + my_beta) * p.inv * kLog2e;
-              if (hlf == 0) sa[u2] = v;
-              else sb[u2] = v;
-            }
-          }
-          // to the IMMA convention: row r in lanes t = 2r, 2r+1
-          const int src = g * 4 + (my_r < R ? my_r : 0);
-#pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            la[u2] = __shfl_sync(0xffffffffu, sa[u2], src);
-            lb[u2] = __shfl_sync(0xffffffffu, sb[u2], src);
+            la[u2] = fmaf(pa, fac[2 * u2], betaL) + corr[2 * u2];
+            lb[u2] = fmaf(pb, fac[2 * u2 + 1], betaL) + corr[2 * u2 + 1];
           }
         }
         if (p.want_cs && row_ok && (t & 1) == 0) cs += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);

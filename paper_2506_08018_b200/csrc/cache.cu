@@ -87,6 +87,44 @@ __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes
     }
     return;
   }
+  if (key) {  // 3-bit Keys: IMMA 2-bit plane of the low bits, then the 1-bit plane
+    const int wpl2 = plane_wpl(D, 2), cw2 = wpl2 < 4 ? wpl2 : 4;
+    for (int pw = threadIdx.x; pw < 32 * wpl2; pw += blockDim.x) {
+      const int chunk = pw / (32 * cw2), within = pw % (32 * cw2);
+      const int lane = within / cw2, w = chunk * cw2 + within % cw2;
+      uint32_t word = 0;
+      for (int f = 0; f < 16; ++f) {
+        int i, d, sh;
+        imma_element(true, D, 2, lane, w, f, &i, &d, &sh);
+        if (i < i_lo || i >= i_hi) continue;
+        word |= ((uint32_t)codes[i * D + d] & 3u) << sh;
+      }
+      if (atomic) {
+        if (word) atomicOr(tile + pw, word);
+      } else {
+        tile[pw] = word;
+      }
+    }
+    const int wpl1 = plane_wpl(D, 1), cw1 = wpl1 < 4 ? wpl1 : 4;
+    uint32_t* t1 = tile + 32 * wpl2;
+    for (int pw = threadIdx.x; pw < 32 * wpl1; pw += blockDim.x) {
+      const int chunk = pw / (32 * cw1), within = pw % (32 * cw1);
+      const int lane = within / cw1, w = chunk * cw1 + within % cw1;
+      uint32_t word = 0;
+      for (int f = 0; f < 32; ++f) {
+        int i, d, sh;
+        imma_key_hi_element(D, lane, w, f, &i, &d, &sh);
+        if (i < i_lo || i >= i_hi) continue;
+        word |= ((uint32_t)codes[i * D + d] >> 2) << sh;
+      }
+      if (atomic) {
+        if (word) atomicOr(t1 + pw, word);
+      } else {
+        t1[pw] = word;
+      }
+    }
+    return;
+  }
   int off = 0;
   for (int pl = 0; pl < 2; ++pl) {
     const int b = pl == 0 ? 2 : 1;

@@ -121,11 +121,14 @@ __host__ __device__ inline size_t words_for(size_t n, int bits) {
 //     d = 16 mt + 8 rh + g: lane 4g+t, q = mt + NM rh, word q/C, bit 8e + b (q%C). Tile 2m
 //     holds a0/a1 (tokens 0..15 of the block), tile 2m+1 holds a2/a3; the class depends on
 //     the channel only (undone per accumulator row).
-// 3-bit codes -- HMMA layout, mma.sync m16n8k16 f16 A fragments (rows g, g+8; cols 2t,2t+1,
-// 2t+8,2t+9). Keys use A = [token][channel] (k-step kk = d/16), Values A = [channel][token]
-// (m-tile mt = d/16). Register r holds a pair (lo half = first element); within a lane,
-// register r at slot s lives at virtual slot vs = r*(D/16) + s of a per-half bit stream with
-// 16/b slots per half. Stored as a 2-bit plane (low bits) followed by a 1-bit plane.
+// 3-bit Keys -- two IMMA planes: the low 2 bits in the 2-bit Key layout above, then the high
+// bit in a 1-bit plane (C = 8 classes per byte): z = q + 2 NK rb, word z / 8, bit 8e + z % 8
+// (for D = 128 the class z % 8 = q depends on the channel only).
+// 3-bit Values -- HMMA layout, mma.sync m16n8k16 f16 A fragments (rows g, g+8; cols 2t,2t+1,
+// 2t+8,2t+9), A = [channel][token] (m-tile mt = d/16). Register r holds a pair (lo half =
+// first element); within a lane, register r at slot s lives at virtual slot vs = r*(D/16) + s
+// of a per-half bit stream with 16/b slots per half. Stored as a 2-bit plane (low bits)
+// followed by a 1-bit plane.
 // ---------------------------------------------------------------------------------------
 struct TileCoord {
   int lane, r, slot, half;
@@ -222,9 +225,31 @@ struct CodeLoc {
   int w1, s1;       // bits 3: field of the high bit (word offset includes the 2-bit plane)
 };
 
+// 1-bit high plane of 3-bit Keys (IMMA): word offset / bit of (token-in-tile i, channel d)
+__host__ __device__ inline void imma_key_hi_field(int D, int i, int d, int* word, int* shift) {
+  const int NK = D >> 5, kk = d >> 5, dc = d & 31, h = dc >> 4, t = (dc & 15) >> 2, e = dc & 3;
+  const int z = kk + NK * h + 2 * NK * (i >> 3);
+  *word = plane_addr(4 * (i & 7) + t, z >> 3, plane_wpl(D, 1));
+  *shift = 8 * e + (z & 7);
+}
+
+// Inverse of imma_key_hi_field for field f (0..31; byte e = f / 8, class f % 8) of word w.
+__host__ __device__ inline void imma_key_hi_element(int D, int lane, int w, int f, int* i, int* d, int* shift) {
+  const int NK = D >> 5, e = f >> 3, z = 8 * w + (f & 7);
+  const int q = z % (2 * NK), rb = z / (2 * NK);
+  const int kk = q % NK, h = q / NK;
+  *i = (lane >> 2) + 8 * rb;
+  *d = 32 * kk + 16 * h + 4 * (lane & 3) + e;
+  *shift = 8 * e + (f & 7);
+}
+
 __host__ __device__ inline CodeLoc code_loc(bool key, int D, int bits, int i, int d) {
   CodeLoc c{0, 0, -1, 0};
-  if (bits == 3) {
+  if (bits == 3 && key) {
+    imma_field(true, D, 2, i, d, &c.w0, &c.s0);
+    imma_key_hi_field(D, i, d, &c.w1, &c.s1);
+    c.w1 += 32 * plane_wpl(D, 2);
+  } else if (bits == 3) {
     const TileCoord tc = key ? key_coord(i, d) : value_coord(i, d);
     plane_field(tc, D, 2, &c.w0, &c.s0);
     plane_field(tc, D, 1, &c.w1, &c.s1);
