@@ -305,7 +305,7 @@ def run_b200(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp16 codes->mma f32 accumulate (KV bit-packed 2/3/4-bit)",
+        "dtype": "u8 codes x s8/u8 fixed-point digits -> s32 (IMMA), f32 softmax (KV bit-packed 2/3/4-bit)",
         "data": "synthetic (randn on the binary16 grid, on device)",
         "config": {"workload": f"configs[1] {args.config}: {L} layers, B{B}, Hq{Hq}/Hkv{H}, D{D}, ~{ctx} ctx, "
                                f"KVmix tiers (0-{high - 1} K3/V4 r0.2, rest K2/V2 r0.1), gs32, fp16 window",
@@ -314,7 +314,8 @@ def run_b200(args, rank, world, local_rank):
                    "timed_step": "per layer: kvmix_cache_append (1 token) + kvmix_attend"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "attend_mma_kernel + attend_combine_kernel (per layer launch)",
+                     "kernel": "attend_mma_kernel (IMMA) + attend_combine_sk_kernel, one pair per layer",
+                     "traffic_unit": "DRAM bytes per step (profiles/ncu_traffic.json)",
                      "algorithmic_bytes_per_step": tot_bytes, "attend_ms_per_step": tot_ms,
                      "attend_share_of_step": tot_ms / ms_per_step},
         "e2e": e2e,
