@@ -262,29 +262,59 @@ def run_b200(args, rank, world, local_rank):
             traffic = json.load(f).get(args.config)
 
     # ---- e2e through the public API with pinned host buffers ----
+    # Every step copies that step's q/k/v from pinned host memory and reads the outputs back;
+    # the copies run on a second stream, double-buffered (step s+1's inputs upload while step
+    # s computes, step s's outputs download while step s+1 computes), as a serving loop would.
     e2e = None
     if not args.no_e2e:
-        q_h = qs[:, :, :, :, :, :].cpu().pin_memory()
+        q_h = qs.cpu().pin_memory()
         k_h = kn.cpu().pin_memory()
         v_h = vn.cpu().pin_memory()
-        o_h = torch.empty(L, B, Hq, 1, D, dtype=torch.float32).pin_memory()
         n_e2e = min(args.steps, total_steps)
+        o_h = torch.empty(n_e2e, L, B, Hq, 1, D, dtype=torch.float32).pin_memory()
+        cp = torch.cuda.Stream(device=dev)
+        qb = [torch.empty_like(qs[0]) for _ in range(2)]
+        kb = [torch.empty_like(kn[0]) for _ in range(2)]
+        vb = [torch.empty_like(vn[0]) for _ in range(2)]
+        ob = [torch.empty_like(outs) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        drained = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step(s):
-            for l, c in enumerate(caches):
-                kd_ = k_h[s, l].to(dev, non_blocking=True)
-                vd_ = v_h[s, l].to(dev, non_blocking=True)
-                qd_ = q_h[s, l].to(dev, non_blocking=True)
-                c.append(kd_, vd_)
-                r = K.attend(qd_, c, checksum=False, out=outs[l])
-                o_h[l].copy_(r.output, non_blocking=True)
+        def upload(s, i):
+            with torch.cuda.stream(cp):
+                cp.wait_event(done[i])  # the buffers' previous step has finished reading them
+                qb[i].copy_(q_h[s % total_steps], non_blocking=True)
+                kb[i].copy_(k_h[s % total_steps], non_blocking=True)
+                vb[i].copy_(v_h[s % total_steps], non_blocking=True)
+                ready[i].record(cp)
 
-        e2e_step(0)
+        def run(n):
+            for i in range(2):
+                done[i].record(stream)
+                drained[i].record(stream)
+            upload(0, 0)
+            for s in range(n):
+                i = s % 2
+                if s + 1 < n:
+                    upload(s + 1, 1 - i)
+                stream.wait_event(ready[i])
+                stream.wait_event(drained[i])  # ob[i] of step s-2 has been read back
+                for l, c in enumerate(caches):
+                    c.append(kb[i][l], vb[i][l])
+                    K.attend(qb[i][l], c, checksum=False, out=ob[i][l])
+                done[i].record(stream)
+                with torch.cuda.stream(cp):
+                    cp.wait_event(done[i])
+                    o_h[s].copy_(ob[i], non_blocking=True)
+                    drained[i].record(cp)
+            stream.wait_stream(cp)
+
+        run(1)
         barrier()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        for s in range(n_e2e):
-            e2e_step(s % total_steps)
+        run(n_e2e)
         s1.record(stream)
         s1.synchronize()
         te = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
@@ -292,7 +322,9 @@ def run_b200(args, rank, world, local_rank):
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": world * B * n_e2e / (float(te.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(L * (qs[0, 0].numel() + kn[0, 0].numel() + vn[0, 0].numel()) * 2),
-               "d2h_bytes_per_step": int(L * outs[0].numel() * 4)}
+               "d2h_bytes_per_step": int(L * outs[0].numel() * 4),
+               "path": "per layer KVLayerCache.append + attend (Python API) on pinned-host inputs; "
+                       "H2D/D2H double-buffered on a copy stream"}
 
     res = {
         "metric": METRIC,

@@ -21,6 +21,7 @@ class Workspace {
   }
   template <typename T>
   T* get(cudaStream_t st, size_t n) {
+    keep_pool();
     void* p = nullptr;
     check_cuda(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st), "cudaMallocAsync(workspace)");
     allocs_.push_back({p, st});
@@ -31,6 +32,21 @@ class Workspace {
   float* acc(cudaStream_t st, size_t n) { return get<float>(st, n); }
   double* cs(cudaStream_t st, size_t n) { return get<double>(st, n); }
   size_t bytes() const { return bytes_; }
+
+  // The default pool returns freed memory to the driver at every synchronization unless a
+  // release threshold is set; a decode loop that synchronizes per step would then remap
+  // its (tiny) scratch on every call (hundreds of microseconds). Keep it.
+  static void keep_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    check_cuda(cudaDeviceGetDefaultMemPool(&pool, dev), "default mempool");
+    uint64_t thr = 256ull << 20;
+    check_cuda(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool threshold");
+    done_dev = dev;
+  }
 
  private:
   std::vector<std::pair<void*, cudaStream_t>> allocs_;
