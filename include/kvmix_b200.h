@@ -155,6 +155,14 @@ kvmix_status kvmix_cache_import_tail(kvmix_cache* cache, int side, const float* 
  * full-precision K/V is materialized; scratch is independent of the token count. */
 kvmix_status kvmix_attend(const kvmix_cache* cache, const void* q, kvmix_dtype dtype, int q_heads,
                           int t, float* out, double* checksum, void* stream);
+/* One decode step of one layer: KVLayerCache::append(k, v) (t tokens, cache.cpp:45-80)
+ * followed by attend(q) (attention.cpp:161-166), with the reference's semantics and errors.
+ * When the append is a 1-token decode step that ages no Key group (the steady state), the
+ * append runs inside the attention launch (one kernel instead of two); otherwise the two
+ * calls run in order. Replaces the CachedDecoder::step pair `cache.append(); attend();`. */
+kvmix_status kvmix_append_attend(kvmix_cache* cache, const void* k, const void* v, kvmix_dtype kv_dtype, int t,
+                                 const void* q, kvmix_dtype q_dtype, int q_heads, int tq, float* out,
+                                 double* checksum, void* stream);
 /* Same, over several layers' caches in one call (one decode step of a model stack):
  * q[l], out[l] per layer. Used by the benchmark to keep host overhead off the step. */
 kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* q,

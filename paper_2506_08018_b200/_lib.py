@@ -99,6 +99,7 @@ def _declare(L):
         "kvmix_cache_import_segment": (i, [vp, i, i, vp, vp, vp]),
         "kvmix_cache_import_tail": (i, [vp, i, vp, i64, vp]),
         "kvmix_attend": (i, [vp, vp, i, i, i, vp, C.POINTER(C.c_double), vp]),
+        "kvmix_append_attend": (i, [vp, vp, vp, i, i, vp, i, i, i, vp, C.POINTER(C.c_double), vp]),
         "kvmix_attend_layers": (i, [C.POINTER(vp), i, C.POINTER(vp), i, i, i, C.POINTER(vp), vp]),
         "kvmix_fused_qk_scores": (i, [vp, vp, i, i, vp, vp]),
         "kvmix_softmax_rows": (i, [vp, i64, i64, vp]),

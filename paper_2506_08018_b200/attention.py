@@ -52,6 +52,27 @@ def attend(query, cache: KVLayerCache, *, checksum: bool = True, out: torch.Tens
     return AttentionOutput(out, cs.value)
 
 
+def append_attend(cache: KVLayerCache, new_keys, new_values, query, *, checksum: bool = False,
+                  out: torch.Tensor | None = None) -> AttentionOutput:
+    """One layer of a decode step: cache.append(new_keys, new_values) then attend(query, cache)
+    (the CachedDecoder::step pair). A 1-token append that ages no Key group runs inside the
+    attention launch; anything else is the two calls in order. Same results and errors."""
+    k = _as_device(new_keys)
+    v = _as_device(new_values)
+    cache._check_append(k, v)
+    if v.dtype != k.dtype:
+        v = v.to(k.dtype)
+    q = _as_device(query)
+    _check_query(q, cache, allow_gqa=True)
+    B, Hq, t, D = (int(x) for x in q.shape)
+    if out is None:
+        out = torch.empty((B, Hq, t, D), dtype=torch.float32, device=q.device)
+    cs = C.c_double(0.0)
+    check(lib().kvmix_append_attend(cache.handle, _ptr(k), _ptr(v), _dtype_code(k), int(k.shape[2]), _ptr(q),
+                                    _dtype_code(q), Hq, t, _ptr(out), C.byref(cs) if checksum else None, _stream()))
+    return AttentionOutput(out, cs.value)
+
+
 def fused_qk_scores(query, cache: KVLayerCache) -> torch.Tensor:
     """fused_qk_scores (attention.cpp:28-81): [B,H,t,total] fp32, already * 1/sqrt(D)."""
     q = _as_device(query)

@@ -117,14 +117,17 @@ class KVLayerCache:
         return self._cap
 
     # ---- append (cache.cpp:45-80) ----------------------------------------------------------
-    def append(self, new_keys, new_values) -> None:
-        k = _as_device(new_keys)
-        v = _as_device(new_values)
+    def _check_append(self, k, v) -> None:
         if (k.dim() != 4 or v.dim() != 4 or k.shape[0] != self._b or k.shape[1] != self._nh or k.shape[3] != self._d
                 or tuple(v.shape[:2]) != (self._b, self._nh) or v.shape[3] != self._d or k.shape[2] != v.shape[2]):
             raise KvmixInvalidArgument("KVLayerCache::append: tensor shape does not match cache")
         if k.shape[2] < 1:
             raise KvmixInvalidArgument("KVLayerCache::append: need at least one token")
+
+    def append(self, new_keys, new_values) -> None:
+        k = _as_device(new_keys)
+        v = _as_device(new_values)
+        self._check_append(k, v)
         if v.dtype != k.dtype:
             v = v.to(k.dtype)
         check(lib().kvmix_cache_append(self._h, _ptr(k), _ptr(v), _dtype_code(k), int(k.shape[2]), _stream()))

@@ -345,11 +345,31 @@ namespace kvb {
 // Dispatcher: the tensor-core kernel (attention_mma.cu) when it supports the shape, the
 // generic kernel otherwise.
 bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
-                Workspace& ws, cudaStream_t st);
+                Workspace& ws, cudaStream_t st, const DecodeAppend* da);
+void launch_decode_append(const DecodeAppend& da, cudaStream_t st);
 void attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
             Workspace& ws, cudaStream_t st) {
   check_attend(c, Hq, tq);
-  if (attend_mma(c, q, dt, Hq, tq, out, checksum, ws, st)) return;
+  if (attend_mma(c, q, dt, Hq, tq, out, checksum, ws, st, nullptr)) return;
   attend_generic(c, q, dt, Hq, tq, out, checksum, ws, st);
+}
+
+// append(k, v) then attend(q) in one launch when the append is a decode step the
+// attention kernel can run in its prologue; otherwise the two calls in order.
+void append_attend(kvmix_cache* c, const void* k, const void* v, kvmix_dtype kv_dt, int t, const void* q,
+                   kvmix_dtype q_dt, int Hq, int tq, float* out, double* checksum, Workspace& ws, cudaStream_t st) {
+  if (c->total() + t > c->cap || t < 1) {
+    cache_append(c, k, v, kv_dt, t, st);  // raises the reference's errors
+  } else {
+    check_attend(c, Hq, tq);  // shape errors before any state changes
+    DecodeAppend da;
+    if (cache_append_decode_plan(c, k, v, kv_dt, t, &da)) {
+      if (attend_mma(c, q, q_dt, Hq, tq, out, checksum, ws, st, &da)) return;
+      launch_decode_append(da, st);
+    } else {
+      cache_append(c, k, v, kv_dt, t, st);
+    }
+  }
+  attend(c, q, q_dt, Hq, tq, out, checksum, ws, st);
 }
 }  // namespace kvb

@@ -60,6 +60,8 @@ void attend_generic(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq,
                     Workspace& ws, cudaStream_t st);
 void attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
             Workspace& ws, cudaStream_t st);
+void append_attend(kvmix_cache* c, const void* k, const void* v, kvmix_dtype kv_dt, int t, const void* q,
+                   kvmix_dtype q_dt, int Hq, int tq, float* out, double* checksum, Workspace& ws, cudaStream_t st);
 void fused_qk_scores(const kvmix_cache* c, const void* q, kvmix_dtype dt, int tq, float* scores, cudaStream_t st);
 void softmax_rows(float* x, int64_t rows, int64_t cols, cudaStream_t st);
 void fused_pv(const kvmix_cache* c, const float* probs, int tq, float* out, cudaStream_t st);

@@ -40,6 +40,8 @@
 // independent warps; each warp writes one partial (m, l, acc) per (b, kv-head) segment it
 // touches, merged in warp order by attend_combine_sk_kernel (deterministic).
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 
@@ -62,6 +64,23 @@ constexpr int kFlushBlocks = 1024;  // Value int32 accumulators: < 2^31 / (32 * 
 // are rescaled (folded) only a handful of times per segment.
 constexpr int kLazy = 3;
 constexpr int kEHead = 2;  // extra fixed-point headroom bits when the Value exponent is reset
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Epoch of one fused call: per-(b, kv-head) "append done" flags are published with it, so the
+// flag array needs no clearing (pool memory holds older epochs; the base is random).
+unsigned long long next_epoch() {
+  static std::atomic<unsigned long long> e{0x9e3779b97f4a7c15ull ^
+                                           (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count()};
+  return e.fetch_add(2) | 1ull;  // odd, distinct per call
+}
 
 // binary16 pair {scale (lo), min (hi)} of a meta word -> fp32
 __device__ __forceinline__ float2 meta_pair(uint32_t m) {
@@ -203,6 +222,10 @@ struct MmaParams {
   uint32_t stage_bytes;
   float inv;  // 1/sqrt(D)
   int want_cs;  // accumulate the double scores checksum (only when the caller asks)
+  int fused;         // the call's 1-token append runs in the prologue (kvmix_append_attend)
+  DecodeAppend da;
+  unsigned long long* flags;  // per (b, kv-head): epoch once its append is done
+  unsigned long long epoch;
   int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
   int tail_unit;     // window tokens per work unit
   float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
@@ -351,6 +374,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     }
   };
   for (int s = 0; s < S; ++s) issue_next(s);
+
+  // fused 1-token append: the warp whose range holds a (b, kv-head)'s first window unit
+  // appends its token (only the window path reads what the append writes), then publishes
+  if (p.fused) {
+    for (int bh = u_beg / p.U; bh <= (u_end - 1) / p.U; ++bh) {
+      const int x = bh * p.U + p.Gf;
+      if (x >= u_beg && x < u_end) {
+        decode_append_warp(p.da, bh, lane);
+        if ((bh + 1) * p.U > u_end) {  // later warps read this window too: publish
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release(p.flags + bh, p.epoch);
+        }
+      }
+    }
+  }
 
   // Key B-build mapping: lane owns channels 4*Lq .. 4*Lq+3 (IMMA: one B register's k rows)
   const int Lq = lane % QL;
@@ -811,6 +850,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * p.tail_unit;
     const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * p.tail_unit) : j_lo;
     if (j_lo < j_hi) {
+      if (p.fused && lo > p.Gf) {  // appended by an earlier warp (resident: in-order dispatch)
+        while (ld_acquire(p.flags + bh) != p.epoch) __nanosleep(32);
+      }
       const int d0 = lane * LC;
       float qt[R][LC];
 #pragma unroll
@@ -843,7 +885,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             if (p.tail16 && LC == 4) {  // this lane's 4 channels: one 8-byte load from the ring
               int64_t slot = p.k.tail_start + (jj - p.k.quantized);
               if (slot >= p.k.tail_cap) slot -= p.k.tail_cap;
-              const uint2 hv = __ldg(reinterpret_cast<const uint2*>(static_cast<const __half*>(p.k.tail) +
+              const uint2 hv = __ldcg(reinterpret_cast<const uint2*>(static_cast<const __half*>(p.k.tail) +
                                                                     ((size_t)bh * p.k.tail_cap + (size_t)slot) * D + d0));
               const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&hv.x));
               const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hv.y));
@@ -868,10 +910,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             const int j32 = (int)jj;
             const uint32_t* tile = p.v.tiles + tile_index(p.v, bh, j32 >> 4);
             const int ti = (j32 & 15) >> 2, te = j32 & 3;
-            const float2 sm = meta_pair(__ldg(p.v.meta + vmeta_index(p.v, bh, j32) + d0 / gs));
+            const float2 sm = meta_pair(__ldcg(p.v.meta + vmeta_index(p.v, bh, j32) + d0 / gs));
 #pragma unroll
             for (int c = 0; c < LC; ++c) {
-              const uint32_t w = __ldg(tile + vbase[c] + ti * VCW);
+              const uint32_t w = __ldcg(tile + vbase[c] + ti * VCW);
               const uint32_t code = (w >> (vsh[c] + 8 * te)) & ((1u << VB) - 1u);
               vx[i][c] = fmaf((float)code, sm.x, sm.y);
             }
@@ -1027,6 +1069,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.part_ml = ws.ml(st, slots * p.rows);
   p.part_acc = ws.acc(st, slots * p.rows * D);
   p.part_cs = ws.cs(st, slots + 1);
+  if (p.fused) p.flags = ws.get<unsigned long long>(st, (size_t)BH);
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
   kern<<<(p.W + kMmaWarps - 1) / kMmaWarps, kMmaWarps * 32, smem, st>>>(p);
   return p.W;
@@ -1057,7 +1100,7 @@ int dispatch_bits(MmaParams& p, int kb, int vb, int BH, Workspace& ws, cudaStrea
 }  // namespace
 
 bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
-                Workspace& ws, cudaStream_t st) {
+                Workspace& ws, cudaStream_t st, const DecodeAppend* da) {
   const int rows = (Hq / c->H) * tq;
   if (rows > 2) return false;
   const int kb = c->k.bits, vb = c->v.bits;
@@ -1101,6 +1144,13 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
+  if (da) {  // fused append: only if the aged Value token is outside the fast groups
+    if (da->v_age && da->v_j < p.P) return false;
+    if (T <= p.P) return false;  // (cannot happen after an append: the new Key is in the window)
+    p.fused = 1;
+    p.da = *da;
+    p.epoch = next_epoch();
+  }
   p.flush_blocks = kFlushBlocks;
   if (const char* e = getenv("KVMIX_TEST_FLUSH_BLOCKS")) p.flush_blocks = std::max(1, std::min(kFlushBlocks, atoi(e)));
   const int R = rows <= 1 ? 1 : 2;

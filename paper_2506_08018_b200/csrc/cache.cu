@@ -345,54 +345,13 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
   }
 }
 
-// Decode-step append (t = 1, no Key group ages): one warp per (b, kv-head). The Key token
-// goes to its ring slot; the Value side either ages one token (the oldest window token or
-// the new one) -- channel-group min/max by shuffles, codes OR-ed into the tile -- and/or
-// stores the new token in its ring. A small kernel: the general append kernel's size costs
+// Decode-step append (t = 1, no Key group ages): one warp per (b, kv-head)
+// (decode_append_warp, cache.cuh). A small kernel: the general append kernel's size costs
 // instruction-cache misses that dominate a 1-token step.
-template <typename TI, typename TT>
-__global__ void __launch_bounds__(kAppendThreads) append_decode_kernel(AppendArgs a, const TI* __restrict__ kin,
-                                                                       const TI* __restrict__ vin) {
+__global__ void __launch_bounds__(kAppendThreads) append_decode_kernel(DecodeAppend a) {
   const int bh = blockIdx.x * (kAppendThreads / 32) + (int)(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (bh >= a.BH) return;
-  const int D = a.D, gs = a.gs, LC = D / 32;
-  // Key: the new token stays (k_n == 0)
-  {
-    TT* ring = static_cast<TT*>(a.k_tail) + ((size_t)bh * a.k_cap + (size_t)((a.k_start + a.k_L) % a.k_cap)) * D;
-    for (int c = 0; c < LC; ++c) ring[lane * LC + c] = from_f<TT>(ld_f<TI>(kin + (size_t)bh * D + lane * LC + c));
-  }
-  if (a.v_n == 1) {
-    Src<TI, TT> src{static_cast<const TT*>(a.v_tail), a.v_cap, a.v_start, a.v_L, vin, 1};
-    const int64_t j = a.v_q0;
-    const int q_max = q_max_for_bits(a.vbits);
-    float x[4];
-    for (int c = 0; c < LC; ++c) x[c] = src.at(bh, 0, lane * LC + c, D);
-    float mn = x[0], mx = x[0];
-    for (int c = 1; c < LC; ++c) {
-      mn = x[c] < mn ? x[c] : mn;
-      mx = x[c] > mx ? x[c] : mx;
-    }
-    const int glanes = min(gs, D) / LC;
-    for (int o = 1; o < glanes; o <<= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, mn, o), ox = __shfl_xor_sync(0xffffffffu, mx, o);
-      mn = om < mn ? om : mn;
-      mx = ox > mx ? ox : mx;
-    }
-    const uint32_t m = make_meta(mn, mx, q_max);
-    if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + lane * LC / gs] = m;
-    if (bh == 0 && lane == 0) a.v_info[j] = make_int2(1, 0);
-    const float sc = meta_scale(m), mnv = meta_min(m);
-    uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
-    for (int c = 0; c < LC; ++c) {
-      const int d = lane * LC + c;
-      const uint64_t si = (uint64_t)bh * D + d;  // segment [B,H,1,D]
-      tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
-    }
-  }
-  if (a.v_stay0 == 0) {  // the new Value token stays in the window
-    TT* ring = static_cast<TT*>(a.v_tail) + ((size_t)bh * a.v_cap + (size_t)((a.v_start + a.v_L) % a.v_cap)) * D;
-    for (int c = 0; c < LC; ++c) ring[lane * LC + c] = from_f<TT>(ld_f<TI>(vin + (size_t)bh * D + lane * LC + c));
-  }
+  decode_append_warp(a, bh, lane);
 }
 
 // ---- snapshot / export / import --------------------------------------------------------
@@ -541,7 +500,71 @@ void launch_append(const AppendArgs& a, int blocks, size_t smem, const void* k, 
 
 }  // namespace
 
+void launch_decode_append(const DecodeAppend& da, cudaStream_t st) {
+  const int blocks = (da.BH + kAppendThreads / 32 - 1) / (kAppendThreads / 32);
+  append_decode_kernel<<<blocks, kAppendThreads, 0, st>>>(da);
+  after_launch("append_decode_kernel");
+}
+
+bool cache_append_decode_plan(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, int t, DecodeAppend* out) {
+  if (t != 1 || (dt != KVMIX_F32 && dt != KVMIX_F16) || !k || !v) return false;
+  if (c->total() + t > c->cap) return false;
+  const int gs = c->cfg.group_size, D = c->D;
+  auto& K = c->k;
+  auto& V = c->v;
+  const int64_t k_cur = K.tail_len + 1;
+  const int64_t k_target = (int64_t)std::floor((double)K.ratio * (double)k_cur);
+  const int64_t k_n = (k_cur - k_target) / gs * gs;
+  const int64_t v_cur = V.tail_len + 1;
+  const int64_t v_target = (int64_t)std::floor((double)V.ratio * (double)v_cur);
+  const int64_t v_n = std::max<int64_t>(0, v_cur - v_target);
+  const int gl = std::min(gs, D) / std::max(1, D / 32);
+  if (k_n > 0 || v_n > 1 || !(D == 64 || D == 128) || (gl & (gl - 1)) != 0 || gs % (D / 32) != 0) return false;
+  if (K.tail_len + 1 > K.tail_cap || V.tail_len + 1 > V.tail_cap) return false;
+  DecodeAppend a{};
+  a.D = D;
+  a.gs = gs;
+  a.BH = c->B * c->H;
+  a.in16 = dt == KVMIX_F16;
+  a.tail16 = c->tail_dtype == KVMIX_F16;
+  a.kin = k;
+  a.vin = v;
+  a.k_tail = K.tail;
+  a.k_cap = K.tail_cap;
+  a.k_slot = (K.tail_start + K.tail_len) % K.tail_cap;
+  a.v_age = (int)v_n;
+  a.v_stay = V.tail_len + 1 - v_n > 0 ? 1 : 0;  // the new token stays unless it is the aged one
+  a.vbits = V.bits;
+  a.v_j = V.quantized;
+  a.v_tail = V.tail;
+  a.v_cap = V.tail_cap;
+  a.v_start = V.tail_start;
+  a.v_L = V.tail_len;
+  a.v_slot = (V.tail_start + V.tail_len) % V.tail_cap;
+  a.v_tiles = V.tiles;
+  a.v_meta = V.meta;
+  a.v_info = V.info;
+  a.vv = view(V);
+  *out = a;
+  // host bookkeeping (cache.cpp:65-79): Key tail grows; one Value token may age
+  K.tail_len += 1;
+  if (v_n > 0) {
+    V.segs.push_back(v_n);
+    V.quantized += v_n;
+    V.tail_start = (V.tail_start + v_n) % V.tail_cap;
+  }
+  V.tail_len = V.tail_len + 1 - v_n;
+  return true;
+}
+
 void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, int t, cudaStream_t st) {
+  {
+    DecodeAppend da;
+    if (cache_append_decode_plan(c, k, v, dt, t, &da)) {
+      launch_decode_append(da, st);
+      return;
+    }
+  }
   if (t < 1) invalid("KVLayerCache::append: need at least one token");
   if (dt != KVMIX_F32 && dt != KVMIX_F16) invalid("unsupported dtype");
   if (!k || !v) invalid("KVLayerCache::append: null tensor");
@@ -625,22 +648,7 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
     else if (in16 && !tail16) launch_append<__half, float>(args, blocks, smem, k, v, st);
     else launch_append<__half, __half>(args, blocks, smem, k, v, st);
   };
-  const int gl = std::min(gs, D) / std::max(1, D / 32);
-  const bool decode = t == 1 && a.k_n == 0 && v_n <= 1 && fused && (D == 64 || D == 128) && (gl & (gl - 1)) == 0 &&
-                      gs % (D / 32) == 0;
-  if (decode) {
-    const bool in16 = dt == KVMIX_F16, tail16 = c->tail_dtype == KVMIX_F16;
-    const int blocks = (BH + kAppendThreads / 32 - 1) / (kAppendThreads / 32);
-    if (!in16 && !tail16)
-      append_decode_kernel<float, float><<<blocks, kAppendThreads, 0, st>>>(a, (const float*)k, (const float*)v);
-    else if (!in16 && tail16)
-      append_decode_kernel<float, __half><<<blocks, kAppendThreads, 0, st>>>(a, (const float*)k, (const float*)v);
-    else if (in16 && !tail16)
-      append_decode_kernel<__half, float><<<blocks, kAppendThreads, 0, st>>>(a, (const __half*)k, (const __half*)v);
-    else
-      append_decode_kernel<__half, __half><<<blocks, kAppendThreads, 0, st>>>(a, (const __half*)k, (const __half*)v);
-    after_launch("append_decode_kernel");
-  } else if (fused) {
+  if (fused) {
     a.phase = 0;
     launch(a, a.k_blocks + a.v_blocks + a.tail_blocks);
   } else {

@@ -116,6 +116,97 @@ __device__ inline float packed_value(bool key, const SideView& s, int bh, int64_
   return decode(code, meta_scale(m), meta_min(m), narrow);
 }
 
+// ---- decode-step append (t = 1, no Key group ages) --------------------------------------
+// Everything one warp needs to append one token of one (b, kv-head): the Key token goes to
+// its ring slot; the Value side ages one token (the oldest window token or the new one) and/or
+// stores the new token in its ring. Used by append_decode_kernel and, fused, by the
+// attention kernel's prologue (kvmix_append_attend).
+struct DecodeAppend {
+  int D, gs, BH;
+  int in16, tail16;          // input / window element types (fp16 or fp32)
+  const void* kin;           // [B*H][D] new Key token
+  const void* vin;           // [B*H][D] new Value token
+  void* k_tail;              // Key ring
+  int64_t k_cap, k_slot;     // ring capacity, slot of the new Key token
+  int v_age;                 // 1: one Value token ages
+  int v_stay;                // 1: the new Value token stays in the window
+  int vbits;
+  int64_t v_j;               // global index of the aged Value token
+  void* v_tail;
+  int64_t v_cap, v_start, v_L, v_slot;  // aged token: window slot v_start if v_L > 0, else the input
+  uint32_t* v_tiles;
+  uint32_t* v_meta;
+  int2* v_info;
+  SideView vv;
+};
+
+__device__ inline float da_load(const void* p, bool f16, size_t i) {
+  return f16 ? __half2float(static_cast<const __half*>(p)[i]) : static_cast<const float*>(p)[i];
+}
+__device__ inline void da_store(void* p, bool f16, size_t i, float x) {
+  if (f16) static_cast<__half*>(p)[i] = __float2half_rn(x);
+  else static_cast<float*>(p)[i] = x;
+}
+
+// one warp, lanes over D/32 channels (D in {64, 128}, power-of-two channel-group lanes)
+__device__ inline void decode_append_warp(const DecodeAppend& a, int bh, int lane) {
+  const int D = a.D, gs = a.gs, LC = D / 32;
+  {
+    const size_t dst = ((size_t)bh * a.k_cap + (size_t)a.k_slot) * D;
+    for (int c = 0; c < LC; ++c) {
+      const int d = lane * LC + c;
+      da_store(a.k_tail, a.tail16, dst + d, da_load(a.kin, a.in16, (size_t)bh * D + d));
+    }
+  }
+  if (a.v_age) {
+    const int q_max = q_max_for_bits(a.vbits);
+    float x[4];
+    for (int c = 0; c < LC; ++c) {
+      const int d = lane * LC + c;
+      // the window holds values already rounded to its element type; a new token is rounded
+      // to it first (cache.cpp keeps one precision per side)
+      x[c] = a.v_L > 0 ? da_load(a.v_tail, a.tail16, ((size_t)bh * a.v_cap + (size_t)a.v_start) * D + d)
+                       : (a.tail16 ? __half2float(__float2half_rn(da_load(a.vin, a.in16, (size_t)bh * D + d)))
+                                   : da_load(a.vin, a.in16, (size_t)bh * D + d));
+    }
+    float mn = x[0], mx = x[0];
+    for (int c = 1; c < LC; ++c) {
+      mn = x[c] < mn ? x[c] : mn;
+      mx = x[c] > mx ? x[c] : mx;
+    }
+    const int glanes = min(gs, D) / LC;
+    for (int o = 1; o < glanes; o <<= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mn, o), ox = __shfl_xor_sync(0xffffffffu, mx, o);
+      mn = om < mn ? om : mn;
+      mx = ox > mx ? ox : mx;
+    }
+    const uint32_t m = make_meta(mn, mx, q_max);
+    const int64_t j = a.v_j;
+    if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + lane * LC / gs] = m;
+    if (bh == 0 && lane == 0) a.v_info[j] = make_int2(1, 0);
+    const float sc = meta_scale(m), mnv = meta_min(m);
+    uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
+    for (int c = 0; c < LC; ++c) {
+      const int d = lane * LC + c;
+      const uint64_t si = (uint64_t)bh * D + d;  // segment [B,H,1,D]
+      tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
+    }
+  }
+  if (a.v_stay) {
+    const size_t dst = ((size_t)bh * a.v_cap + (size_t)a.v_slot) * D;
+    for (int c = 0; c < LC; ++c) {
+      const int d = lane * LC + c;
+      da_store(a.v_tail, a.tail16, dst + d, da_load(a.vin, a.in16, (size_t)bh * D + d));
+    }
+  }
+}
+
+// Host: if this append is a decode step the one-warp path handles, fill `out`, apply the
+// host bookkeeping of the append (counters, segments, ring positions) and return true; the
+// caller must then run decode_append_warp for every (b, kv-head) before the cache is read.
+bool cache_append_decode_plan(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, int t, DecodeAppend* out);
+void launch_decode_append(const DecodeAppend& da, cudaStream_t st);
+
 void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, int t, cudaStream_t st);
 void cache_snapshot(const kvmix_cache* c, float* keys, float* values, cudaStream_t st);
 void cache_export_segment(const kvmix_cache* c, int side, int idx, uint32_t* words, uint16_t* meta,

@@ -355,6 +355,16 @@ kvmix_status kvmix_attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, i
   });
 }
 
+kvmix_status kvmix_append_attend(kvmix_cache* c, const void* k, const void* v, kvmix_dtype kv_dt, int t, const void* q,
+                                 kvmix_dtype q_dt, int q_heads, int tq, float* out, double* checksum, void* stream) {
+  return guard([&] {
+    check_cache(c);
+    if (q_dt != KVMIX_F32 && q_dt != KVMIX_F16) invalid("unsupported dtype");
+    Workspace ws;
+    append_attend(c, k, v, kv_dt, t, q, q_dt, q_heads, tq, out, checksum, ws, as_stream(stream));
+  });
+}
+
 kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* q, kvmix_dtype dt,
                                  int q_heads, int t, float* const* out, void* stream) {
   return guard([&] {

@@ -253,3 +253,31 @@ def test_errors(cuda):
         K.attend(np.zeros((1, 1, 1, 64), np.float32), empty)
     with pytest.raises(K.KvmixInvalidArgument):
         K.attend(np.zeros((1, 3, 1, 64), np.float32), dev)
+
+
+@pytest.mark.parametrize("kb,vb,D,G,tail", [(2, 2, 128, 1, torch.float16), (3, 4, 128, 1, torch.float32),
+                                             (4, 2, 64, 2, torch.float16), (2, 4, 128, 1, torch.float32)])
+def test_append_attend_matches_separate_calls(cuda, kb, vb, D, G, tail):
+    """kvmix_append_attend (the append fused into the attention launch when it is a decode
+    step) == append() then attend(): identical outputs, identical cache state, and the fused
+    path is the one that runs in the steady state."""
+    B, H = 2, 3
+    fused = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, 0.1, 0.1, 32), B, H, D, capacity_tokens=700, tail_dtype=tail)
+    sep = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, 0.1, 0.1, 32), B, H, D, capacity_tokens=700, tail_dtype=tail)
+    pre = torch.from_numpy(O.random_h16(70, (B, H, 500, D))).cuda()
+    pre_v = torch.from_numpy(O.random_h16(71, (B, H, 500, D))).cuda()
+    fused.append(pre, pre_v)
+    sep.append(pre, pre_v)
+    n_fused = 0
+    for s in range(80):
+        k = torch.from_numpy(O.random_h16(100 + s, (B, H, 1, D))).cuda().half()
+        v = torch.from_numpy(O.random_h16(300 + s, (B, H, 1, D))).cuda().half()
+        q = torch.from_numpy(O.random_h16(500 + s, (B, H * G, 1, D))).cuda()
+        a0 = K.launch_count_of("append_decode_kernel") + K.launch_count_of("append_kernel")
+        r1 = K.append_attend(fused, k, v, q)
+        n_fused += (K.launch_count_of("append_decode_kernel") + K.launch_count_of("append_kernel")) == a0
+        sep.append(k, v)
+        r2 = K.attend(q, sep, checksum=False)
+        assert torch.equal(r1.output, r2.output), s
+    assert fused.dump() == sep.dump()
+    assert n_fused >= 60  # steady-state steps ran as one launch
