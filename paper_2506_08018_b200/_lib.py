@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkvmix_b200.so")
+LIB_PATH = os.environ.get("KVMIX_LIB") or os.path.join(HERE, "libkvmix_b200.so")
 
 OK, INVALID_ARGUMENT, OUT_OF_RANGE, RUNTIME_ERROR, CUDA_ERROR, OUT_OF_MEMORY = range(6)
 F32, F16 = 0, 1

@@ -53,7 +53,10 @@ namespace {
 
 constexpr int kMmaWarps = 4;
 #ifndef KVB_MIN_CTAS
-#define KVB_MIN_CTAS(KB) 4  // CTAs per SM the register budget is sized for
+#ifndef KVB_MIN_CTAS_N
+#define KVB_MIN_CTAS_N 4
+#endif
+#define KVB_MIN_CTAS(KB) KVB_MIN_CTAS_N  // CTAs per SM the register budget is sized for
 #endif
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -212,9 +215,16 @@ struct MmaParams {
   int q16, tail16;
   int H, Hq, tq, rows, gs, cg;
   int64_t T, P;  // total tokens; fast-path limit (multiple of gs)
+  int64_t Pw;    // window blocks cover tokens [P, Pw) (Keys fp16 in the ring, Values packed)
+  int nwb;       // window blocks per (b, kv-head)
   // stream-K work list: per (b, kv-head) U = Gf fast groups + ceil((T - P) / kTailUnit)
   // tail units, N = BH * U units in bh-major order; warp w of W takes [w N / W, (w+1) N / W)
   int Gf, U, N;  // 32-bit: the host falls back to the generic path beyond 2^31 units
+  // cost-weighted split: a group costs Qc, a window token 1; (b, kv-head) cost cost_bh =
+  // Qc Gf + (U - Gf), total Nc = BH cost_bh; warp w owns the units starting in cost range
+  // [w Nc / W, (w+1) Nc / W)
+  int Qc;
+  int64_t cost_bh, Nc;
   int Grec;      // group records per (b, kv-head) (bh stride of the record array)
   int W;
   int stages;
@@ -228,6 +238,7 @@ struct MmaParams {
   unsigned long long epoch;
   int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
   int tail_unit;     // window tokens per work unit
+  int skip_tail;     // profiling only (KVMIX_PROF_SKIP_TAIL): leave the window out
   float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
   float* part_acc;
   double* part_cs;
@@ -237,6 +248,16 @@ struct MmaParams {
 // token (lane-parallel dequantization of partially aged Values, no TMA staging), so units
 // are small to keep the stream-K ranges balanced (KVMIX_TAIL_UNIT overrides, for tuning).
 constexpr int kTailUnit = 1;
+constexpr int kGroupCost = 1;  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
+
+// first unit whose start cost is >= c (units: Gf groups of cost Qc, then window units of 1)
+__device__ __forceinline__ int unit_at_cost(const MmaParams& p, int64_t c) {
+  const int bh = (int)(c / p.cost_bh);
+  const int64_t cl = c - (int64_t)bh * p.cost_bh;
+  const int64_t gcost = (int64_t)p.Qc * p.Gf;
+  const int64_t local = cl <= gcost ? (cl + p.Qc - 1) / p.Qc : p.Gf + (cl - gcost);
+  return bh * p.U + (int)local;
+}
 
 // Dequantized packed element (token j < quantized, channel d) with compile-time D.
 template <int D, bool KEY, int BITS>
@@ -270,8 +291,9 @@ struct WarpLayout {
   static constexpr int kKB = 8 * 4 * (D / 32) * 2 * 4;
   static constexpr int kK = KB == 3 ? 2 * kKB + 2 * D * 4 : kKB;
   static constexpr int kV = (D / 32) * 8 * 32;
+  static constexpr int kQ = D * 4;  // q of all channels (window blocks)
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
-    const size_t n = (size_t)stages * stage_bytes + kK + kV + (size_t)stages * 8;
+    const size_t n = (size_t)stages * stage_bytes + kK + kV + kQ + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
   }
 };
@@ -310,7 +332,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   const int CG = GS ? D / GS : p.cg;
   const int NBLK = gs / 32;  // 32-token blocks per group
   const int S = p.stages;
-  const int u_beg = (int)((int64_t)wg * p.N / p.W), u_end = (int)((int64_t)(wg + 1) * p.N / p.W);
+  const int64_t c_beg = (int64_t)wg * p.Nc / p.W, c_end = (int64_t)(wg + 1) * p.Nc / p.W;
+  const int u_beg = unit_at_cost(p, c_beg), u_end = unit_at_cost(p, c_end);
+  if (u_beg >= u_end) {  // no unit starts in this cost range: neutral partial for the combine
+    const int bh = (int)(c_beg / p.cost_bh);
+    if (lane < p.rows) p.part_ml[((size_t)wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
+    if (lane == 0 && p.want_cs) p.part_cs[(size_t)wg + bh] = 0.0;
+    return;
+  }
 
   uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
   uint8_t* ring = wbase;
@@ -319,7 +348,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   float* ytab = reinterpret_cast<float*>(kstage + 2 * WL::kKB);
   uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + 2 * WL::kKB + D * 4);
   uint8_t* vbs = kstage + WL::kK;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vbs + WL::kV);
+  float* qbuf = reinterpret_cast<float*>(vbs + WL::kV);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vbs + WL::kV + WL::kQ);
 
   // zero the B staging (columns of absent query rows / digits must stay 0)
   {
@@ -477,6 +507,121 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         accv[mt][0] = accv[mt][1] = accv[mt][2] = accv[mt][3] = 0;
       }
       nacc = 0;
+    };
+
+    // Value k-step of one 32-token block: lane (g, t) owns token j = g + 8t (p of it for every
+    // row in pr); fixed-point exponent / fold bookkeeping, B digits, 8 IMMA.
+    auto value_block = [&](const uint32_t* vt2, const uint32_t* vm2, const float (&pr)[R], float alpha, bool tok_ok) {
+      const int j = g + 8 * t;
+      float sv[CGMAX], mv[CGMAX];
+      {
+        const uint32_t* vmt = vm2 + (size_t)j * CG;
+        if constexpr (GS != 0 && D / (GS ? GS : 1) == 4) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(vmt);
+          const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float2 f = meta_pair(w4[c]);
+            sv[c] = f.x;
+            mv[c] = f.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CGMAX; ++c) {
+            const float2 f = meta_pair(c < CG ? vmt[c] : 0u);
+            sv[c] = f.x;
+            mv[c] = f.y;
+          }
+        }
+      }
+      if (!tok_ok) {  // window block past the aged Values: rows never written
+#pragma unroll
+        for (int c = 0; c < CGMAX; ++c) sv[c] = mv[c] = 0.f;
+      }
+      // fixed-point exponent: max scale of the block * 2^E < 2^30 (p <= 1)
+      float smax = sv[0];
+#pragma unroll
+      for (int c = 1; c < CGMAX; ++c) smax = fmaxf(smax, sv[c]);
+      const uint32_t smu = __reduce_max_sync(0xffffffffu, __float_as_uint(smax));
+      // (p <= 2^kLazy): y = p s 2^E < 2^30 for E <= e_blk
+      const int e_blk = min(156 - kLazy - (int)((smu >> 23) & 0xffu), 100);
+      if (!dirty) {
+        e_cur = e_blk - kEHead;
+      } else {
+        const bool moved = __any_sync(0xffffffffu, row_ok && alpha != 1.0f);
+        if (moved || e_cur > e_blk || nacc >= p.flush_blocks) {
+          flush(alpha);
+          if (moved) {
+            const float ax = __shfl_xor_sync(0xffffffffu, alpha, 2);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+              for (int c = 0; c < CGMAX; ++c) bias[r][c] *= (r == my_r) ? alpha : ax;
+          }
+          e_cur = e_blk - kEHead;
+        }
+      }
+      dirty = true;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < CGMAX; ++c) bias[r][c] = fmaf(pr[r], mv[c], bias[r][c]);
+      // B digits of y = p s 2^E (u8, four columns per row) -> vbs[c][4r + n][pos(j)]
+      {
+        const float pe = pow2i(e_cur);
+        float ppe[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) ppe[r] = pr[r] * pe;
+        const int pos = ((g >> 2) + 2 * (t & 1)) * 8 + (t >> 1) * 4 + (g & 3);
+#pragma unroll
+        for (int c = 0; c < CGMAX; ++c) {
+          if (GS == 0 && c >= CG) break;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const uint32_t v = (uint32_t)__float2int_rn(ppe[r] * sv[c]);
+            uint8_t* dst = vbs + c * 256 + (4 * r) * 32 + pos;
+            dst[0] = (uint8_t)v;
+            dst[32] = (uint8_t)(v >> 8);
+            dst[64] = (uint8_t)(v >> 16);
+            dst[96] = (uint8_t)(v >> 24);
+          }
+        }
+      }
+      __syncwarp();
+      {
+        uint32_t vw0[VW], vw1[VW];
+        lds_tile<D, VB>(vt2, lane, vw0);
+        lds_tile<D, VB>(vt2 + tile_words(D, VB), lane, vw1);
+        uint32_t vb[CGMAX][2];
+        if constexpr (GS != 0) {
+#pragma unroll
+          for (int c = 0; c < CGMAX; ++c) {
+            if (c < D / (GS ? GS : 1)) {
+              const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
+              vb[c][0] = x.x;
+              vb[c][1] = x.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int mt = 0; mt < NM; ++mt) {
+          const int q0 = mt, q1 = mt + NM;
+          const uint32_t a0 = vw0[q0 / CV] & (VMASK << (VB * (q0 % CV)));
+          const uint32_t a1 = vw0[q1 / CV] & (VMASK << (VB * (q1 % CV)));
+          const uint32_t a2 = vw1[q0 / CV] & (VMASK << (VB * (q0 % CV)));
+          const uint32_t a3 = vw1[q1 / CV] & (VMASK << (VB * (q1 % CV)));
+          if constexpr (GS != 0) {
+            const int c = (mt * 16) / (GS ? GS : 1);
+            imma_uu(accv[mt], a0, a1, a2, a3, vb[c][0], vb[c][1]);
+          } else {
+            const int c = (mt * 16) / gs;
+            const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
+            imma_uu(accv[mt], a0, a1, a2, a3, x.x, x.y);
+          }
+        }
+      }
+      ++nacc;
+      __syncwarp();  // vbs is rewritten by the next block
     };
 
     const int g_stop = min(hi, p.Gf);
@@ -694,117 +839,98 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
           for (int r = 0; r < R; ++r) pr[r] = (r == my_r) ? mine : recv;
         }
-        float sv[CGMAX], mv[CGMAX];
-        {
-          const uint32_t* vmt = vm2 + (size_t)j * CG;
-          if constexpr (GS != 0 && D / (GS ? GS : 1) == 4) {
-            const uint4 q4 = *reinterpret_cast<const uint4*>(vmt);
-            const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float2 f = meta_pair(w4[c]);
-              sv[c] = f.x;
-              mv[c] = f.y;
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < CGMAX; ++c) {
-              const float2 f = meta_pair(c < CG ? vmt[c] : 0u);
-              sv[c] = f.x;
-              mv[c] = f.y;
-            }
-          }
-        }
-        // fixed-point exponent: max scale of the block * 2^E < 2^30 (p <= 1)
-        float smax = sv[0];
-#pragma unroll
-        for (int c = 1; c < CGMAX; ++c) smax = fmaxf(smax, sv[c]);
-        const uint32_t smu = __reduce_max_sync(0xffffffffu, __float_as_uint(smax));
-        // (p <= 2^kLazy): y = p s 2^E < 2^30 for E <= e_blk
-        const int e_blk = min(156 - kLazy - (int)((smu >> 23) & 0xffu), 100);
-        if (!dirty) {
-          e_cur = e_blk - kEHead;
-        } else {
-          const bool moved = __any_sync(0xffffffffu, row_ok && alpha != 1.0f);
-          if (moved || e_cur > e_blk || nacc >= p.flush_blocks) {
-            flush(alpha);
-            if (moved) {
-              const float ax = __shfl_xor_sync(0xffffffffu, alpha, 2);
-#pragma unroll
-              for (int r = 0; r < R; ++r)
-#pragma unroll
-                for (int c = 0; c < CGMAX; ++c) bias[r][c] *= (r == my_r) ? alpha : ax;
-            }
-            e_cur = e_blk - kEHead;
-          }
-        }
-        dirty = true;
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int c = 0; c < CGMAX; ++c) bias[r][c] = fmaf(pr[r], mv[c], bias[r][c]);
-        // B digits of y = p s 2^E (u8, four columns per row) -> vbs[c][4r + n][pos(j)]
-        {
-          const float pe = pow2i(e_cur);
-          float ppe[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) ppe[r] = pr[r] * pe;
-          const int pos = ((g >> 2) + 2 * (t & 1)) * 8 + (t >> 1) * 4 + (g & 3);
-#pragma unroll
-          for (int c = 0; c < CGMAX; ++c) {
-            if (GS == 0 && c >= CG) break;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const uint32_t v = (uint32_t)__float2int_rn(ppe[r] * sv[c]);
-              uint8_t* dst = vbs + c * 256 + (4 * r) * 32 + pos;
-              dst[0] = (uint8_t)v;
-              dst[32] = (uint8_t)(v >> 8);
-              dst[64] = (uint8_t)(v >> 16);
-              dst[96] = (uint8_t)(v >> 24);
-            }
-          }
-        }
-        __syncwarp();
-        {
-          uint32_t vw0[VW], vw1[VW];
-          lds_tile<D, VB>(vt2, lane, vw0);
-          lds_tile<D, VB>(vt2 + tile_words(D, VB), lane, vw1);
-          uint32_t vb[CGMAX][2];
-          if constexpr (GS != 0) {
-#pragma unroll
-            for (int c = 0; c < CGMAX; ++c) {
-              if (c < D / (GS ? GS : 1)) {
-                const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
-                vb[c][0] = x.x;
-                vb[c][1] = x.y;
-              }
-            }
-          }
-#pragma unroll
-          for (int mt = 0; mt < NM; ++mt) {
-            const int q0 = mt, q1 = mt + NM;
-            const uint32_t a0 = vw0[q0 / CV] & (VMASK << (VB * (q0 % CV)));
-            const uint32_t a1 = vw0[q1 / CV] & (VMASK << (VB * (q1 % CV)));
-            const uint32_t a2 = vw1[q0 / CV] & (VMASK << (VB * (q0 % CV)));
-            const uint32_t a3 = vw1[q1 / CV] & (VMASK << (VB * (q1 % CV)));
-            if constexpr (GS != 0) {
-              const int c = (mt * 16) / (GS ? GS : 1);
-              imma_uu(accv[mt], a0, a1, a2, a3, vb[c][0], vb[c][1]);
-            } else {
-              const int c = (mt * 16) / gs;
-              const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
-              imma_uu(accv[mt], a0, a1, a2, a3, x.x, x.y);
-            }
-          }
-        }
-        ++nacc;
-        __syncwarp();  // vbs is rewritten by the next block
+        value_block(vt2, vm2, pr, alpha, true);
       }
       // refill this stage S groups ahead
       issue_next(s);
       if (++s == S) {
         s = 0;
         phase ^= 1u;
+      }
+    }
+
+    // ---- window blocks: 32 tokens of the full-precision Key window whose Values are packed
+    // (Keys: lane = token fp32 dot products from the ring; Values: the IMMA block path on the
+    // partial group's tiles). Waits for the fused append when an earlier warp made it.
+    if (p.fused && lo > p.Gf && hi > p.Gf) {
+      while (ld_acquire(p.flags + bh) != p.epoch) __nanosleep(32);
+    }
+    if constexpr (R == 1) {
+      const int wb_lo = max(lo, p.Gf) - p.Gf, wb_hi = min(hi, p.Gf + p.nwb) - p.Gf;
+      if (wb_lo < wb_hi) {
+        // q of every channel for the lane = token dot products
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qbuf[4 * Lq + c] = qv[0][c];
+        __syncwarp();
+      }
+      for (int wb = wb_lo; wb < wb_hi; ++wb) {
+        const int64_t j0 = p.P + 32 * (int64_t)wb;
+        const int jt = g + 8 * t;
+        const int64_t jj = j0 + jt;
+        const bool valid = jj < p.Pw;
+        float sl = -INFINITY;
+        if (valid) {
+          int64_t slot = p.k.tail_start + (jj - p.k.quantized);
+          if (slot >= p.k.tail_cap) slot -= p.k.tail_cap;
+          float acc = 0.f;
+          if (p.tail16) {
+            const uint4* row = reinterpret_cast<const uint4*>(static_cast<const __half*>(p.k.tail) +
+                                                              ((size_t)bh * p.k.tail_cap + (size_t)slot) * D);
+#pragma unroll 4
+            for (int ch = 0; ch < D / 8; ++ch) {
+              const uint4 hv = __ldcg(row + ch);
+              const float4 qa = *reinterpret_cast<const float4*>(qbuf + 8 * ch);
+              const float4 qb = *reinterpret_cast<const float4*>(qbuf + 8 * ch + 4);
+              const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&hv.x));
+              const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hv.y));
+              const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&hv.z));
+              const float2 f3 = __half22float2(*reinterpret_cast<const __half2*>(&hv.w));
+              acc = fmaf(qa.x, f0.x, acc);
+              acc = fmaf(qa.y, f0.y, acc);
+              acc = fmaf(qa.z, f1.x, acc);
+              acc = fmaf(qa.w, f1.y, acc);
+              acc = fmaf(qb.x, f2.x, acc);
+              acc = fmaf(qb.y, f2.y, acc);
+              acc = fmaf(qb.z, f3.x, acc);
+              acc = fmaf(qb.w, f3.y, acc);
+            }
+          } else {
+            const float4* row = reinterpret_cast<const float4*>(static_cast<const float*>(p.k.tail) +
+                                                                ((size_t)bh * p.k.tail_cap + (size_t)slot) * D);
+#pragma unroll 4
+            for (int ch = 0; ch < D / 4; ++ch) {
+              const float4 kv4 = __ldcg(row + ch);
+              const float4 qa = *reinterpret_cast<const float4*>(qbuf + 4 * ch);
+              acc = fmaf(qa.x, kv4.x, acc);
+              acc = fmaf(qa.y, kv4.y, acc);
+              acc = fmaf(qa.z, kv4.z, acc);
+              acc = fmaf(qa.w, kv4.w, acc);
+            }
+          }
+          const float scn = acc * p.inv;
+          if (p.want_cs) cs += (double)scn;
+          sl = scn * kLog2e;
+        }
+        float tmax = sl;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        // every lane scores a token of row 0: use row 0's reference max (lanes t >= 2 carry
+        // the unused row 1 of the fast blocks)
+        const float m_ref = __shfl_sync(0xffffffffu, m_run, 0);
+        const float m_new = tmax > m_ref + (float)kLazy ? tmax : m_ref;
+        const float alpha = fast_exp2(m_ref - m_new);
+        const float pj = valid ? fast_exp2(sl - m_new) : 0.f;
+        // l of row 0 in the lanes t = 0, 1 convention: the quad (g, 0..3) holds tokens g, g+8, 16+g, 24+g
+        float quad = pj + __shfl_xor_sync(0xffffffffu, pj, 1);
+        quad += __shfl_xor_sync(0xffffffffu, quad, 2);
+        l_run = l_run * alpha + quad;
+        m_run = m_new;
+        const int gi = (int)(j0 / gs), bi = (int)((j0 - (int64_t)gi * gs) / 32);
+        const uint8_t* rec = reinterpret_cast<const uint8_t*>(p.k.tiles) + ((size_t)bh * p.Grec + gi) * p.stage_bytes;
+        const uint32_t* vt2 = reinterpret_cast<const uint32_t*>(rec + p.kt_bytes) + (size_t)(2 * bi) * tile_words(D, VB);
+        const uint32_t* vm2 = reinterpret_cast<const uint32_t*>(rec + p.kt_bytes + p.vt_bytes) + (size_t)(32 * bi) * CG;
+        const float pr[R] = {pj};
+        value_block(vt2, vm2, pr, alpha, valid);
       }
     }
 
@@ -847,12 +973,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       }
 
     // ---- tokens past the fast region: lane-parallel over channels ------------------------
-    const int64_t j_lo = p.P + (int64_t)max(lo - p.Gf, 0) * p.tail_unit;
-    const int64_t j_hi = hi > p.Gf ? min(p.T, p.P + (int64_t)(hi - p.Gf) * p.tail_unit) : j_lo;
+    const int tb0 = p.Gf + p.nwb;  // first lane-parallel window unit
+    const int64_t j_lo = p.Pw + (int64_t)max(lo - tb0, 0) * p.tail_unit;
+    const int64_t j_hi = hi > tb0 && !p.skip_tail ? min(p.T, p.Pw + (int64_t)(hi - tb0) * p.tail_unit) : j_lo;
     if (j_lo < j_hi) {
-      if (p.fused && lo > p.Gf) {  // appended by an earlier warp (resident: in-order dispatch)
-        while (ld_acquire(p.flags + bh) != p.epoch) __nanosleep(32);
-      }
       const int d0 = lane * LC;
       float qt[R][LC];
 #pragma unroll
@@ -987,16 +1111,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 // this kernel with the attention kernel's tail measured bimodal step times; not used.)
 constexpr int kCombineWarps = 4;
 __global__ void __launch_bounds__(kCombineWarps * 32) attend_combine_sk_kernel(
-    const float2* __restrict__ part_ml, const float* __restrict__ part_acc, int N, int W, int U, int R, int BH, int H,
-    int Hq, int tq, int D, float* __restrict__ out) {
+    const float2* __restrict__ part_ml, const float* __restrict__ part_acc, int64_t Nc, int W, int64_t cost_bh, int Qc,
+    int Gf, int ntail, int R, int BH, int H, int Hq, int tq, int D, float* __restrict__ out) {
   const int item = blockIdx.x * kCombineWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (item >= BH * R) return;
   const int bh = item / R, r = item % R;
   const int b = bh / H, h = bh % H, G = Hq / H;
   const int gi = r / tq, qi = r % tq;
   const int hq = h * G + gi;
-  const int w0 = (int)((((int64_t)bh * U + 1) * W - 1) / N);
-  const int w1 = (int)((((int64_t)bh + 1) * U * W - 1) / N);  // 64-bit products
+  // warp owning a unit that starts at cost sx: floor(((sx + 1) W - 1) / Nc)
+  const int64_t s0 = (int64_t)bh * cost_bh;
+  const int64_t s1 = s0 + (ntail > 0 ? (int64_t)Qc * Gf + ntail - 1 : (int64_t)Qc * (Gf - 1));
+  const int w0 = (int)(((s0 + 1) * W - 1) / Nc);
+  const int w1 = (int)(((s1 + 1) * W - 1) / Nc);
   float M = -INFINITY;
   for (int w = w0 + lane; w <= w1; w += 32) M = fmaxf(M, part_ml[((size_t)w + bh) * R + r].x);
 #pragma unroll
@@ -1125,13 +1252,26 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.cg = c->cgroups();
   p.T = T;
   p.P = (std::min(c->k.quantized, c->v.quantized) / gs) * gs;
+  // window blocks: one query row, the Key window starting at P (Keys age in whole groups)
+  p.Pw = p.P;
+  p.nwb = 0;
+  if (rows == 1 && c->k.quantized == p.P && !getenv("KVMIX_PROF_NO_WINDOW")) {
+    p.Pw = std::min(T, c->v.quantized);
+    if (p.Pw > p.P) p.nwb = (int)((p.Pw - p.P + 31) / 32);
+    else p.Pw = p.P;
+  }
   p.tail_unit = kTailUnit;
+  p.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
   if (const char* e = getenv("KVMIX_TAIL_UNIT")) p.tail_unit = std::max(1, std::min(64, atoi(e)));
-  const int64_t U = p.P / gs + (T - p.P + p.tail_unit - 1) / p.tail_unit;
+  const int64_t U = p.P / gs + p.nwb + (T - p.Pw + p.tail_unit - 1) / p.tail_unit;
   if ((int64_t)BH * U >= (int64_t)1 << 31) return false;
   p.Gf = (int)(p.P / gs);
   p.U = (int)U;
   p.N = BH * p.U;
+  p.Qc = kGroupCost;
+  if (const char* e = getenv("KVMIX_GROUP_COST")) p.Qc = std::max(1, std::min(64, atoi(e)));
+  p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
+  p.Nc = (int64_t)BH * p.cost_bh;
   p.kt_bytes = (uint32_t)((gs / 16) * c->k.tile_words * 4);
   p.vt_bytes = (uint32_t)((gs / 16) * c->v.tile_words * 4);
   p.vm_bytes = (uint32_t)(gs * p.cg * 4);
@@ -1168,7 +1308,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   {
     const int items = BH * rows;
     attend_combine_sk_kernel<<<(items + kCombineWarps - 1) / kCombineWarps, kCombineWarps * 32, 0, st>>>(
-        p.part_ml, p.part_acc, p.N, p.W, p.U, rows, BH, c->H, Hq, tq, D, out);
+        p.part_ml, p.part_acc, p.Nc, p.W, p.cost_bh, p.Qc, p.Gf, p.U - p.Gf, rows, BH, c->H, Hq, tq, D, out);
   }
   after_launch("attend_combine_sk_kernel");
   if (checksum) {

@@ -281,3 +281,21 @@ def test_append_attend_matches_separate_calls(cuda, kb, vb, D, G, tail):
         assert torch.equal(r1.output, r2.output), s
     assert fused.dump() == sep.dump()
     assert n_fused >= 60  # steady-state steps ran as one launch
+
+
+@pytest.mark.parametrize("kb,vb,gs,rk,rv,tail", [(2, 2, 32, 0.1, 0.1, torch.float32), (3, 4, 32, 0.2, 0.2, torch.float16),
+                                                 (2, 4, 64, 0.1, 0.1, torch.float16), (4, 2, 32, 0.1, 0.3, torch.float32)])
+def test_attend_window_blocks_through_a_cycle(cuda, kb, vb, gs, rk, rv, tail):
+    """The Key window (full precision, Values already packed) runs through the IMMA Value
+    path in 32-token window blocks. Walk a whole Key age-out cycle one decode step at a time
+    with many (b, kv-head) so warps mix fast groups, window blocks and window tokens."""
+    B, H, D = 1, 32, 128
+    dev, ora = build(kb, vb, rk, rv, gs, B, H, D, [1500], seed=61, tail_dtype=tail, cap=1600)
+    q = O.random_h16(62, (B, H, 1, D), sigma=1.5)
+    for s in range(40):
+        k = O.random_h16(700 + s, (B, H, 1, D))
+        v = O.random_h16(800 + s, (B, H, 1, D))
+        dev.append(k, v)
+        ora.append(k, v)
+        if s % 3 == 0 or s > 34:
+            check_attend(dev, ora, q, expect_mma=True)
