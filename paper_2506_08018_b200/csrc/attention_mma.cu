@@ -37,8 +37,9 @@
 //
 // Work distribution (stream-K): a list of per-(b, kv-head) units (fast groups, then tail
 // units of the full-precision window) is cut into equal ranges over one resident wave of
-// independent warps; each warp writes one partial (m, l, acc) per (b, kv-head) segment it
-// touches, merged in warp order by attend_combine_sk_kernel (deterministic).
+// independent warps. A (b, kv-head) inside one warp's range is normalized and written by that
+// warp; one split across warps is merged (in warp order: deterministic) by the last of its
+// warps to publish a partial (tagged atomic counter) -- no separate combine launch.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -236,6 +237,8 @@ struct MmaParams {
   DecodeAppend da;
   unsigned long long* flags;  // per (b, kv-head): epoch once its append is done
   unsigned long long epoch;
+  unsigned long long* cnt;    // per (b, kv-head): {call tag, partials published} (merge by the last)
+  float* out;
   int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
   int tail_unit;     // window tokens per work unit
   int skip_tail;     // profiling only (KVMIX_PROF_SKIP_TAIL): leave the window out
@@ -281,6 +284,74 @@ __device__ __forceinline__ float tail_val(const SideView& s, bool f16, int bh, i
   return f16 ? tail_at<__half>(s, bh, j, d, D) : tail_at<float>(s, bh, j, d, D);
 }
 
+// warp owning the unit that starts at cost sx: floor(((sx + 1) W - 1) / Nc)
+__device__ __forceinline__ int warp_at_cost(const MmaParams& p, int64_t sx) {
+  return (int)(((sx + 1) * p.W - 1) / p.Nc);
+}
+// first and last warp whose ranges hold units of (b, kv-head) bh
+__device__ __forceinline__ void bh_warps(const MmaParams& p, int bh, int& w0, int& w1) {
+  const int64_t s0 = (int64_t)bh * p.cost_bh;
+  const int ntail = p.U - p.Gf;
+  const int64_t s1 = s0 + (ntail > 0 ? (int64_t)p.Qc * p.Gf + ntail - 1 : (int64_t)p.Qc * (p.Gf - 1));
+  w0 = warp_at_cost(p, s0);
+  w1 = warp_at_cost(p, s1);
+}
+
+// Publish this warp's partial of bh; returns true for the last of the bh's warps to arrive
+// (the counter word carries the call's tag, so it needs no clearing between calls).
+__device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane) {
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    int w0, w1;
+    bh_warps(p, bh, w0, w1);
+    const unsigned long long tag = p.epoch & 0xffffffffull;
+    unsigned long long* cw = p.cnt + bh;
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cw), assumed;
+    unsigned int ct;
+    do {
+      assumed = old;
+      ct = (assumed >> 32) == tag ? (unsigned int)assumed : 0u;
+      old = atomicCAS(cw, assumed, (tag << 32) | (ct + 1u));
+    } while (old != assumed);
+    last = (int)(ct + 1u) == w1 - w0 + 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) __threadfence();
+  return last != 0;
+}
+
+// Merge the partials of warps w0..w1 of bh in warp order (deterministic) -> out.
+template <int D>
+__device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane) {
+  constexpr int LC = D / 32;
+  int w0, w1;
+  bh_warps(p, bh, w0, w1);
+  const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
+  for (int r = 0; r < p.rows; ++r) {
+    float M = -INFINITY;
+    for (int w = w0; w <= w1; ++w) M = fmaxf(M, __ldcg(&p.part_ml[((size_t)w + bh) * p.rows + r]).x);
+    float L = 0.f, a[LC];
+#pragma unroll
+    for (int c = 0; c < LC; ++c) a[c] = 0.f;
+    for (int w = w0; w <= w1; ++w) {
+      const size_t pi = ((size_t)w + bh) * p.rows + r;
+      const float2 ml = __ldcg(&p.part_ml[pi]);
+      if (ml.x == -INFINITY) continue;
+      const float f = expf(ml.x - M);
+      L += ml.y * f;
+#pragma unroll
+      for (int c = 0; c < LC; ++c) a[c] += __ldcg(&p.part_acc[pi * D + lane * LC + c]) * f;
+    }
+    const int gi = r / p.tq, qi = r % p.tq;
+    float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
+    const float il = 1.0f / L;
+#pragma unroll
+    for (int c = 0; c < LC; ++c) o[c] = a[c] * il;
+  }
+}
+
 // Per-warp dynamic shared layout (bytes):
 //   ring[S][stage_bytes] | kstage | vbs[CGMAX][8][32] u8 | bars[S] u64
 // kstage: kbs[planes][8 cols][4 t][NK][2] u32 (digit words of the Key B fragments; 3-bit
@@ -291,7 +362,7 @@ struct WarpLayout {
   static constexpr int kKB = 8 * 4 * (D / 32) * 2 * 4;
   static constexpr int kK = KB == 3 ? 2 * kKB + 2 * D * 4 : kKB;
   static constexpr int kV = (D / 32) * 8 * 32;
-  static constexpr int kQ = D * 4;  // q of all channels (window blocks)
+  static constexpr int kQ = D * 4 + 32 * 8;  // q of all channels (window blocks), checksum slots
   __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
     const size_t n = (size_t)stages * stage_bytes + kK + kV + kQ + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
@@ -334,10 +405,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   const int S = p.stages;
   const int64_t c_beg = (int64_t)wg * p.Nc / p.W, c_end = (int64_t)(wg + 1) * p.Nc / p.W;
   const int u_beg = unit_at_cost(p, c_beg), u_end = unit_at_cost(p, c_end);
-  if (u_beg >= u_end) {  // no unit starts in this cost range: neutral partial for the combine
+  if (u_beg >= u_end) {  // no unit starts in this cost range: neutral partial
     const int bh = (int)(c_beg / p.cost_bh);
+    int w0, w1;
+    bh_warps(p, bh, w0, w1);
+    if (wg < w0 || wg > w1) return;
     if (lane < p.rows) p.part_ml[((size_t)wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
     if (lane == 0 && p.want_cs) p.part_cs[(size_t)wg + bh] = 0.0;
+    if (arrive_last(p, bh, lane)) merge_bh<D>(p, bh, lane);
     return;
   }
 
@@ -349,6 +424,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + 2 * WL::kKB + D * 4);
   uint8_t* vbs = kstage + WL::kK;
   float* qbuf = reinterpret_cast<float*>(vbs + WL::kV);
+  double* csm = reinterpret_cast<double*>(vbs + WL::kV + D * 4);  // per-lane checksum partials
   uint64_t* bars = reinterpret_cast<uint64_t*>(vbs + WL::kV + WL::kQ);
 
   // zero the B staging (columns of absent query rows / digits must stay 0)
@@ -365,11 +441,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   // this lane's softmax row: lanes t = 2r, 2r+1 hold row r (IMMA score columns 4r .. 4r+3)
   const int my_r = t >> 1;
   const bool row_ok = my_r < p.rows;
-  const uint64_t policy = evict_first_policy();
 
   // producer: this warp's fast groups in work-list order, issued S ahead of the consumer
   // (running record pointer, groups left in the current (b, kv-head), groups left to issue)
-  const uint8_t* src_rec;
+  int rec_i;  // group record index (records of all (b, kv-head) are one array)
   int left_bh, left_all;
   {
     int i_bh = u_beg / p.U, i_g = u_beg - i_bh * p.U;
@@ -377,7 +452,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       ++i_bh;
       i_g = 0;
     }
-    src_rec = reinterpret_cast<const uint8_t*>(p.k.tiles) + ((size_t)i_bh * p.Grec + i_g) * p.stage_bytes;
+    rec_i = i_bh * p.Grec + i_g;
     left_bh = p.Gf - i_g;
     // fast groups of [u_beg, u_end): whole (b, kv-head) ranges clipped at both ends
     const int bh0 = u_beg / p.U, bh1 = (u_end - 1) / p.U;
@@ -388,17 +463,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     }
     left_all = n;
   }
-  const size_t skip_bytes = (size_t)(p.Grec - p.Gf) * p.stage_bytes;
   auto issue_next = [&](int s) {
     if (left_all > 0) {
       if (lane == 0) {
         mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
-        bulk_g2s(ring + (size_t)s * p.stage_bytes, src_rec, p.stage_bytes, &bars[s], policy);
+        bulk_g2s(ring + (size_t)s * p.stage_bytes,
+                 reinterpret_cast<const uint8_t*>(p.k.tiles) + (size_t)rec_i * p.stage_bytes, p.stage_bytes, &bars[s],
+                 evict_first_policy());
       }
       --left_all;
-      src_rec += p.stage_bytes;
+      ++rec_i;
       if (--left_bh == 0) {
-        src_rec += skip_bytes;
+        rec_i += p.Grec - p.Gf;
         left_bh = p.Gf;
       }
     }
@@ -429,6 +505,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   // 3-bit Keys: 4 * 2^-class of the high-bit plane (class q for D = 128), channel offset
   // of this (b, kv-head) in the Mixed3 stream mod 11, and the channel -> field table
   const float clsH = K3 ? 4.f * pow2i(-((kkL + NK * hL) & 7)) : 0.f;
+  const float invL = pow2i(KB2 * ((kkL + NK * hL) % CK));  // 1 / clsL
+  const float clsHL = clsH * invL;                          // clsH / clsL
   if constexpr (K3) {
     for (int d = lane; d < D; d += 32) {
       int w, sh;
@@ -463,13 +541,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         qv[r][c] = r < p.rows ? x : 0.f;
       }
     }
-    float qc[R][4];  // q * 2^-(b class) of this lane's Key channels
+    if constexpr (R == 1) {  // q of every channel for the window blocks' dot products
+      if (p.nwb > 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qbuf[4 * Lq + c] = qv[0][c];
+      }
+    }
+    float qc[R][4];  // q * 2^-(b class) of this lane's Key channels (exact: power of two)
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) qc[r][c] = qv[r][c] * clsL;
     float m_run = -INFINITY, l_run = 0.f;  // row my_r (lazy reference max, log2 units)
-    double cs = 0.0;
+    if (p.want_cs) csm[lane] = 0.0;
     int accv[NM][4];
 #pragma unroll
     for (int i = 0; i < NM; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0;
@@ -667,12 +751,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             x[c] = qc[r][c] * sc[c];
             mx = fmaxf(mx, fabsf(x[c]));
             if constexpr (K3) {
-              xh[c] = qv[r][c] * clsH * sc[c];  // 4 q s 2^-class_hi
+              xh[c] = qc[r][c] * clsHL * sc[c];  // 4 q s 2^-class_hi
               mx = fmaxf(mx, fabsf(xh[c]));
             }
-            bt = fmaf(qv[r][c], mn[c], bt);
+            bt = fmaf(qc[r][c], mn[c], bt);  // * 2^(b class) below
           }
-          if (qdup) bt = 0.f;
+          bt = qdup ? 0.f : bt * invL;  // sum_c q_c m_c of this lane (undo the class factor)
           // sigma = 2^(29 - floor(log2 max|x|)): max|x sigma| in [2^29, 2^30)
           const uint32_t mxu = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
           const int e = (int)((mxu >> 23) & 0xffu);
@@ -689,10 +773,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             store_digits(kbs + 8 * 4 * 2 * NK + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL, 4 * 2 * NK, uu);
             if (r == 0) {  // narrow-slot correction table (one query row: the host routes R = 1)
               float4 y;
-              y.x = qv[0][0] * (wide_scale(sc[0]) - sc[0]);
-              y.y = qv[0][1] * (wide_scale(sc[1]) - sc[1]);
-              y.z = qv[0][2] * (wide_scale(sc[2]) - sc[2]);
-              y.w = qv[0][3] * (wide_scale(sc[3]) - sc[3]);
+              y.x = qc[0][0] * invL * (wide_scale(sc[0]) - sc[0]);
+              y.y = qc[0][1] * invL * (wide_scale(sc[1]) - sc[1]);
+              y.z = qc[0][2] * invL * (wide_scale(sc[2]) - sc[2]);
+              y.w = qc[0][3] * invL * (wide_scale(sc[3]) - sc[3]);
               *reinterpret_cast<float4*>(ytab + 4 * lane) = y;
             }
           }
@@ -811,7 +895,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             lb[u2] = fmaf(pb, fac[2 * u2 + 1], betaL) + corr[2 * u2 + 1];
           }
         }
-        if (p.want_cs && row_ok && (t & 1) == 0) cs += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);
+        if (p.want_cs && row_ok && (t & 1) == 0) csm[lane] += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);
 
         // ---- online softmax (row my_r) -----------------------------------------------------
         float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
@@ -858,10 +942,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     if constexpr (R == 1) {
       const int wb_lo = max(lo, p.Gf) - p.Gf, wb_hi = min(hi, p.Gf + p.nwb) - p.Gf;
       if (wb_lo < wb_hi) {
-        // q of every channel for the lane = token dot products
-#pragma unroll
-        for (int c = 0; c < 4; ++c) qbuf[4 * Lq + c] = qv[0][c];
-        __syncwarp();
+        __syncwarp();  // qbuf (filled at the segment start) visible
       }
       for (int wb = wb_lo; wb < wb_hi; ++wb) {
         const int64_t j0 = p.P + 32 * (int64_t)wb;
@@ -908,7 +989,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             }
           }
           const float scn = acc * p.inv;
-          if (p.want_cs) cs += (double)scn;
+          if (p.want_cs) csm[lane] += (double)scn;
           sl = scn * kLog2e;
         }
         float tmax = sl;
@@ -1066,7 +1147,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           for (int r = 0; r < R; ++r) {
             if (r < p.rows) {
               const float sc = x[i][r] * p.inv;
-              if (p.want_cs && lane == 0) cs += (double)sc;
+              if (p.want_cs && lane == 0) csm[0] += (double)sc;
               const float ls = sc * kLog2e;
               const float m_new = fmaxf(m_all[r], ls);
               const float alpha = exp2f(m_all[r] - m_new);
@@ -1081,77 +1162,44 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       }
     }
 
-    // ---- segment epilogue: this warp's partial for (b, kv-head) -> slot wg + bh ----------
+    // ---- segment epilogue ----------------------------------------------------------------
+    // A (b, kv-head) inside this warp's range is normalized and written directly; otherwise
+    // the partial goes to slot wg + bh and the last of its warps to arrive merges them.
     const int64_t slot = (int64_t)wg + bh;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (r < p.rows) {
-        const size_t pi = (size_t)slot * p.rows + r;
-        if constexpr (LC == 4) {
-          *reinterpret_cast<float4*>(p.part_acc + pi * D + lane * LC) =
-              make_float4(acct[r][0], acct[r][1], acct[r][2], acct[r][3]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < LC; ++c) p.part_acc[pi * D + lane * LC + c] = acct[r][c];
-        }
-        if (lane == 0) p.part_ml[pi] = make_float2(m_all[r] == -INFINITY ? -INFINITY : m_all[r] * kLn2, l_all[r]);
-      }
-    }
     if (p.want_cs) {
-      for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-      if (lane == 0) p.part_cs[slot] = cs;
+      double csl = csm[lane];
+      for (int o = 16; o > 0; o >>= 1) csl += __shfl_xor_sync(0xffffffffu, csl, o);
+      if (lane == 0) p.part_cs[slot] = csl;
+    }
+    if (lo == 0 && hi == p.U) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r < p.rows) {
+          const int gi = r / p.tq, qi = r % p.tq;
+          float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
+          const float il = 1.0f / l_all[r];
+#pragma unroll
+          for (int c = 0; c < LC; ++c) o[c] = acct[r][c] * il;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r < p.rows) {
+          const size_t pi = (size_t)slot * p.rows + r;
+          if constexpr (LC == 4) {
+            *reinterpret_cast<float4*>(p.part_acc + pi * D + lane * LC) =
+                make_float4(acct[r][0], acct[r][1], acct[r][2], acct[r][3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < LC; ++c) p.part_acc[pi * D + lane * LC + c] = acct[r][c];
+          }
+          if (lane == 0) p.part_ml[pi] = make_float2(m_all[r] == -INFINITY ? -INFINITY : m_all[r] * kLn2, l_all[r]);
+        }
+      }
+      if (arrive_last(p, bh, lane)) merge_bh<D>(p, bh, lane);
     }
     __syncwarp();  // s_acc is rewritten by the next segment
-  }
-}
-
-// Combine the stream-K partials of each (b, kv-head): the warps whose unit ranges meet
-// [bh U, (bh+1) U), slot w + bh, merged in warp order (deterministic). One warp per
-// (b, kv-head, row), lanes over channels. (A programmatic-dependent launch that overlaps
-// this kernel with the attention kernel's tail measured bimodal step times; not used.)
-constexpr int kCombineWarps = 4;
-__global__ void __launch_bounds__(kCombineWarps * 32) attend_combine_sk_kernel(
-    const float2* __restrict__ part_ml, const float* __restrict__ part_acc, int64_t Nc, int W, int64_t cost_bh, int Qc,
-    int Gf, int ntail, int R, int BH, int H, int Hq, int tq, int D, float* __restrict__ out) {
-  const int item = blockIdx.x * kCombineWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (item >= BH * R) return;
-  const int bh = item / R, r = item % R;
-  const int b = bh / H, h = bh % H, G = Hq / H;
-  const int gi = r / tq, qi = r % tq;
-  const int hq = h * G + gi;
-  // warp owning a unit that starts at cost sx: floor(((sx + 1) W - 1) / Nc)
-  const int64_t s0 = (int64_t)bh * cost_bh;
-  const int64_t s1 = s0 + (ntail > 0 ? (int64_t)Qc * Gf + ntail - 1 : (int64_t)Qc * (Gf - 1));
-  const int w0 = (int)(((s0 + 1) * W - 1) / Nc);
-  const int w1 = (int)(((s1 + 1) * W - 1) / Nc);
-  float M = -INFINITY;
-  for (int w = w0 + lane; w <= w1; w += 32) M = fmaxf(M, part_ml[((size_t)w + bh) * R + r].x);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float L = 0.f;
-  for (int w = w0 + lane; w <= w1; w += 32) {
-    const float2 ml = part_ml[((size_t)w + bh) * R + r];
-    if (ml.x != -INFINITY) L += ml.y * expf(ml.x - M);
-  }
-  // fixed-order sum over lanes (deterministic: same shuffle tree every call)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-  const float invL = 1.0f / L;
-  for (int d0 = lane * 4; d0 < D; d0 += 128) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int w = w0; w <= w1; ++w) {
-      const size_t pi = ((size_t)w + bh) * R + r;
-      const float2 ml = part_ml[pi];
-      if (ml.x == -INFINITY) continue;
-      const float f = expf(ml.x - M);
-      const float4 x = *reinterpret_cast<const float4*>(part_acc + pi * D + d0);
-      a.x += x.x * f;
-      a.y += x.y * f;
-      a.z += x.z * f;
-      a.w += x.w * f;
-    }
-    *reinterpret_cast<float4*>(out + (((size_t)b * Hq + hq) * tq + qi) * D + d0) =
-        make_float4(a.x * invL, a.y * invL, a.z * invL, a.w * invL);
   }
 }
 
@@ -1196,6 +1244,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.part_ml = ws.ml(st, slots * p.rows);
   p.part_acc = ws.acc(st, slots * p.rows * D);
   p.part_cs = ws.cs(st, slots + 1);
+  p.cnt = ws.get<unsigned long long>(st, (size_t)BH);
   if (p.fused) p.flags = ws.get<unsigned long long>(st, (size_t)BH);
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
   kern<<<(p.W + kMmaWarps - 1) / kMmaWarps, kMmaWarps * 32, smem, st>>>(p);
@@ -1284,12 +1333,13 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
+  p.out = out;
+  p.epoch = next_epoch();
   if (da) {  // fused append: only if the aged Value token is outside the fast groups
     if (da->v_age && da->v_j < p.P) return false;
     if (T <= p.P) return false;  // (cannot happen after an append: the new Key is in the window)
     p.fused = 1;
     p.da = *da;
-    p.epoch = next_epoch();
   }
   p.flush_blocks = kFlushBlocks;
   if (const char* e = getenv("KVMIX_TEST_FLUSH_BLOCKS")) p.flush_blocks = std::max(1, std::min(kFlushBlocks, atoi(e)));
@@ -1305,12 +1355,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
 #undef KVB_DISPATCH_D
   if (W == 0) return false;
   after_launch("attend_mma_kernel");
-  {
-    const int items = BH * rows;
-    attend_combine_sk_kernel<<<(items + kCombineWarps - 1) / kCombineWarps, kCombineWarps * 32, 0, st>>>(
-        p.part_ml, p.part_acc, p.Nc, p.W, p.cost_bh, p.Qc, p.Gf, p.U - p.Gf, rows, BH, c->H, Hq, tq, D, out);
-  }
-  after_launch("attend_combine_sk_kernel");
+
   if (checksum) {
     const size_t nslot = (size_t)p.W + BH;
     checksum_kernel<<<1, 32, 0, st>>>(p.part_cs, nslot, p.part_cs + nslot);
