@@ -348,7 +348,7 @@ def run_b200(args, rank, world, local_rank):
                    "timed_step": "per layer: append(1 token) + attend = kvmix_append_attend"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "attend_mma_kernel (IMMA) + attend_combine_sk_kernel, one pair per layer",
+                     "kernel": "attend_mma_kernel (IMMA; append in its prologue, split partials merged in-kernel), one launch per layer",
                      "traffic_unit": "DRAM bytes per step (profiles/ncu_traffic.json)",
                      "algorithmic_bytes_per_step": tot_bytes, "attend_ms_per_step": tot_ms,
                      "attend_share_of_step": tot_ms / ms_per_step},
