@@ -557,11 +557,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     int accv[NM][4];
 #pragma unroll
     for (int i = 0; i < NM; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0;
-    float bias[R][CGMAX];
+    float bias[R];  // sum_j p_j m_jc of this lane's channel group cq = lane / 8 and token quads
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < CGMAX; ++c) bias[r][c] = 0.f;
+    for (int r = 0; r < R; ++r) bias[r] = 0.f;
     int e_cur = 0;      // Value fixed-point exponent
     int nacc = 0;       // blocks in the int32 Value accumulators
     bool dirty = false;  // s_acc / accumulators / bias hold something
@@ -595,39 +593,24 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 
     // Value k-step of one 32-token block: lane (g, t) owns token j = g + 8t (p of it for every
     // row in pr); fixed-point exponent / fold bookkeeping, B digits, 8 IMMA.
-    auto value_block = [&](const uint32_t* vt2, const uint32_t* vm2, const float (&pr)[R], float alpha, bool tok_ok) {
-      const int j = g + 8 * t;
-      float sv[CGMAX], mv[CGMAX];
-      {
-        const uint32_t* vmt = vm2 + (size_t)j * CG;
-        if constexpr (GS != 0 && D / (GS ? GS : 1) == 4) {
-          const uint4 q4 = *reinterpret_cast<const uint4*>(vmt);
-          const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
+    auto value_block = [&](const uint32_t* vt2, const uint32_t* vm2, const float (&pr)[R], float alpha, int nvalid) {
+      // lane (cq, tq) = (lane / 8, lane % 8) handles channel group cq of tokens 4tq .. 4tq+3
+      const int cq = lane >> 3, tq = lane & 7;
+      const bool cg_ok = cq < CG;
+      float pq[R][4], sv[4], mv[4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float2 f = meta_pair(w4[c]);
-            sv[c] = f.x;
-            mv[c] = f.y;
-          }
-        } else {
+      for (int i = 0; i < 4; ++i) {
+        const int jj = 4 * tq + i;  // owned (p) by lane 4 (jj % 8) + jj / 8
 #pragma unroll
-          for (int c = 0; c < CGMAX; ++c) {
-            const float2 f = meta_pair(c < CG ? vmt[c] : 0u);
-            sv[c] = f.x;
-            mv[c] = f.y;
-          }
-        }
+        for (int r = 0; r < R; ++r) pq[r][i] = __shfl_sync(0xffffffffu, pr[r], 4 * (jj & 7) + (jj >> 3));
+        const uint32_t w = (cg_ok && jj < nvalid) ? vm2[(size_t)jj * CG + cq] : 0u;  // rows past nvalid never written
+        const float2 f = meta_pair(w);
+        sv[i] = f.x;
+        mv[i] = f.y;
       }
-      if (!tok_ok) {  // window block past the aged Values: rows never written
-#pragma unroll
-        for (int c = 0; c < CGMAX; ++c) sv[c] = mv[c] = 0.f;
-      }
-      // fixed-point exponent: max scale of the block * 2^E < 2^30 (p <= 1)
-      float smax = sv[0];
-#pragma unroll
-      for (int c = 1; c < CGMAX; ++c) smax = fmaxf(smax, sv[c]);
+      // fixed-point exponent: max scale of the block * 2^E < 2^30 (p <= 2^kLazy)
+      const float smax = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
       const uint32_t smu = __reduce_max_sync(0xffffffffu, __float_as_uint(smax));
-      // (p <= 2^kLazy): y = p s 2^E < 2^30 for E <= e_blk
       const int e_blk = min(156 - kLazy - (int)((smu >> 23) & 0xffu), 100);
       if (!dirty) {
         e_cur = e_blk - kEHead;
@@ -638,9 +621,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           if (moved) {
             const float ax = __shfl_xor_sync(0xffffffffu, alpha, 2);
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-#pragma unroll
-              for (int c = 0; c < CGMAX; ++c) bias[r][c] *= (r == my_r) ? alpha : ax;
+            for (int r = 0; r < R; ++r) bias[r] *= (r == my_r) ? alpha : ax;
           }
           e_cur = e_blk - kEHead;
         }
@@ -649,26 +630,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int c = 0; c < CGMAX; ++c) bias[r][c] = fmaf(pr[r], mv[c], bias[r][c]);
-      // B digits of y = p s 2^E (u8, four columns per row) -> vbs[c][4r + n][pos(j)]
-      {
+        for (int i = 0; i < 4; ++i) bias[r] = fmaf(pq[r][i], mv[i], bias[r]);
+      // B digits of y = p s 2^E (u8, four columns per row): one word per (digit, row) holds the
+      // quad's four tokens -> vbs[cq][4r + n][pos(4tq) .. +3]
+      if (cg_ok) {
         const float pe = pow2i(e_cur);
-        float ppe[R];
+        const int pos = (tq & 3) * 8 + (tq >> 2) * 4;
 #pragma unroll
-        for (int r = 0; r < R; ++r) ppe[r] = pr[r] * pe;
-        const int pos = ((g >> 2) + 2 * (t & 1)) * 8 + (t >> 1) * 4 + (g & 3);
+        for (int r = 0; r < R; ++r) {
+          uint32_t uu[4];
 #pragma unroll
-        for (int c = 0; c < CGMAX; ++c) {
-          if (GS == 0 && c >= CG) break;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const uint32_t v = (uint32_t)__float2int_rn(ppe[r] * sv[c]);
-            uint8_t* dst = vbs + c * 256 + (4 * r) * 32 + pos;
-            dst[0] = (uint8_t)v;
-            dst[32] = (uint8_t)(v >> 8);
-            dst[64] = (uint8_t)(v >> 16);
-            dst[96] = (uint8_t)(v >> 24);
-          }
+          for (int i = 0; i < 4; ++i) uu[i] = (uint32_t)__float2int_rn(pq[r][i] * pe * sv[i]);
+          store_digits(reinterpret_cast<uint32_t*>(vbs + cq * 256 + (4 * r) * 32 + pos), 8, uu);
         }
       }
       __syncwarp();
@@ -913,8 +886,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         l_run = l_run * alpha + ((pa[0] + pb[0]) + (pa[1] + pb[1]));
         m_run = m_new;
 
-        // ---- Value block: lane (g, t) owns token j = g + 8t of the 32 ---------------------
-        const int j = g + 8 * t;
+        // ---- Value block: lane (g, t) owns token g + 8t of the 32 -------------------------
         float pr[R];  // p of token j for every row
         {
           const float mine = (t & 1) ? ((t >> 1) ? pb[1] : pb[0]) : ((t >> 1) ? pa[1] : pa[0]);
@@ -923,7 +895,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
           for (int r = 0; r < R; ++r) pr[r] = (r == my_r) ? mine : recv;
         }
-        value_block(vt2, vm2, pr, alpha, true);
+        value_block(vt2, vm2, pr, alpha, 32);
       }
       // refill this stage S groups ahead
       issue_next(s);
@@ -1011,21 +983,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         const uint32_t* vt2 = reinterpret_cast<const uint32_t*>(rec + p.kt_bytes) + (size_t)(2 * bi) * tile_words(D, VB);
         const uint32_t* vm2 = reinterpret_cast<const uint32_t*>(rec + p.kt_bytes + p.vt_bytes) + (size_t)(32 * bi) * CG;
         const float pr[R] = {pj};
-        value_block(vt2, vm2, pr, alpha, valid);
+        value_block(vt2, vm2, pr, alpha, (int)(p.Pw - j0 < 32 ? p.Pw - j0 : 32));
       }
     }
 
     // ---- end of the fast region: fold accumulators, gather the softmax state ------------
     if (dirty) flush(1.0f);
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < CGMAX; ++c) {
-        float x = bias[r][c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        bias[r][c] = x;
-      }
+    for (int r = 0; r < R; ++r) {  // channel group cq's total over its 8 token-quad lanes
+      bias[r] += __shfl_xor_sync(0xffffffffu, bias[r], 1);
+      bias[r] += __shfl_xor_sync(0xffffffffu, bias[r], 2);
+      bias[r] += __shfl_xor_sync(0xffffffffu, bias[r], 4);
+    }
     float m_all[R], l_all[R];
     {
       float lr = l_run;
@@ -1046,10 +1015,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
         const int d = lane * LC + c;
-        float bsel = bias[r][0];
-#pragma unroll
-        for (int cc = 1; cc < CGMAX; ++cc)
-          if (cc == d / gs) bsel = bias[r][cc];
+        const float bsel = __shfl_sync(0xffffffffu, bias[r], 8 * (d / gs));  // group d / gs: lanes 8 cg ..
         acct[r][c] = s_acc[warp][r][d] + bsel;
       }
 
