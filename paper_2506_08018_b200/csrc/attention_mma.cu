@@ -215,6 +215,7 @@ struct MmaParams {
   const void* q;
   int q16, tail16;
   int H, Hq, tq, rows, gs, cg;
+  int row0;  // first query row of this pass (rows > 2 run as passes of <= 2 rows)
   int64_t T, P;  // total tokens; fast-path limit (multiple of gs)
   int64_t Pw;    // window blocks cover tokens [P, Pw) (Keys fp16 in the ring, Values packed)
   int nwb;       // window blocks per (b, kv-head)
@@ -344,7 +345,7 @@ __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane) {
 #pragma unroll
       for (int c = 0; c < LC; ++c) a[c] += __ldcg(&p.part_acc[pi * D + lane * LC + c]) * f;
     }
-    const int gi = r / p.tq, qi = r % p.tq;
+    const int gi = (p.row0 + r) / p.tq, qi = (p.row0 + r) % p.tq;
     float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
     const float il = 1.0f / L;
 #pragma unroll
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     float qv[R][4];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int rr = r < p.rows ? r : 0;
+      const int rr = p.row0 + (r < p.rows ? r : 0);
       const int gi = rr / p.tq, qi = rr % p.tq;
       const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + 4 * Lq;
 #pragma unroll
@@ -1028,7 +1029,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       float qt[R][LC];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int rr = r < p.rows ? r : 0;
+        const int rr = p.row0 + (r < p.rows ? r : 0);
         const int gi = rr / p.tq, qi = rr % p.tq;
         const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + d0;
 #pragma unroll
@@ -1141,7 +1142,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r < p.rows) {
-          const int gi = r / p.tq, qi = r % p.tq;
+          const int gi = (p.row0 + r) / p.tq, qi = (p.row0 + r) % p.tq;
           float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
           const float il = 1.0f / l_all[r];
 #pragma unroll
@@ -1220,7 +1221,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
 template <int D, int KB, int VB, int R>
 int dispatch_gs(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   if constexpr (KB == 3 && (D != 128 || R != 1)) {
-    return 0;  // 3-bit Keys with two rows: the residue columns spill; generic path
+    return 0;  // 3-bit Keys: one query row per pass (attend_mma never asks for two)
   } else {
     return p.gs == 32 ? launch<D, KB, VB, R, 32>(p, BH, ws, st) : launch<D, KB, VB, R, 0>(p, BH, ws, st);
   }
@@ -1244,13 +1245,16 @@ int dispatch_bits(MmaParams& p, int kb, int vb, int BH, Workspace& ws, cudaStrea
 bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
                 Workspace& ws, cudaStream_t st, const DecodeAppend* da) {
   const int rows = (Hq / c->H) * tq;
-  if (rows > 2) return false;
   const int kb = c->k.bits, vb = c->v.bits;
   if (vb == 3) return false;
   const int D = c->D, gs = c->cfg.group_size;
   if (gs % 32 != 0) return false;  // groups are processed in 32-token blocks
   if (D != 64 && D != 128) return false;
-  if (kb == 3 && (D != 128 || rows != 1)) return false;
+  if (kb == 3 && D != 128) return false;
+  // query rows per pass: 2 (the B operand holds two rows' four digits), 1 for 3-bit Keys
+  // (their narrow-slot table is per row); more rows (GQA G > 2, several query tokens) run
+  // as successive passes over the cache
+  const int per_pass = kb == 3 ? 1 : 2;
   const int BH = c->B * c->H;
   const int64_t T = c->total();
   MmaParams p{};
@@ -1262,31 +1266,11 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.H = c->H;
   p.Hq = Hq;
   p.tq = tq;
-  p.rows = rows;
   p.gs = gs;
   p.cg = c->cgroups();
   p.T = T;
   p.P = (std::min(c->k.quantized, c->v.quantized) / gs) * gs;
-  // window blocks: one query row, the Key window starting at P (Keys age in whole groups)
-  p.Pw = p.P;
-  p.nwb = 0;
-  if (rows == 1 && c->k.quantized == p.P && !getenv("KVMIX_PROF_NO_WINDOW")) {
-    p.Pw = std::min(T, c->v.quantized);
-    if (p.Pw > p.P) p.nwb = (int)((p.Pw - p.P + 31) / 32);
-    else p.Pw = p.P;
-  }
-  p.tail_unit = kTailUnit;
-  p.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
-  if (const char* e = getenv("KVMIX_TAIL_UNIT")) p.tail_unit = std::max(1, std::min(64, atoi(e)));
-  const int64_t U = p.P / gs + p.nwb + (T - p.Pw + p.tail_unit - 1) / p.tail_unit;
-  if ((int64_t)BH * U >= (int64_t)1 << 31) return false;
   p.Gf = (int)(p.P / gs);
-  p.U = (int)U;
-  p.N = BH * p.U;
-  p.Qc = kGroupCost;
-  if (const char* e = getenv("KVMIX_GROUP_COST")) p.Qc = std::max(1, std::min(64, atoi(e)));
-  p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
-  p.Nc = (int64_t)BH * p.cost_bh;
   p.kt_bytes = (uint32_t)((gs / 16) * c->k.tile_words * 4);
   p.vt_bytes = (uint32_t)((gs / 16) * c->v.tile_words * 4);
   p.vm_bytes = (uint32_t)(gs * p.cg * 4);
@@ -1300,35 +1284,71 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
   p.out = out;
-  p.epoch = next_epoch();
+  p.tail_unit = kTailUnit;
+  p.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
+  if (const char* e = getenv("KVMIX_TAIL_UNIT")) p.tail_unit = std::max(1, std::min(64, atoi(e)));
+  p.Qc = kGroupCost;
+  if (const char* e = getenv("KVMIX_GROUP_COST")) p.Qc = std::max(1, std::min(64, atoi(e)));
+  p.flush_blocks = kFlushBlocks;
+  if (const char* e = getenv("KVMIX_TEST_FLUSH_BLOCKS")) p.flush_blocks = std::max(1, std::min(kFlushBlocks, atoi(e)));
   if (da) {  // fused append: only if the aged Value token is outside the fast groups
     if (da->v_age && da->v_j < p.P) return false;
     if (T <= p.P) return false;  // (cannot happen after an append: the new Key is in the window)
-    p.fused = 1;
-    p.da = *da;
   }
-  p.flush_blocks = kFlushBlocks;
-  if (const char* e = getenv("KVMIX_TEST_FLUSH_BLOCKS")) p.flush_blocks = std::max(1, std::min(kFlushBlocks, atoi(e)));
-  const int R = rows <= 1 ? 1 : 2;
-  int W = 0;
-#define KVB_DISPATCH_D(DD)                                                  \
-  if (D == DD) {                                                            \
-    if (R == 1) W = dispatch_bits<DD, 1>(p, kb, vb, BH, ws, st);           \
-    else W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st);                  \
-  }
-  KVB_DISPATCH_D(64)
-  KVB_DISPATCH_D(128)
-#undef KVB_DISPATCH_D
-  if (W == 0) return false;
-  after_launch("attend_mma_kernel");
+  // unit lists of the passes: window blocks only with one query row
+  auto layout = [&](int nrows) {
+    p.Pw = p.P;
+    p.nwb = 0;
+    if (nrows == 1 && c->k.quantized == p.P && !getenv("KVMIX_PROF_NO_WINDOW")) {
+      p.Pw = std::min(T, c->v.quantized);
+      if (p.Pw > p.P) p.nwb = (int)((p.Pw - p.P + 31) / 32);
+      else p.Pw = p.P;
+    }
+    return (int64_t)p.Gf + p.nwb + (T - p.Pw + p.tail_unit - 1) / p.tail_unit;
+  };
+  for (int r0 = 0; r0 < rows; r0 += per_pass)
+    if ((int64_t)BH * layout(std::min(per_pass, rows - r0)) >= (int64_t)1 << 31) return false;
 
-  if (checksum) {
-    const size_t nslot = (size_t)p.W + BH;
-    checksum_kernel<<<1, 32, 0, st>>>(p.part_cs, nslot, p.part_cs + nslot);
-    after_launch("checksum_kernel");
-    check_cuda(cudaMemcpyAsync(checksum, p.part_cs + nslot, 8, cudaMemcpyDeviceToHost, st), "memcpy");
-    check_cuda(cudaStreamSynchronize(st), "sync");
+  double cs_total = 0.0;
+  for (int r0 = 0; r0 < rows; r0 += per_pass) {
+    const int nrows = std::min(per_pass, rows - r0);
+    p.row0 = r0;
+    p.rows = nrows;
+    p.U = (int)layout(nrows);
+    p.N = BH * p.U;
+    p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
+    p.Nc = (int64_t)BH * p.cost_bh;
+    p.epoch = next_epoch();
+    p.fused = 0;
+    if (da && r0 == 0) {  // the first pass runs the append; later passes follow in stream order
+      p.fused = 1;
+      p.da = *da;
+    }
+    int W = 0;
+#define KVB_DISPATCH_D(DD)                                                  \
+    if (D == DD) {                                                          \
+      if (nrows == 1) W = dispatch_bits<DD, 1>(p, kb, vb, BH, ws, st);     \
+      else W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st);                \
+    }
+    KVB_DISPATCH_D(64)
+    KVB_DISPATCH_D(128)
+#undef KVB_DISPATCH_D
+    if (W == 0) {
+      if (r0 == 0) return false;  // nothing launched yet: the caller takes the generic path
+      throw Error(KVMIX_RUNTIME_ERROR, "attend: tensor-core pass unavailable after the first");
+    }
+    after_launch("attend_mma_kernel");
+    if (checksum) {
+      const size_t nslot = (size_t)p.W + BH;
+      checksum_kernel<<<1, 32, 0, st>>>(p.part_cs, nslot, p.part_cs + nslot);
+      after_launch("checksum_kernel");
+      double part = 0.0;
+      check_cuda(cudaMemcpyAsync(&part, p.part_cs + nslot, 8, cudaMemcpyDeviceToHost, st), "memcpy");
+      check_cuda(cudaStreamSynchronize(st), "sync");
+      cs_total += part;
+    }
   }
+  if (checksum) *checksum = cs_total;
   return true;
 }
 
