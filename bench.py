@@ -41,6 +41,7 @@ CONFIGS = {
     "layer-4k": (1, 1, 32, 32, 128, 4096, 0),                  # configs[0] shape
     "mistral-7b-32k": (32, 8, 8, 32, 128, 32768, 6),          # configs[2]
 }
+CONFIG_INDEX = {"llama2-7b-8k": "configs[1]", "layer-4k": "configs[0]", "mistral-7b-32k": "configs[2]"}
 
 
 def parse():
@@ -344,10 +345,11 @@ def run_b200(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "u8 codes x s8/u8 fixed-point digits -> s32 (IMMA), f32 softmax (KV bit-packed 2/3/4-bit)",
         "data": "synthetic (randn on the binary16 grid, on device)",
-        "config": {"workload": f"configs[1] {args.config}: {L} layers, B{B}, Hq{Hq}/Hkv{H}, D{D}, ~{ctx} ctx, "
+        "config": {"workload": f"{CONFIG_INDEX[args.config]} {args.config}: {L} layers, B{B}, Hq{Hq}/Hkv{H}, D{D}, ~{ctx} ctx, "
                                f"KVmix tiers (0-{high - 1} K3/V4 r0.2, rest K2/V2 r0.1), gs32, fp16 window",
                    "global_batch": B * world, "seq_len": ctx, "parallelism": f"dp{world} (batch x kv-head shards)",
-                   "l2": "per-step cache bytes (>14 GB) >> 126 MB L2; no flush needed",
+                   "l2": (f"per-step cache bytes ({tot_bytes / 1e9:.2f} GB) >> 126 MB L2; no flush needed"
+                          if tot_bytes > 1e9 else f"per-step cache bytes {tot_bytes / 1e6:.0f} MB: partly L2-resident"),
                    "timed_step": "per layer: append(1 token) + attend = kvmix_append_attend"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
