@@ -364,10 +364,30 @@ struct WarpLayout {
   static constexpr int kK = KB == 3 ? 2 * kKB + 2 * D * 4 : kKB;
   static constexpr int kV = (D / 32) * 8 * 32;
   static constexpr int kQ = D * 4 + 32 * 8;  // q of all channels (window blocks), checksum slots
-  __host__ __device__ static size_t bytes(int stages, uint32_t stage_bytes) {
+  __host__ __device__ static constexpr size_t bytes(int stages, uint32_t stage_bytes) {
     const size_t n = (size_t)stages * stage_bytes + kK + kV + kQ + (size_t)stages * 8;
     return (n + 127) / 128 * 128;  // keep every warp's ring 128-byte aligned
   }
+};
+
+// Compile-time stage geometry for a compile-time group size: record = K tiles | V tiles |
+// V meta | K meta, ring depth chosen for 4 CTAs per SM (same rule as launch()).
+template <int D, int KB, int VB, int R, int GS>
+struct StageGeo {
+  static constexpr uint32_t kKT = GS ? (uint32_t)((GS / 16) * tile_words(D, KB) * 4) : 0;
+  static constexpr uint32_t kVT = GS ? (uint32_t)((GS / 16) * tile_words(D, VB) * 4) : 0;
+  static constexpr uint32_t kVM = GS ? (uint32_t)(GS * ((D + (GS ? GS : 1) - 1) / (GS ? GS : 1)) * 4) : 0;
+  static constexpr uint32_t kKM = (uint32_t)(D * 4);
+  static constexpr uint32_t kStage = kKT + kVT + kVM + kKM;
+  static constexpr long kStatic = (long)kMmaWarps * R * D * 4;  // s_acc
+  static constexpr int stages_for(int occ) {
+    return (int)(((227L * 1024 / occ - 1024 - kStatic) / kMmaWarps - (long)WarpLayout<D, KB, R>::bytes(0, 0) - 32 - 128) /
+                 (long)(kStage ? kStage : 1));
+  }
+  static constexpr int kStages = GS == 0 ? 0
+                                 : stages_for(4) >= 2 ? (stages_for(4) < 4 ? stages_for(4) : 4)
+                                 : stages_for(3) >= 2 ? (stages_for(3) < 4 ? stages_for(3) : 4)
+                                                      : 2;
 };
 
 // GS: 0 = runtime group size (a multiple of 32), else compile-time (32 is the KVmix default).
@@ -403,7 +423,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   const int gs = GS ? GS : p.gs;
   const int CG = GS ? D / GS : p.cg;
   const int NBLK = gs / 32;  // 32-token blocks per group
-  const int S = p.stages;
+  using SG = StageGeo<D, KB, VB, R, GS>;
+  const int S = GS ? SG::kStages : p.stages;
+  const uint32_t SB = GS ? SG::kStage : p.stage_bytes;            // bytes per group record
+  const uint32_t KTB = GS ? SG::kKT : p.kt_bytes, VTB = GS ? SG::kVT : p.vt_bytes;
+  const uint32_t VMB = GS ? SG::kVM : p.vm_bytes;
   const int64_t c_beg = (int64_t)wg * p.Nc / p.W, c_end = (int64_t)(wg + 1) * p.Nc / p.W;
   const int u_beg = unit_at_cost(p, c_beg), u_end = unit_at_cost(p, c_end);
   if (u_beg >= u_end) {  // no unit starts in this cost range: neutral partial
@@ -417,9 +441,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     return;
   }
 
-  uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, p.stage_bytes);
+  uint8_t* wbase = dsm + (size_t)warp * WL::bytes(S, SB);
   uint8_t* ring = wbase;
-  uint8_t* kstage = ring + (size_t)S * p.stage_bytes;
+  uint8_t* kstage = ring + (size_t)S * SB;
   uint32_t* kbs = reinterpret_cast<uint32_t*>(kstage);
   float* ytab = reinterpret_cast<float*>(kstage + 2 * WL::kKB);
   uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + 2 * WL::kKB + D * 4);
@@ -467,9 +491,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   auto issue_next = [&](int s) {
     if (left_all > 0) {
       if (lane == 0) {
-        mbar_arrive_expect_tx(&bars[s], p.stage_bytes);
-        bulk_g2s(ring + (size_t)s * p.stage_bytes,
-                 reinterpret_cast<const uint8_t*>(p.k.tiles) + (size_t)rec_i * p.stage_bytes, p.stage_bytes, &bars[s],
+        mbar_arrive_expect_tx(&bars[s], SB);
+        bulk_g2s(ring + (size_t)s * SB, reinterpret_cast<const uint8_t*>(p.k.tiles) + (size_t)rec_i * SB, SB, &bars[s],
                  evict_first_policy());
       }
       --left_all;
@@ -685,11 +708,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     const int g_stop = min(hi, p.Gf);
     for (int grp = lo; grp < g_stop; ++grp) {
       mbar_wait(&bars[s], phase);
-      const uint8_t* st = ring + (size_t)s * p.stage_bytes;
+      const uint8_t* st = ring + (size_t)s * SB;
       const uint32_t* kt = reinterpret_cast<const uint32_t*>(st);
-      const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + p.kt_bytes);
-      const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes);
-      const uint32_t* km = reinterpret_cast<const uint32_t*>(st + p.kt_bytes + p.vt_bytes + p.vm_bytes);
+      const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + KTB);
+      const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + KTB + VTB);
+      const uint32_t* km = reinterpret_cast<const uint32_t*>(st + KTB + VTB + VMB);
 
       // ---- Key group: B operand ---------------------------------------------------------
       // Fixed-point B = round(q s 2^-(b class) sigma) in four balanced s8 digits; 3-bit Keys
@@ -980,9 +1003,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         l_run = l_run * alpha + quad;
         m_run = m_new;
         const int gi = (int)(j0 / gs), bi = (int)((j0 - (int64_t)gi * gs) / 32);
-        const uint8_t* rec = reinterpret_cast<const uint8_t*>(p.k.tiles) + ((size_t)bh * p.Grec + gi) * p.stage_bytes;
-        const uint32_t* vt2 = reinterpret_cast<const uint32_t*>(rec + p.kt_bytes) + (size_t)(2 * bi) * tile_words(D, VB);
-        const uint32_t* vm2 = reinterpret_cast<const uint32_t*>(rec + p.kt_bytes + p.vt_bytes) + (size_t)(32 * bi) * CG;
+        const uint8_t* rec = reinterpret_cast<const uint8_t*>(p.k.tiles) + ((size_t)bh * p.Grec + gi) * SB;
+        const uint32_t* vt2 = reinterpret_cast<const uint32_t*>(rec + KTB) + (size_t)(2 * bi) * tile_words(D, VB);
+        const uint32_t* vm2 = reinterpret_cast<const uint32_t*>(rec + KTB + VTB) + (size_t)(32 * bi) * CG;
         const float pr[R] = {pj};
         value_block(vt2, vm2, pr, alpha, (int)(p.Pw - j0 < 32 ? p.Pw - j0 : 32));
       }
@@ -1192,6 +1215,12 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
       stages = (int)std::min<long>(4, s_fit);
       break;
     }
+  }
+  if constexpr (GS != 0) {
+    using SG = StageGeo<D, KB, VB, R, GS>;
+    static_assert(SG::kStages >= 2, "stage geometry");
+    if (p.stage_bytes != SG::kStage) throw Error(KVMIX_RUNTIME_ERROR, "attend: record geometry mismatch");
+    stages = SG::kStages;
   }
   p.stages = stages;
   const size_t smem = (size_t)kMmaWarps * WL::bytes(p.stages, p.stage_bytes);

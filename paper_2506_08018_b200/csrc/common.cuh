@@ -155,9 +155,9 @@ __host__ __device__ inline TileCoord value_coord(int i, int d) {
 }
 
 // words per lane of one b-bit plane
-__host__ __device__ inline int plane_wpl(int D, int b) { return D * b / 64; }
+__host__ __device__ constexpr int plane_wpl(int D, int b) { return D * b / 64; }
 // total words of one tile at `bits` (3 -> 2-bit plane + 1-bit plane)
-__host__ __device__ inline int tile_words(int D, int bits) {
+__host__ __device__ constexpr int tile_words(int D, int bits) {
   return bits == 3 ? 32 * (plane_wpl(D, 2) + plane_wpl(D, 1)) : 32 * plane_wpl(D, bits);
 }
 // word offset of (lane, w) inside a plane with `wpl` words per lane (chunks of <=4 words
