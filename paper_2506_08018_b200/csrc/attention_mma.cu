@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       // planes accumulate into the same int32 scores) and the narrow-slot table
       // ytab[d] = q_d (wide_scale(s_d) - s_d) for the Mixed3 correction.
       float betaL;       // sum_d q_d m_d of row my_r, scaled to log2 units
-      float wsc0, wsc1;  // weights of this lane's two score columns (log2 units)
+      float wsc0;        // weight of this lane's score column pair (log2 units)
       uint32_t kb[NK][2], kbh[K3 ? NK : 1][2];
       int nmod = 0, omod = 0;  // 3-bit Keys: segment length / group offset mod 11
       {
@@ -813,7 +813,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             bb = beta[r];
           }
         wsc0 = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
-        wsc1 = wsc0 * 256.f;
         betaL = bb * p.inv * kLog2e;
       }
 
@@ -884,8 +883,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           }
 #pragma unroll
           for (int u2 = 0; u2 < 2; ++u2) {
-            float pa = fmaf((float)dk[u2][1], wsc1, (float)dk[u2][0] * wsc0);
-            float pb = fmaf((float)dk[u2][3], wsc1, (float)dk[u2][2] * wsc0);
+            // digits n0, n0+1 of this lane's columns: dk0 + 256 dk1 fits int32 (|dk| < 2^23)
+            float pa = (float)(dk[u2][0] + (dk[u2][1] << 8)) * wsc0;
+            float pb = (float)(dk[u2][2] + (dk[u2][3] << 8)) * wsc0;
             pa += __shfl_xor_sync(0xffffffffu, pa, 1);
             pb += __shfl_xor_sync(0xffffffffu, pb, 1);
             la[u2] = fmaf(pa, fac[2 * u2], betaL) + corr[2 * u2];
