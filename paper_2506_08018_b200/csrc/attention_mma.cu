@@ -300,8 +300,16 @@ __device__ __forceinline__ void bh_warps(const MmaParams& p, int bh, int& w0, in
 
 // Publish this warp's partial of bh; returns true for the last of the bh's warps to arrive
 // (the counter word carries the call's tag, so it needs no clearing between calls).
+__device__ __forceinline__ unsigned long long cas_acq_rel(unsigned long long* a, unsigned long long cmp,
+                                                          unsigned long long val) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;\n" : "=l"(old) : "l"(a), "l"(cmp), "l"(val) : "memory");
+  return old;
+}
+
+// (the warp barrier orders every lane's partial before lane 0's release; the acquiring lane
+// 0 of the last arriver passes the order on to its lanes through the next warp barrier)
 __device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane) {
-  __threadfence();
   __syncwarp();
   int last = 0;
   if (lane == 0) {
@@ -314,12 +322,12 @@ __device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane
     do {
       assumed = old;
       ct = (assumed >> 32) == tag ? (unsigned int)assumed : 0u;
-      old = atomicCAS(cw, assumed, (tag << 32) | (ct + 1u));
+      old = cas_acq_rel(cw, assumed, (tag << 32) | (ct + 1u));
     } while (old != assumed);
     last = (int)(ct + 1u) == w1 - w0 + 1;
   }
   last = __shfl_sync(0xffffffffu, last, 0);
-  if (last) __threadfence();
+  __syncwarp();
   return last != 0;
 }
 
