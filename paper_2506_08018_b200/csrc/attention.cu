@@ -6,8 +6,8 @@
 // dequantization inside the dot products (no K/V materialization), online softmax per
 // query row, split-K over the token axis with a deterministic combine kernel. It handles
 // every shape the device cache accepts (any G = Hq/H, any number of query rows, all bit
-// widths, tokens in the full-precision tail). The tensor-core fast path for full packed
-// tiles lives in attention_mma.cu and falls back to this code for the ragged end.
+// widths, tokens in the full-precision tail). The tensor-core path (attention_mma.cu)
+// serves D in {64, 128} with 2/3/4-bit Keys and 2/4-bit Values; this kernel the rest.
 #include <algorithm>
 #include <cmath>
 

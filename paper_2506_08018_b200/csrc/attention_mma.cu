@@ -25,18 +25,25 @@
 // HMMA m16n8k16 and IMMA m16n8k32 (profiles/probes/imma_rate.cu), so k32 integer MMAs
 // halve the tensor-pipe time as well as the unpack work of the fp16 formulation.
 //
-// Mixed3 (3-bit) Keys keep the fp16 HMMA formulation (HMMA layout): the reference's narrow
-// slots (stream index % 11 == 10) dequantize with scale*7/3; for channel d of a group the
-// narrow tokens are t = tau_d (mod 11), so the correction is 11 extra residue-class B
-// columns (hi/lo fp16 pairs) in the same MMAs.
+// Mixed3 (3-bit) Keys: the low 2 bits and the high bit are two IMMA planes whose B operands
+// share sigma (4 q s 2^-class_hi for the high plane), so both accumulate into one int32
+// score. The reference's narrow slots (stream index % 11 == 10) dequantize with scale*7/3:
+// for a token the narrow channels are d = d0 + 11k, corrected on the CUDA cores (one token
+// per lane, channel -> field table) with q_d (wide_scale(s_d) - s_d).
+//
+// Query rows: two per pass (one B column quadruple each); more rows (GQA with G > 2, several
+// query tokens) run as passes over the cache; 3-bit Keys one row per pass.
+//
+// The full-precision Key window whose Values are already packed runs as 32-token "window
+// blocks" (lane = token fp32 dot products from the ring, then the IMMA Value block).
 //
 // Memory pipeline: every unit of work (one Key group of gs tokens of one (b, kv-head)) is
 // one contiguous record (Key tiles | Value tiles | Value meta | Key meta) copied by one
 // elected lane with cp.async.bulk into a ring of S stages; the warp waits on the stage's
 // mbarrier (complete_tx), computes, and refills the stage S groups ahead.
 //
-// Work distribution (stream-K): a list of per-(b, kv-head) units (fast groups, then tail
-// units of the full-precision window) is cut into equal ranges over one resident wave of
+// Work distribution (stream-K): a list of per-(b, kv-head) units (fast groups, window
+// blocks, then single window tokens) is cut into equal ranges over one resident wave of
 // independent warps. A (b, kv-head) inside one warp's range is normalized and written by that
 // warp; one split across warps is merged (in warp order: deterministic) by the last of its
 // warps to publish a partial (tagged atomic counter) -- no separate combine launch.
@@ -219,8 +226,8 @@ struct MmaParams {
   int64_t T, P;  // total tokens; fast-path limit (multiple of gs)
   int64_t Pw;    // window blocks cover tokens [P, Pw) (Keys fp16 in the ring, Values packed)
   int nwb;       // window blocks per (b, kv-head)
-  // stream-K work list: per (b, kv-head) U = Gf fast groups + ceil((T - P) / kTailUnit)
-  // tail units, N = BH * U units in bh-major order; warp w of W takes [w N / W, (w+1) N / W)
+  // stream-K work list: per (b, kv-head) U = Gf fast groups + nwb window blocks +
+  // ceil((T - Pw) / tail_unit) window-token units, N = BH * U units in bh-major order
   int Gf, U, N;  // 32-bit: the host falls back to the generic path beyond 2^31 units
   // cost-weighted split: a group costs Qc, a window token 1; (b, kv-head) cost cost_bh =
   // Qc Gf + (U - Gf), total Nc = BH cost_bh; warp w owns the units starting in cost range
