@@ -69,56 +69,58 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   __syncthreads();
 
   const int cpw = codes_per_word(bits);
-  // one thread per channel run; a run's owned words are contiguous in `words`
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+  // every thread emits words: thread i -> channel d = i % D (a warp reads 32 consecutive
+  // channels of one token row: conflict-free), word j = i / D of that channel's run. A
+  // run's owned words are those whose FIRST code lies in it; trailing codes of the last
+  // one that belong to the next run are encoded straight from global memory.
+  const int nwr_max = (nt + cpw - 1) / cpw + 1;  // owned words per run are at most this
+  for (int i = threadIdx.x; i < D * nwr_max; i += blockDim.x) {
+    const int d = i % D, j = i / D;
     const size_t c = (size_t)bh * D + d;
     const size_t s0 = c * (size_t)T_ + t0;
     const size_t s1 = s0 + nt;
     const size_t w_begin = (s0 + cpw - 1) / cpw, w_end = (s1 + cpw - 1) / cpw;
-    // cache for out-of-run codes (next run): its channel/group meta
-    size_t cached_group = ~(size_t)0;
-    float o_scale = 0.f, o_min = 0.f;
-    for (size_t w = w_begin; w < w_end; ++w) {
-      uint32_t word = 0;
-      const size_t p0 = w * cpw;
-      for (int k = 0; k < cpw; ++k) {
-        const size_t p = p0 + k;
-        if (p >= n_total) break;
-        float xv, sc, mnv;
-        if (p < s1) {
-          const int tt = (int)(p - s0);
-          xv = xs[tt * D + d];
-          const uint32_t m = ms[d * gpt + tt / gs];
-          sc = meta_scale(m);
-          mnv = meta_min(m);
-        } else {
-          const size_t c2 = p / T_;
-          const int t2 = (int)(p % T_);
-          const size_t bh2 = c2 / D;
-          const int d2 = (int)(c2 % D);
-          const size_t grp = c2 * gpc + t2 / gs;
-          const T* base = x + (bh2 * T_ + (size_t)(t2 / gs) * gs) * D + d2;
-          if (grp != cached_group) {
-            float mn = gload(base, 0), mx = mn;
-            for (int j = 1; j < gs; ++j) {
-              const float v = gload(base, (size_t)j * D);
-              mn = v < mn ? v : mn;
-              mx = v > mx ? v : mx;
-            }
-            const uint32_t m = make_meta(mn, mx, q_max);
-            o_scale = meta_scale(m);
-            o_min = meta_min(m);
-            cached_group = grp;
-          }
-          xv = gload(x, (bh2 * T_ + t2) * D + d2);
-          sc = o_scale;
-          mnv = o_min;
-        }
-        const uint32_t code = encode(xv, sc, mnv, bits, is_narrow(bits, p));
-        word |= code << field_shift(bits, (uint32_t)k);
+    const size_t w = w_begin + j;
+    if (w >= w_end) continue;
+    const size_t p0 = w * cpw;
+    uint32_t word = 0;
+    int tt = (int)(p0 - s0);                                    // token of the first code
+    int r11 = bits == 3 ? (int)(p0 % 11u) : 0;                  // stream index mod 11
+    int g = tt / gs, gend = (g + 1) * gs;                       // current group and its end
+    uint32_t m = ms[d * gpt + g];
+    float sc = meta_scale(m), mnv = meta_min(m);
+    int k = 0;
+    for (; k < cpw && tt < nt; ++k, ++tt) {
+      if (tt == gend) {
+        ++g;
+        gend += gs;
+        m = ms[d * gpt + g];
+        sc = meta_scale(m);
+        mnv = meta_min(m);
       }
-      words[w] = word;
+      const uint32_t code = encode(xs[tt * D + d], sc, mnv, bits, bits == 3 && r11 == 10);
+      word |= code << field_shift(bits, (uint32_t)k);
+      if (++r11 == 11) r11 = 0;
     }
+    for (; k < cpw; ++k) {  // codes of the next run (rare: only at run ends)
+      const size_t p = p0 + k;
+      if (p >= n_total) break;
+      const size_t c2 = p / T_;
+      const int t2 = (int)(p % T_);
+      const size_t bh2 = c2 / D;
+      const int d2 = (int)(c2 % D);
+      const T* base = x + (bh2 * T_ + (size_t)(t2 / gs) * gs) * D + d2;
+      float mn = gload(base, 0), mx = mn;
+      for (int jj = 1; jj < gs; ++jj) {
+        const float v = gload(base, (size_t)jj * D);
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+      }
+      const uint32_t m2 = make_meta(mn, mx, q_max);
+      const float xv = gload(x, (bh2 * T_ + t2) * D + d2);
+      word |= encode(xv, meta_scale(m2), meta_min(m2), bits, is_narrow(bits, p)) << field_shift(bits, (uint32_t)k);
+    }
+    words[w] = word;
   }
 }
 
@@ -161,32 +163,49 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
   for (size_t w = w_begin + threadIdx.x; w < w_end; w += blockDim.x) {
     uint32_t word = 0;
     const size_t p0 = w * cpw;
+    // row / channel / group / stream-index-mod-11 of the first code, then stepped per code
+    const int off = (int)(p0 - s0);
+    int rr = off / D, d = off - rr * D;
+    int g = d / gs, gend = min((g + 1) * gs, D);
+    int r11 = bits == 3 ? (int)(p0 % 11u) : 0;
+    uint32_t m = rr < nr ? ms[rr * gpt + g] : 0u;
+    float sc = meta_scale(m), mnv = meta_min(m);
     for (int k = 0; k < cpw; ++k) {
       const size_t p = p0 + k;
       if (p >= n_total) break;
-      float xv, sc, mnv;
+      float xv;
       if (p < s1) {
-        const int rr = (int)((p - s0) / D), d = (int)((p - s0) % D);
         xv = xs[rr * Dp + d];
-        const uint32_t m = ms[rr * gpt + d / gs];
-        sc = meta_scale(m);
-        mnv = meta_min(m);
-      } else {
+      } else {  // codes of the next span (rare: only at span ends)
         const size_t row = p / D;
-        const int d = (int)(p % D);
-        const int d0 = (d / gs) * gs, d1 = min(d0 + gs, D);
+        const int dd = (int)(p % D);
+        const int d0 = (dd / gs) * gs, d1 = min(d0 + gs, D);
         float mn = gload(x, row * D + d0), mx = mn;
         for (int e = d0 + 1; e < d1; ++e) {
           const float v = gload(x, row * D + e);
           mn = v < mn ? v : mn;
           mx = v > mx ? v : mx;
         }
-        const uint32_t m = make_meta(mn, mx, q_max);
-        sc = meta_scale(m);
-        mnv = meta_min(m);
+        const uint32_t m2 = make_meta(mn, mx, q_max);
+        sc = meta_scale(m2);
+        mnv = meta_min(m2);
         xv = gload(x, p);
       }
-      word |= encode(xv, sc, mnv, bits, is_narrow(bits, p)) << field_shift(bits, (uint32_t)k);
+      word |= encode(xv, sc, mnv, bits, bits == 3 && r11 == 10) << field_shift(bits, (uint32_t)k);
+      if (++r11 == 11) r11 = 0;
+      if (++d == gend) {  // next channel group (or next row)
+        if (d == D) {
+          d = 0;
+          ++rr;
+        }
+        g = d / gs;
+        gend = min((g + 1) * gs, D);
+        if (rr < nr) {
+          m = ms[rr * gpt + g];
+          sc = meta_scale(m);
+          mnv = meta_min(m);
+        }
+      }
     }
     words[w] = word;
   }
