@@ -31,14 +31,45 @@ __device__ inline float gload(const T* x, size_t i) {
   return ld_f<T>(x + i);
 }
 
+// 16-byte vector of the input (8 halves / 4 floats) -> fp32
+template <typename T>
+struct Vec;
+template <>
+struct Vec<__half> {
+  static constexpr int N = 8;
+  __device__ static void load(const __half* p, float* o) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(h[i]);
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ static void load(const float* p, float* o) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  }
+};
+
 // ---- Keys -------------------------------------------------------------------------------
 // x: [B,H,T,D]; words/meta in reference order. Tile: n tokens (multiple of gs), all D.
-template <typename T>
+template <typename T, int BITS>
 __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __restrict__ x, int H, int T_,
-                                                                 int D, int bits, int gs, int n,
+                                                                 int D, int bits_rt, int gs, int n, int vec,
                                                                  uint32_t* __restrict__ words,
                                                                  uint32_t* __restrict__ meta,
                                                                  size_t n_total) {
+  constexpr int bits = BITS;
+  (void)bits_rt;
   extern __shared__ float smem[];
   float* xs = smem;                                   // [n][D]
   uint32_t* ms = reinterpret_cast<uint32_t*>(xs + (size_t)n * D);  // [D][n/gs]
@@ -50,7 +81,16 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   const int q_max = q_max_for_bits(bits);
   const T* src = x + ((size_t)bh * T_ + t0) * D;
 
-  for (int i = threadIdx.x; i < nt * D; i += blockDim.x) xs[i] = gload(src, i);
+  if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked)
+    for (int i = threadIdx.x; i < nt * D / Vec<T>::N; i += blockDim.x) {
+      float v[Vec<T>::N];
+      Vec<T>::load(src + (size_t)i * Vec<T>::N, v);
+#pragma unroll
+      for (int e = 0; e < Vec<T>::N; ++e) xs[i * Vec<T>::N + e] = v[e];
+    }
+  } else {
+    for (int i = threadIdx.x; i < nt * D; i += blockDim.x) xs[i] = gload(src, i);
+  }
   __syncthreads();
 
   for (int i = threadIdx.x; i < D * gpt; i += blockDim.x) {
@@ -126,11 +166,13 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
 
 // ---- Values -----------------------------------------------------------------------------
 // x: [rows][D] with rows = B*H*T token slots; groups along channels (partial last group).
-template <typename T>
+template <typename T, int BITS>
 __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __restrict__ x, size_t rows,
-                                                                   int D, int bits, int gs, int R,
+                                                                   int D, int bits_rt, int gs, int R, int vec,
                                                                    uint32_t* __restrict__ words,
                                                                    uint32_t* __restrict__ meta) {
+  constexpr int bits = BITS;
+  (void)bits_rt;
   extern __shared__ float smem[];
   const int gpt = (D + gs - 1) / gs;
   const int Dp = D + 1;                                                // padded row stride
@@ -140,7 +182,18 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
   const int nr = (int)min((size_t)R, rows - r0);
   const int q_max = q_max_for_bits(bits);
   const T* src = x + r0 * D;
-  for (int i = threadIdx.x; i < nr * D; i += blockDim.x) xs[(i / D) * Dp + i % D] = gload(src, i);
+  if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked)
+    const int vpr = D / Vec<T>::N;  // vectors per row
+    for (int i = threadIdx.x; i < nr * vpr; i += blockDim.x) {
+      const int rr = i / vpr, c0 = (i - rr * vpr) * Vec<T>::N;
+      float v[Vec<T>::N];
+      Vec<T>::load(src + (size_t)rr * D + c0, v);
+#pragma unroll
+      for (int e = 0; e < Vec<T>::N; ++e) xs[rr * Dp + c0 + e] = v[e];
+    }
+  } else {
+    for (int i = threadIdx.x; i < nr * D; i += blockDim.x) xs[(i / D) * Dp + i % D] = gload(src, i);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < nr * gpt; i += blockDim.x) {
     const int rr = i / gpt, g = i % gpt;
@@ -296,6 +349,7 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
   if (n == 0) return;
   if (dt != KVMIX_F32 && dt != KVMIX_F16) invalid("unsupported dtype");
   auto* m32 = reinterpret_cast<uint32_t*>(meta);
+  const int vec = (D % (dt == KVMIX_F16 ? 8 : 4) == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) ? 1 : 0;
   const int max_smem = 96 * 1024;
   if (grouping == KVMIX_PER_CHANNEL_KEY) {
     // tile of k groups of gs tokens: aim for ~128 tokens, bounded by shared memory
@@ -306,14 +360,22 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     const int n_tok = k * gs;
     const size_t smem = smem_of(k);
     dim3 grid((T + n_tok - 1) / n_tok, B * H);
+    auto go = [&](auto kern, const auto* xp) {
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kQThreads, smem, st>>>(xp, H, T, D, bits, gs, n_tok, vec, words, m32, n);
+    };
+    const float* xf = static_cast<const float*>(x);
+    const __half* xh = static_cast<const __half*>(x);
     if (dt == KVMIX_F32) {
-      auto kern = quantize_key_kernel<float>;
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
-      kern<<<grid, kQThreads, smem, st>>>(static_cast<const float*>(x), H, T, D, bits, gs, n_tok, words, m32, n);
+      if (bits == 1) go(quantize_key_kernel<float, 1>, xf);
+      else if (bits == 2) go(quantize_key_kernel<float, 2>, xf);
+      else if (bits == 3) go(quantize_key_kernel<float, 3>, xf);
+      else go(quantize_key_kernel<float, 4>, xf);
     } else {
-      auto kern = quantize_key_kernel<__half>;
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
-      kern<<<grid, kQThreads, smem, st>>>(static_cast<const __half*>(x), H, T, D, bits, gs, n_tok, words, m32, n);
+      if (bits == 1) go(quantize_key_kernel<__half, 1>, xh);
+      else if (bits == 2) go(quantize_key_kernel<__half, 2>, xh);
+      else if (bits == 3) go(quantize_key_kernel<__half, 3>, xh);
+      else go(quantize_key_kernel<__half, 4>, xh);
     }
     after_launch("quantize_key_kernel");
   } else {
@@ -325,14 +387,22 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     const size_t rows = (size_t)B * H * T;
     const size_t smem = smem_of(R);
     const unsigned grid = (unsigned)((rows + R - 1) / R);
+    auto go = [&](auto kern, const auto* xp) {
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kQThreads, smem, st>>>(xp, rows, D, bits, gs, R, vec, words, m32);
+    };
+    const float* xf = static_cast<const float*>(x);
+    const __half* xh = static_cast<const __half*>(x);
     if (dt == KVMIX_F32) {
-      auto kern = quantize_value_kernel<float>;
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
-      kern<<<grid, kQThreads, smem, st>>>(static_cast<const float*>(x), rows, D, bits, gs, R, words, m32);
+      if (bits == 1) go(quantize_value_kernel<float, 1>, xf);
+      else if (bits == 2) go(quantize_value_kernel<float, 2>, xf);
+      else if (bits == 3) go(quantize_value_kernel<float, 3>, xf);
+      else go(quantize_value_kernel<float, 4>, xf);
     } else {
-      auto kern = quantize_value_kernel<__half>;
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
-      kern<<<grid, kQThreads, smem, st>>>(static_cast<const __half*>(x), rows, D, bits, gs, R, words, m32);
+      if (bits == 1) go(quantize_value_kernel<__half, 1>, xh);
+      else if (bits == 2) go(quantize_value_kernel<__half, 2>, xh);
+      else if (bits == 3) go(quantize_value_kernel<__half, 3>, xh);
+      else go(quantize_value_kernel<__half, 4>, xh);
     }
     after_launch("quantize_value_kernel");
   }
