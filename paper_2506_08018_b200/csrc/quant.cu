@@ -142,23 +142,31 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       word |= code << field_shift(bits, (uint32_t)k);
       if (++r11 == 11) r11 = 0;
     }
-    for (; k < cpw; ++k) {  // codes of the next run (rare: only at run ends)
+    size_t cached = ~(size_t)0;  // codes of the next run (only at run ends): group meta once
+    float sc2 = 0.f, mn2 = 0.f;
+    for (; k < cpw; ++k) {
       const size_t p = p0 + k;
       if (p >= n_total) break;
       const size_t c2 = p / T_;
       const int t2 = (int)(p % T_);
       const size_t bh2 = c2 / D;
       const int d2 = (int)(c2 % D);
-      const T* base = x + (bh2 * T_ + (size_t)(t2 / gs) * gs) * D + d2;
-      float mn = gload(base, 0), mx = mn;
-      for (int jj = 1; jj < gs; ++jj) {
-        const float v = gload(base, (size_t)jj * D);
-        mn = v < mn ? v : mn;
-        mx = v > mx ? v : mx;
+      const size_t grp = c2 * (size_t)gpc + (size_t)(t2 / gs);
+      if (grp != cached) {
+        const T* base = x + (bh2 * T_ + (size_t)(t2 / gs) * gs) * D + d2;
+        float mn = gload(base, 0), mx = mn;
+        for (int jj = 1; jj < gs; ++jj) {
+          const float v = gload(base, (size_t)jj * D);
+          mn = v < mn ? v : mn;
+          mx = v > mx ? v : mx;
+        }
+        const uint32_t m2 = make_meta(mn, mx, q_max);
+        sc2 = meta_scale(m2);
+        mn2 = meta_min(m2);
+        cached = grp;
       }
-      const uint32_t m2 = make_meta(mn, mx, q_max);
       const float xv = gload(x, (bh2 * T_ + t2) * D + d2);
-      word |= encode(xv, meta_scale(m2), meta_min(m2), bits, is_narrow(bits, p)) << field_shift(bits, (uint32_t)k);
+      word |= encode(xv, sc2, mn2, bits, is_narrow(bits, p)) << field_shift(bits, (uint32_t)k);
     }
     words[w] = word;
   }
@@ -223,25 +231,33 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;
     uint32_t m = rr < nr ? ms[rr * gpt + g] : 0u;
     float sc = meta_scale(m), mnv = meta_min(m);
+    size_t cached = ~(size_t)0;
+    float sc2 = 0.f, mn2 = 0.f;
     for (int k = 0; k < cpw; ++k) {
       const size_t p = p0 + k;
       if (p >= n_total) break;
       float xv;
       if (p < s1) {
         xv = xs[rr * Dp + d];
-      } else {  // codes of the next span (rare: only at span ends)
+      } else {  // codes of the next span (only at span ends): group meta once per group
         const size_t row = p / D;
         const int dd = (int)(p % D);
         const int d0 = (dd / gs) * gs, d1 = min(d0 + gs, D);
-        float mn = gload(x, row * D + d0), mx = mn;
-        for (int e = d0 + 1; e < d1; ++e) {
-          const float v = gload(x, row * D + e);
-          mn = v < mn ? v : mn;
-          mx = v > mx ? v : mx;
+        const size_t grp = row * (size_t)gpt + (size_t)(dd / gs);
+        if (grp != cached) {
+          float mn = gload(x, row * D + d0), mx = mn;
+          for (int e = d0 + 1; e < d1; ++e) {
+            const float v = gload(x, row * D + e);
+            mn = v < mn ? v : mn;
+            mx = v > mx ? v : mx;
+          }
+          const uint32_t m2 = make_meta(mn, mx, q_max);
+          sc2 = meta_scale(m2);
+          mn2 = meta_min(m2);
+          cached = grp;
         }
-        const uint32_t m2 = make_meta(mn, mx, q_max);
-        sc = meta_scale(m2);
-        mnv = meta_min(m2);
+        sc = sc2;
+        mnv = mn2;
         xv = gload(x, p);
       }
       word |= encode(xv, sc, mnv, bits, bits == 3 && r11 == 10) << field_shift(bits, (uint32_t)k);
