@@ -370,13 +370,17 @@ __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane) {
 
 // Per-warp dynamic shared layout (bytes):
 //   ring[S][stage_bytes] | kstage | vbs[CGMAX][8][32] u8 | bars[S] u64
-// kstage: kbs[planes][8 cols][4 t][NK][2] u32 (digit words of the Key B fragments; 3-bit
-//         Keys have a second plane), then for 3-bit Keys ytab[D] f32 (narrow-slot factors)
+// kstage: kbs[planes][4R cols][4 t][NK][2] u32 (digit words of the Key B fragments; 3-bit
+//         Keys have a second plane), zeros[4 t][NK][2] (B columns without a query row),
+//         then for 3-bit Keys ytab[D] f32 (narrow-slot factors)
 //         and ntab[D] u32 (word offset | shift << 16 of each channel's low 2 bits at row 0).
 template <int D, int KB, int R>
 struct WarpLayout {
-  static constexpr int kKB = 8 * 4 * (D / 32) * 2 * 4;
-  static constexpr int kK = KB == 3 ? 2 * kKB + 2 * D * 4 : kKB;
+  static constexpr int kKC = 4 * R;  // B columns that carry query rows (lanes g >= kKC read 0)
+  static constexpr int kKB = kKC * 4 * (D / 32) * 2 * 4;
+  static constexpr int kZ = (KB == 3 ? 2 : 1) * kKB;  // zero words read by the lanes g >= kKC
+  static constexpr int kY = kZ + 4 * (D / 32) * 2 * 4;
+  static constexpr int kK = KB == 3 ? kY + 2 * D * 4 : kY;
   static constexpr int kV = (D / 32) * 8 * 32;
   static constexpr int kQ = D * 4 + 32 * 8;  // q of all channels (window blocks), checksum slots
   __host__ __device__ static constexpr size_t bytes(int stages, uint32_t stage_bytes) {
@@ -460,8 +464,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   uint8_t* ring = wbase;
   uint8_t* kstage = ring + (size_t)S * SB;
   uint32_t* kbs = reinterpret_cast<uint32_t*>(kstage);
-  float* ytab = reinterpret_cast<float*>(kstage + 2 * WL::kKB);
-  uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + 2 * WL::kKB + D * 4);
+  float* ytab = reinterpret_cast<float*>(kstage + WL::kY);
+  uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + WL::kY + D * 4);
   uint8_t* vbs = kstage + WL::kK;
   float* qbuf = reinterpret_cast<float*>(vbs + WL::kV);
   double* csm = reinterpret_cast<double*>(vbs + WL::kV + D * 4);  // per-lane checksum partials
@@ -782,7 +786,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           if constexpr (K3) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) uu[c] = ((uint32_t)__float2int_rn(xh[c] * sg) + 0x80808080u) ^ 0x80808080u;
-            store_digits(kbs + 8 * 4 * 2 * NK + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL, 4 * 2 * NK, uu);
+            store_digits(kbs + WL::kKC * 4 * 2 * NK + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL, 4 * 2 * NK, uu);
             if (r == 0) {  // narrow-slot correction table (one query row: the host routes R = 1)
               float4 y;
               y.x = qc[0][0] * invL * (wide_scale(sc[0]) - sc[0]);
@@ -799,7 +803,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
         __syncwarp();
         // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column g (digit g%4 of row g/4)
         {
-          const uint32_t* src = kbs + (g * 4 + t) * (2 * NK);
+          const bool has_col = g < WL::kKC;
+          const uint32_t* zsrc = reinterpret_cast<const uint32_t*>(kstage + WL::kZ) + t * (2 * NK);
+          const uint32_t* src = has_col ? kbs + (g * 4 + t) * (2 * NK) : zsrc;
 #pragma unroll
           for (int kk = 0; kk < NK; kk += 2) {
             const uint4 v = *reinterpret_cast<const uint4*>(src + 2 * kk);
@@ -811,7 +817,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           if constexpr (K3) {
 #pragma unroll
             for (int kk = 0; kk < NK; kk += 2) {
-              const uint4 v = *reinterpret_cast<const uint4*>(src + 8 * 4 * 2 * NK + 2 * kk);
+              const uint32_t* srch = has_col ? src + WL::kKC * 4 * 2 * NK : zsrc;
+              const uint4 v = *reinterpret_cast<const uint4*>(srch + 2 * kk);
               kbh[kk][0] = v.x;
               kbh[kk][1] = v.y;
               kbh[kk + 1][0] = v.z;
