@@ -222,7 +222,12 @@ struct MmaParams {
   const void* q;
   int q16, tail16;
   int H, Hq, tq, rows, gs, cg;
-  int row0;  // first query row of this pass (rows > 2 run as passes of <= 2 rows)
+  int row0;  // first query row of this launch; rows = query rows per pass (the slot stride)
+  // passes: query rows [row0, row0 + rows_all) run as npass row passes of <= rows rows in one
+  // launch, each unit range by npass adjacent warps (pass = global warp % npass) that stream
+  // the same records at the same time (one DRAM read, the twins hit L2); pass x uses partial
+  // slots x * pslots + (w + bh) and counters cnt[x * nbh + bh]
+  int npass, rows_all, pslots, nbh;
   int64_t T, P;  // total tokens; fast-path limit (multiple of gs)
   int64_t Pw;    // window blocks cover tokens [P, Pw) (Keys fp16 in the ring, Values packed)
   int nwb;       // window blocks per (b, kv-head)
@@ -259,7 +264,8 @@ struct MmaParams {
 // token (lane-parallel dequantization of partially aged Values, no TMA staging), so units
 // are small to keep the stream-K ranges balanced (KVMIX_TAIL_UNIT overrides, for tuning).
 constexpr int kTailUnit = 1;
-constexpr int kGroupCost = 1;  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
+constexpr int kGroupCost = 1;
+constexpr int kMaxPasses = 8;  // row passes per launch  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
 
 // first unit whose start cost is >= c (units: Gf groups of cost Qc, then window units of 1)
 __device__ __forceinline__ int unit_at_cost(const MmaParams& p, int64_t c) {
@@ -316,14 +322,14 @@ __device__ __forceinline__ unsigned long long cas_acq_rel(unsigned long long* a,
 
 // (the warp barrier orders every lane's partial before lane 0's release; the acquiring lane
 // 0 of the last arriver passes the order on to its lanes through the next warp barrier)
-__device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane) {
+__device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane, int pass) {
   __syncwarp();
   int last = 0;
   if (lane == 0) {
     int w0, w1;
     bh_warps(p, bh, w0, w1);
     const unsigned long long tag = p.epoch & 0xffffffffull;
-    unsigned long long* cw = p.cnt + bh;
+    unsigned long long* cw = p.cnt + (size_t)pass * p.nbh + bh;
     unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cw), assumed;
     unsigned int ct;
     do {
@@ -340,19 +346,20 @@ __device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane
 
 // Merge the partials of warps w0..w1 of bh in warp order (deterministic) -> out.
 template <int D>
-__device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane) {
+__device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane, int pass, int prow0, int prows) {
   constexpr int LC = D / 32;
   int w0, w1;
   bh_warps(p, bh, w0, w1);
   const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
-  for (int r = 0; r < p.rows; ++r) {
+  const size_t s0 = (size_t)pass * p.pslots + bh;
+  for (int r = 0; r < prows; ++r) {
     float M = -INFINITY;
-    for (int w = w0; w <= w1; ++w) M = fmaxf(M, __ldcg(&p.part_ml[((size_t)w + bh) * p.rows + r]).x);
+    for (int w = w0; w <= w1; ++w) M = fmaxf(M, __ldcg(&p.part_ml[(s0 + w) * p.rows + r]).x);
     float L = 0.f, a[LC];
 #pragma unroll
     for (int c = 0; c < LC; ++c) a[c] = 0.f;
     for (int w = w0; w <= w1; ++w) {
-      const size_t pi = ((size_t)w + bh) * p.rows + r;
+      const size_t pi = (s0 + w) * p.rows + r;
       const float2 ml = __ldcg(&p.part_ml[pi]);
       if (ml.x == -INFINITY) continue;
       const float f = expf(ml.x - M);
@@ -360,7 +367,7 @@ __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane) {
 #pragma unroll
       for (int c = 0; c < LC; ++c) a[c] += __ldcg(&p.part_acc[pi * D + lane * LC + c]) * f;
     }
-    const int gi = (p.row0 + r) / p.tq, qi = (p.row0 + r) % p.tq;
+    const int gi = (prow0 + r) / p.tq, qi = (prow0 + r) % p.tq;
     float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
     const float il = 1.0f / L;
 #pragma unroll
@@ -435,8 +442,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   __shared__ float s_acc[kMmaWarps][R][D];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wg = blockIdx.x * kMmaWarps + warp;  // warps are independent: no CTA barriers
+  // warps are independent (no CTA barriers); npass adjacent warps share a unit range
+  const int gw = blockIdx.x * kMmaWarps + warp;
+  const int pass = gw % p.npass, wg = gw / p.npass;
   if (wg >= p.W) return;
+  const int prow0 = p.row0 + pass * p.rows;                // this pass's query rows
+  const int prows = min(p.rows, p.rows_all - pass * p.rows);
+  const size_t pbase = (size_t)pass * p.pslots;            // this pass's partial slots
   const int g = lane >> 2, t = lane & 3;
   const int G = p.Hq / p.H;
   const int gs = GS ? GS : p.gs;
@@ -454,9 +466,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     int w0, w1;
     bh_warps(p, bh, w0, w1);
     if (wg < w0 || wg > w1) return;
-    if (lane < p.rows) p.part_ml[((size_t)wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
-    if (lane == 0 && p.want_cs) p.part_cs[(size_t)wg + bh] = 0.0;
-    if (arrive_last(p, bh, lane)) merge_bh<D>(p, bh, lane);
+    if (lane < prows) p.part_ml[(pbase + wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
+    if (lane == 0 && p.want_cs) p.part_cs[pbase + wg + bh] = 0.0;
+    if (arrive_last(p, bh, lane, pass)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
     return;
   }
 
@@ -484,7 +496,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 
   // this lane's softmax row: lanes t = 2r, 2r+1 hold row r (IMMA score columns 4r .. 4r+3)
   const int my_r = t >> 1;
-  const bool row_ok = my_r < p.rows;
+  const bool row_ok = my_r < prows;
 
   // producer: this warp's fast groups in work-list order, issued S ahead of the consumer
   // (running record pointer, groups left in the current (b, kv-head), groups left to issue)
@@ -526,12 +538,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 
   // fused 1-token append: the warp whose range holds a (b, kv-head)'s first window unit
   // appends its token (only the window path reads what the append writes), then publishes
-  if (p.fused) {
+  // (pass 0 only; the other passes' twins wait for the flag like later warps)
+  if (p.fused && pass == 0) {
     for (int bh = u_beg / p.U; bh <= (u_end - 1) / p.U; ++bh) {
       const int x = bh * p.U + p.Gf;
       if (x >= u_beg && x < u_end) {
         decode_append_warp(p.da, bh, lane);
-        if ((bh + 1) * p.U > u_end) {  // later warps read this window too: publish
+        if ((bh + 1) * p.U > u_end || p.npass > 1) {  // other warps read this window too: publish
           __threadfence();
           __syncwarp();
           if (lane == 0) st_release(p.flags + bh, p.epoch);
@@ -575,13 +588,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     float qv[R][4];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int rr = p.row0 + (r < p.rows ? r : 0);
+      const int rr = prow0 + (r < prows ? r : 0);
       const int gi = rr / p.tq, qi = rr % p.tq;
       const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + 4 * Lq;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float x = p.q16 ? __half2float(static_cast<const __half*>(p.q)[off + c]) : static_cast<const float*>(p.q)[off + c];
-        qv[r][c] = r < p.rows ? x : 0.f;
+        qv[r][c] = r < prows ? x : 0.f;
       }
     }
     if constexpr (R == 1) {  // q of every channel for the window blocks' dot products
@@ -954,7 +967,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     // ---- window blocks: 32 tokens of the full-precision Key window whose Values are packed
     // (Keys: lane = token fp32 dot products from the ring; Values: the IMMA block path on the
     // partial group's tiles). Waits for the fused append when an earlier warp made it.
-    if (p.fused && lo > p.Gf && hi > p.Gf) {
+    if (p.fused && (lo > p.Gf || pass != 0) && hi > p.Gf) {
       while (ld_acquire(p.flags + bh) != p.epoch) __nanosleep(32);
     }
     if constexpr (R == 1) {
@@ -1074,7 +1087,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
       float qt[R][LC];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int rr = p.row0 + (r < p.rows ? r : 0);
+        const int rr = prow0 + (r < prows ? r : 0);
         const int gi = rr / p.tq, qi = rr % p.tq;
         const size_t off = (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + d0;
 #pragma unroll
@@ -1157,7 +1170,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           if (j0 + i >= j_hi) break;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            if (r < p.rows) {
+            if (r < prows) {
               const float sc = x[i][r] * p.inv;
               if (p.want_cs && lane == 0) csm[0] += (double)sc;
               const float ls = sc * kLog2e;
@@ -1177,7 +1190,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     // ---- segment epilogue ----------------------------------------------------------------
     // A (b, kv-head) inside this warp's range is normalized and written directly; otherwise
     // the partial goes to slot wg + bh and the last of its warps to arrive merges them.
-    const int64_t slot = (int64_t)wg + bh;
+    const size_t slot = pbase + wg + bh;
     if (p.want_cs) {
       double csl = csm[lane];
       for (int o = 16; o > 0; o >>= 1) csl += __shfl_xor_sync(0xffffffffu, csl, o);
@@ -1186,8 +1199,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     if (lo == 0 && hi == p.U) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (r < p.rows) {
-          const int gi = (p.row0 + r) / p.tq, qi = (p.row0 + r) % p.tq;
+        if (r < prows) {
+          const int gi = (prow0 + r) / p.tq, qi = (prow0 + r) % p.tq;
           float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
           const float il = 1.0f / l_all[r];
 #pragma unroll
@@ -1197,8 +1210,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (r < p.rows) {
-          const size_t pi = (size_t)slot * p.rows + r;
+        if (r < prows) {
+          const size_t pi = slot * p.rows + r;
           if constexpr (LC == 4) {
             *reinterpret_cast<float4*>(p.part_acc + pi * D + lane * LC) =
                 make_float4(acct[r][0], acct[r][1], acct[r][2], acct[r][3]);
@@ -1209,7 +1222,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           if (lane == 0) p.part_ml[pi] = make_float2(m_all[r] == -INFINITY ? -INFINITY : m_all[r] * kLn2, l_all[r]);
         }
       }
-      if (arrive_last(p, bh, lane)) merge_bh<D>(p, bh, lane);
+      if (arrive_last(p, bh, lane, pass)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
     }
     __syncwarp();  // s_acc is rewritten by the next segment
   }
@@ -1255,17 +1268,22 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   }
   // one resident wave of independent warps (persistent): equal unit ranges, no stragglers;
   // never more warps than units so every range is non-empty
+  // (the npass warps of a unit range count once per pass)
   const int64_t wave = (int64_t)std::max(1, occ) * num_sms() * kMmaWarps;
-  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(p.N, wave));
-  // partial slots w + bh < W + BH: scratch depends on (B, H, rows, D, SM count) only
-  const size_t slots = (size_t)wave + BH;
+  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(p.N, wave / p.npass));
+  // partial slots x * pslots + w + bh (w + bh < W + BH): scratch depends on (B, H, rows, D,
+  // SM count) only
+  p.pslots = (int)(wave + BH);
+  p.nbh = BH;
+  const size_t slots = (size_t)p.npass * p.pslots;
   p.part_ml = ws.ml(st, slots * p.rows);
   p.part_acc = ws.acc(st, slots * p.rows * D);
   p.part_cs = ws.cs(st, slots + 1);
-  p.cnt = ws.get<unsigned long long>(st, (size_t)BH);
+  p.cnt = ws.get<unsigned long long>(st, (size_t)p.npass * BH);
   if (p.fused) p.flags = ws.get<unsigned long long>(st, (size_t)BH);
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
-  kern<<<(p.W + kMmaWarps - 1) / kMmaWarps, kMmaWarps * 32, smem, st>>>(p);
+  const int64_t warps = (int64_t)p.W * p.npass;
+  kern<<<(unsigned)((warps + kMmaWarps - 1) / kMmaWarps), kMmaWarps * 32, smem, st>>>(p);
   return p.W;
 }
 
@@ -1304,8 +1322,11 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (kb == 3 && D != 128) return false;
   // query rows per pass: 2 (the B operand holds two rows' four digits), 1 for 3-bit Keys
   // (their narrow-slot table is per row); more rows (GQA G > 2, several query tokens) run
-  // as successive passes over the cache
-  const int per_pass = kb == 3 ? 1 : 2;
+  // as row passes inside one launch, up to kMaxPasses per launch (their warps stream the
+  // same records together, so the cache is read from DRAM about once per launch)
+  const int per_pass = rows == 1 ? 1 : kb == 3 ? 1 : 2;
+  const int npass_all = (rows + per_pass - 1) / per_pass;
+  const int chunk = std::min(npass_all, kMaxPasses);
   const int BH = c->B * c->H;
   const int64_t T = c->total();
   MmaParams p{};
@@ -1357,21 +1378,23 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     }
     return (int64_t)p.Gf + p.nwb + (T - p.Pw + p.tail_unit - 1) / p.tail_unit;
   };
-  for (int r0 = 0; r0 < rows; r0 += per_pass)
-    if ((int64_t)BH * layout(std::min(per_pass, rows - r0)) >= (int64_t)1 << 31) return false;
+  if ((int64_t)BH * layout(per_pass) >= (int64_t)1 << 31) return false;
 
   double cs_total = 0.0;
-  for (int r0 = 0; r0 < rows; r0 += per_pass) {
-    const int nrows = std::min(per_pass, rows - r0);
+  for (int x0 = 0; x0 < npass_all; x0 += chunk) {
+    const int r0 = x0 * per_pass;
+    const int nrows = per_pass;  // rows per pass (the last pass of a launch may hold fewer)
     p.row0 = r0;
     p.rows = nrows;
+    p.npass = std::min(chunk, npass_all - x0);
+    p.rows_all = std::min(rows - r0, p.npass * per_pass);
     p.U = (int)layout(nrows);
     p.N = BH * p.U;
     p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
     p.Nc = (int64_t)BH * p.cost_bh;
     p.epoch = next_epoch();
     p.fused = 0;
-    if (da && r0 == 0) {  // the first pass runs the append; later passes follow in stream order
+    if (da && r0 == 0) {  // the first launch runs the append; later launches follow in stream order
       p.fused = 1;
       p.da = *da;
     }
@@ -1390,7 +1413,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     }
     after_launch("attend_mma_kernel");
     if (checksum) {
-      const size_t nslot = (size_t)p.W + BH;
+      const size_t nslot = (size_t)p.npass * p.pslots;
       checksum_kernel<<<1, 32, 0, st>>>(p.part_cs, nslot, p.part_cs + nslot);
       after_launch("checksum_kernel");
       double part = 0.0;

@@ -115,10 +115,11 @@ def test_attend_gqa(cuda, G):
     check_attend(dev, ora, q, G=G, expect_mma=True)
 
 
-@pytest.mark.parametrize("kb,vb,G,tq", [(3, 4, 2, 1), (4, 2, 4, 1), (2, 4, 1, 3)])
+@pytest.mark.parametrize("kb,vb,G,tq", [(3, 4, 2, 1), (4, 2, 4, 1), (2, 4, 1, 3), (2, 2, 4, 5), (3, 2, 2, 5), (4, 4, 8, 3)])
 def test_attend_multi_pass_rows(cuda, kb, vb, G, tq):
-    """More than two query rows per KV head (GQA and/or several query tokens): passes over
-    the cache (one row per pass for 3-bit Keys), checksums summed over the passes."""
+    """More than two query rows per KV head (GQA and/or several query tokens): row passes
+    (one row per pass for 3-bit Keys) inside one launch, up to 8 per launch (20 rows: two
+    launches), a last pass with one row, checksums summed over the passes."""
     dev, ora = build(kb, vb, 0.2, 0.2, 32, 1, 4, 128, [900] + [1] * 12, seed=27)
     q = O.random_h16(28, (1, 4 * G, tq, 128), sigma=1.5)
     check_attend(dev, ora, q, G=G, expect_mma=True)
@@ -266,7 +267,8 @@ def test_errors(cuda):
 
 
 @pytest.mark.parametrize("kb,vb,D,G,tail", [(2, 2, 128, 1, torch.float16), (3, 4, 128, 1, torch.float32),
-                                             (4, 2, 64, 2, torch.float16), (2, 4, 128, 1, torch.float32)])
+                                             (4, 2, 64, 2, torch.float16), (2, 4, 128, 1, torch.float32),
+                                             (2, 2, 128, 4, torch.float16), (3, 4, 128, 4, torch.float32)])
 def test_append_attend_matches_separate_calls(cuda, kb, vb, D, G, tail):
     """kvmix_append_attend (the append fused into the attention launch when it is a decode
     step) == append() then attend(): identical outputs, identical cache state, and the fused
