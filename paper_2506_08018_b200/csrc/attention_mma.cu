@@ -250,7 +250,8 @@ struct MmaParams {
   DecodeAppend da;
   unsigned long long* flags;  // per (b, kv-head): epoch once its append is done
   unsigned long long epoch;
-  unsigned long long* cnt;    // per (b, kv-head): {call tag, partials published} (merge by the last)
+  unsigned long long* cnt;    // per (b, kv-head): {call tag, octets published} (merge by the last)
+  unsigned long long* cnt8;   // per (warp octet k, bh) at slot k + bh: {call tag, partials published}
   float* out;
   int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
   int tail_unit;     // window tokens per work unit
@@ -311,8 +312,7 @@ __device__ __forceinline__ void bh_warps(const MmaParams& p, int bh, int& w0, in
   w1 = warp_at_cost(p, s1);
 }
 
-// Publish this warp's partial of bh; returns true for the last of the bh's warps to arrive
-// (the counter word carries the call's tag, so it needs no clearing between calls).
+// 64-bit CAS with acquire-release semantics at GPU scope
 __device__ __forceinline__ unsigned long long cas_acq_rel(unsigned long long* a, unsigned long long cmp,
                                                           unsigned long long val) {
   unsigned long long old;
@@ -320,58 +320,111 @@ __device__ __forceinline__ unsigned long long cas_acq_rel(unsigned long long* a,
   return old;
 }
 
+// Tagged arrival counter: returns true for the n-th arriver of this call (the word carries
+// the call's tag, so it needs no clearing between calls).
+__device__ __forceinline__ bool count_arrival(unsigned long long* cw, unsigned long long tag, int n) {
+  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cw), assumed;
+  unsigned int ct;
+  do {
+    assumed = old;
+    ct = (assumed >> 32) == tag ? (unsigned int)assumed : 0u;
+    old = cas_acq_rel(cw, assumed, (tag << 32) | (ct + 1u));
+  } while (old != assumed);
+  return (int)(ct + 1u) == n;
+}
+
+// Publish this warp's partial of bh; returns true for the last of the bh's warps to arrive.
+// Two levels (warps in octets, then the octets) keep at most 8 warps retrying a CAS on one
+// word: a (b, kv-head) split over dozens of warps would otherwise serialize on its counter.
 // (the warp barrier orders every lane's partial before lane 0's release; the acquiring lane
 // 0 of the last arriver passes the order on to its lanes through the next warp barrier)
-__device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane, int pass) {
+__device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane, int pass, int wg) {
   __syncwarp();
   int last = 0;
   if (lane == 0) {
     int w0, w1;
     bh_warps(p, bh, w0, w1);
     const unsigned long long tag = p.epoch & 0xffffffffull;
-    unsigned long long* cw = p.cnt + (size_t)pass * p.nbh + bh;
-    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cw), assumed;
-    unsigned int ct;
-    do {
-      assumed = old;
-      ct = (assumed >> 32) == tag ? (unsigned int)assumed : 0u;
-      old = cas_acq_rel(cw, assumed, (tag << 32) | (ct + 1u));
-    } while (old != assumed);
-    last = (int)(ct + 1u) == w1 - w0 + 1;
+    const int k = wg >> 3;
+    const int a = max(w0, 8 * k), z = min(w1, 8 * k + 7);
+    last = z == a || count_arrival(p.cnt8 + (size_t)pass * p.pslots + k + bh, tag, z - a + 1);
+    const int nsub = (w1 >> 3) - (w0 >> 3) + 1;
+    if (last && nsub > 1) last = count_arrival(p.cnt + (size_t)pass * p.nbh + bh, tag, nsub);
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   __syncwarp();
   return last != 0;
 }
 
-// Merge the partials of warps w0..w1 of bh in warp order (deterministic) -> out.
+// Merge the partials of warps w0..w1 of bh (deterministic) -> out. A (b, kv-head) can be
+// split over dozens of warps when there are few of them (B8 x 8 KV heads: ~37 per head), so
+// the lanes read the partials' (m, l) in parallel and the accumulator rows are streamed with
+// several loads in flight; the rows sum in warp order.
+template <int D>
+__device__ __forceinline__ float4 ld_part(const float* a) {
+  if constexpr (D == 128) return __ldcg(reinterpret_cast<const float4*>(a));
+  else {
+    const float2 x = __ldcg(reinterpret_cast<const float2*>(a));
+    return make_float4(x.x, x.y, 0.f, 0.f);
+  }
+}
 template <int D>
 __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane, int pass, int prow0, int prows) {
   constexpr int LC = D / 32;
+  static_assert(LC == 2 || LC == 4, "merge: D in {64, 128}");
   int w0, w1;
   bh_warps(p, bh, w0, w1);
   const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
   const size_t s0 = (size_t)pass * p.pslots + bh;
   for (int r = 0; r < prows; ++r) {
     float M = -INFINITY;
-    for (int w = w0; w <= w1; ++w) M = fmaxf(M, __ldcg(&p.part_ml[(s0 + w) * p.rows + r]).x);
-    float L = 0.f, a[LC];
+    for (int w = w0 + lane; w <= w1; w += 32) M = fmaxf(M, __ldcg(&p.part_ml[(s0 + w) * p.rows + r]).x);
 #pragma unroll
-    for (int c = 0; c < LC; ++c) a[c] = 0.f;
-    for (int w = w0; w <= w1; ++w) {
-      const size_t pi = (s0 + w) * p.rows + r;
-      const float2 ml = __ldcg(&p.part_ml[pi]);
-      if (ml.x == -INFINITY) continue;
-      const float f = expf(ml.x - M);
-      L += ml.y * f;
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int wb = w0; wb <= w1; wb += 32) {
+      float f = 0.f;
+      if (wb + lane <= w1) {
+        const float2 ml = __ldcg(&p.part_ml[(s0 + wb + lane) * p.rows + r]);
+        if (ml.x != -INFINITY) {
+          f = expf(ml.x - M);
+          L += ml.y * f;
+        }
+      }
+      const int nb = min(32, w1 - wb + 1);
+      const float* base = p.part_acc + ((s0 + wb) * p.rows + r) * D + lane * LC;
+      const size_t step = (size_t)p.rows * D;
+      for (int i = 0; i < nb; i += 4) {
+        float fi[4];
+        float4 x[4];
 #pragma unroll
-      for (int c = 0; c < LC; ++c) a[c] += __ldcg(&p.part_acc[pi * D + lane * LC + c]) * f;
+        for (int k = 0; k < 4; ++k) {
+          fi[k] = __shfl_sync(0xffffffffu, f, (i + k) & 31);
+          if (i + k >= nb) fi[k] = 0.f;
+          // neutral partials (f = 0) never wrote their accumulator row: not read
+          x[k] = fi[k] != 0.f ? ld_part<D>(base + (size_t)(i + k) * step) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          a.x = fmaf(x[k].x, fi[k], a.x);
+          a.y = fmaf(x[k].y, fi[k], a.y);
+          a.z = fmaf(x[k].z, fi[k], a.z);
+          a.w = fmaf(x[k].w, fi[k], a.w);
+        }
+      }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     const int gi = (prow0 + r) / p.tq, qi = (prow0 + r) % p.tq;
     float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
     const float il = 1.0f / L;
-#pragma unroll
-    for (int c = 0; c < LC; ++c) o[c] = a[c] * il;
+    o[0] = a.x * il;
+    o[1] = a.y * il;
+    if constexpr (LC == 4) {
+      o[2] = a.z * il;
+      o[3] = a.w * il;
+    }
   }
 }
 
@@ -468,7 +521,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
     if (wg < w0 || wg > w1) return;
     if (lane < prows) p.part_ml[(pbase + wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
     if (lane == 0 && p.want_cs) p.part_cs[pbase + wg + bh] = 0.0;
-    if (arrive_last(p, bh, lane, pass)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
+    if (arrive_last(p, bh, lane, pass, wg)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
     return;
   }
 
@@ -1222,7 +1275,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
           if (lane == 0) p.part_ml[pi] = make_float2(m_all[r] == -INFINITY ? -INFINITY : m_all[r] * kLn2, l_all[r]);
         }
       }
-      if (arrive_last(p, bh, lane, pass)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
+      if (arrive_last(p, bh, lane, pass, wg)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
     }
     __syncwarp();  // s_acc is rewritten by the next segment
   }
@@ -1280,6 +1333,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.part_acc = ws.acc(st, slots * p.rows * D);
   p.part_cs = ws.cs(st, slots + 1);
   p.cnt = ws.get<unsigned long long>(st, (size_t)p.npass * BH);
+  p.cnt8 = ws.get<unsigned long long>(st, slots);
   if (p.fused) p.flags = ws.get<unsigned long long>(st, (size_t)BH);
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
   const int64_t warps = (int64_t)p.W * p.npass;

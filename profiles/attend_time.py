@@ -1,5 +1,6 @@
 """In-stream attention time per tier at the config-2 state (B16, H32, D128, ~8k ctx, decode
-appends to the steady window), CUDA events, median of 20 launches per window length."""
+appends to the steady window), CUDA events, median of 20 launches per window length.
+SHAPE=B,H,G,CTX overrides the shape (e.g. SHAPE=8,8,4,32768 for the Mistral-7B GQA config)."""
 import os
 import statistics
 import sys
@@ -10,12 +11,15 @@ import torch  # noqa: E402
 import paper_2506_08018_b200 as K  # noqa: E402
 
 B, H, D, CTX = 16, 32, 128, 8192
+G = 1
+if os.environ.get("SHAPE"):
+    B, H, G, CTX = (int(x) for x in os.environ["SHAPE"].split(","))
 torch.manual_seed(0)
 for kb, vb, r in ((2, 2, 0.1), (3, 4, 0.2)):
     c = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), B, H, D, capacity_tokens=CTX + 64, tail_dtype=torch.float16)
     c.append(torch.randn(B, H, CTX - 64, D, device="cuda", dtype=torch.float16),
              torch.randn(B, H, CTX - 64, D, device="cuda", dtype=torch.float16))
-    q = torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16)
+    q = torch.randn(B, H * G, 1, D, device="cuda", dtype=torch.float16)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     res = []
     for s in range(40):

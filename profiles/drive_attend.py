@@ -13,6 +13,9 @@ import torch  # noqa: E402
 import paper_2506_08018_b200 as K  # noqa: E402
 
 B, H, D, CTX = 16, 32, 128, 8192
+G = 1
+if os.environ.get("SHAPE"):  # B,H,G,CTX (e.g. 8,8,4,32768: the Mistral-7B GQA config)
+    B, H, G, CTX = (int(x) for x in os.environ["SHAPE"].split(","))
 tiers = [(2, 2, 0.1), (3, 4, 0.2)]
 if len(sys.argv) > 1:
     tiers = [tiers[int(i)] for i in sys.argv[1].split(",")]
@@ -24,7 +27,7 @@ for kb, vb, r in tiers:
     for _ in range(64):
         x = torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16)
         c.append(x, x)
-    q = torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16)
+    q = torch.randn(B, H * G, 1, D, device="cuda", dtype=torch.float16)
     for _ in range(3):
         K.attend(q, c, checksum=False)
     torch.cuda.synchronize()
