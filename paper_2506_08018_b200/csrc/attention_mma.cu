@@ -32,7 +32,7 @@
 // per lane, channel -> field table) with q_d (wide_scale(s_d) - s_d).
 //
 // Query rows: two per pass (one B column quadruple each); more rows (GQA with G > 2, several
-// query tokens) run as passes over the cache; 3-bit Keys one row per pass.
+// query tokens) run as row passes inside one launch.
 //
 // The full-precision Key window whose Values are already packed runs as 32-token "window
 // blocks" (lane = token fp32 dot products from the ring, then the IMMA Value block).
@@ -64,7 +64,9 @@ constexpr int kMmaWarps = 4;
 #ifndef KVB_MIN_CTAS_N
 #define KVB_MIN_CTAS_N 4
 #endif
-#define KVB_MIN_CTAS(KB) KVB_MIN_CTAS_N  // CTAs per SM the register budget is sized for
+// CTAs per SM the register budget is sized for: 3-bit Keys with two query rows (GQA) get 3
+// (their B staging leaves shared memory for 3 CTAs with a two-stage ring anyway)
+#define KVB_MIN_CTAS(KB, R) ((KB) == 3 && (R) == 2 ? 3 : KVB_MIN_CTAS_N)
 #endif
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -432,7 +434,7 @@ __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane, i
 //   ring[S][stage_bytes] | kstage | vbs[CGMAX][8][32] u8 | bars[S] u64
 // kstage: kbs[planes][4R cols][4 t][NK][2] u32 (digit words of the Key B fragments; 3-bit
 //         Keys have a second plane), zeros[4 t][NK][2] (B columns without a query row),
-//         then for 3-bit Keys ytab[D] f32 (narrow-slot factors)
+//         then for 3-bit Keys ytab[R][D] f32 (narrow-slot factors per query row)
 //         and ntab[D] u32 (word offset | shift << 16 of each channel's low 2 bits at row 0).
 template <int D, int KB, int R>
 struct WarpLayout {
@@ -440,7 +442,7 @@ struct WarpLayout {
   static constexpr int kKB = kKC * 4 * (D / 32) * 2 * 4;
   static constexpr int kZ = (KB == 3 ? 2 : 1) * kKB;  // zero words read by the lanes g >= kKC
   static constexpr int kY = kZ + 4 * (D / 32) * 2 * 4;
-  static constexpr int kK = KB == 3 ? kY + 2 * D * 4 : kY;
+  static constexpr int kK = KB == 3 ? kY + (R + 1) * D * 4 : kY;
   static constexpr int kV = (D / 32) * 8 * 32;
   static constexpr int kQ = D * 4 + 32 * 8;  // q of all channels (window blocks), checksum slots
   __host__ __device__ static constexpr size_t bytes(int stages, uint32_t stage_bytes) {
@@ -471,7 +473,7 @@ struct StageGeo {
 
 // GS: 0 = runtime group size (a multiple of 32), else compile-time (32 is the KVmix default).
 template <int D, int KB, int VB, int R, int GS>
-__global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_kernel(MmaParams p) {
+__global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mma_kernel(MmaParams p) {
   static_assert(D == 64 || D == 128, "IMMA attention handles D in {64, 128}");
   static_assert(VB == 2 || VB == 4, "Values: 2 or 4 bits");
   static_assert(R == 1 || R == 2, "one or two query rows per KV head");
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
   uint8_t* kstage = ring + (size_t)S * SB;
   uint32_t* kbs = reinterpret_cast<uint32_t*>(kstage);
   float* ytab = reinterpret_cast<float*>(kstage + WL::kY);
-  uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + WL::kY + D * 4);
+  uint32_t* ntab = reinterpret_cast<uint32_t*>(kstage + WL::kY + R * D * 4);
   uint8_t* vbs = kstage + WL::kK;
   float* qbuf = reinterpret_cast<float*>(vbs + WL::kV);
   double* csm = reinterpret_cast<double*>(vbs + WL::kV + D * 4);  // per-lane checksum partials
@@ -853,13 +855,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
 #pragma unroll
             for (int c = 0; c < 4; ++c) uu[c] = ((uint32_t)__float2int_rn(xh[c] * sg) + 0x80808080u) ^ 0x80808080u;
             store_digits(kbs + WL::kKC * 4 * 2 * NK + ((4 * r) * 4 + tL) * (2 * NK) + kkL * 2 + hL, 4 * 2 * NK, uu);
-            if (r == 0) {  // narrow-slot correction table (one query row: the host routes R = 1)
+            {  // narrow-slot correction table of this row
               float4 y;
-              y.x = qc[0][0] * invL * (wide_scale(sc[0]) - sc[0]);
-              y.y = qc[0][1] * invL * (wide_scale(sc[1]) - sc[1]);
-              y.z = qc[0][2] * invL * (wide_scale(sc[2]) - sc[2]);
-              y.w = qc[0][3] * invL * (wide_scale(sc[3]) - sc[3]);
-              *reinterpret_cast<float4*>(ytab + 4 * lane) = y;
+              y.x = qc[r][0] * invL * (wide_scale(sc[0]) - sc[0]);
+              y.y = qc[r][1] * invL * (wide_scale(sc[1]) - sc[1]);
+              y.z = qc[r][2] * invL * (wide_scale(sc[2]) - sc[2]);
+              y.w = qc[r][3] * invL * (wide_scale(sc[3]) - sc[3]);
+              *reinterpret_cast<float4*>(ytab + r * D + 4 * lane) = y;
             }
           }
 #pragma unroll
@@ -943,7 +945,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
             // lane (g, t) corrects token jt = g + 8t of the block: narrow channels d = d0 + 11k
             const int jt = g + 8 * t, tg = 32 * blk + jt;
             const int rres = ((10 - omod - tg) % 11 + 11) % 11;
-            float dlt = 0.f;
+            float dlt[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) dlt[r] = 0.f;
             if (nmod != 0) {
               const int d0 = ((rres * inv11(nmod) - cb11) % 11 + 11) % 11;
               const uint32_t* tile = kt2 + (t >> 1) * tile_words(D, KB);
@@ -954,13 +958,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB)) attend_mma_k
                 if (d < D) {
                   const uint32_t tb = ntab[d];  // {word offset at row 0 | shift << 16}
                   const uint32_t code = (tile[(tb & 0xffffu) + rowoff] >> (tb >> 16)) & 3u;
-                  dlt = fmaf((float)code, ytab[d], dlt);
+#pragma unroll
+                  for (int r = 0; r < R; ++r) dlt[r] = fmaf((float)code, ytab[r * D + d], dlt[r]);
                 }
               }
             }
             const float wsn = p.inv * kLog2e;
 #pragma unroll
-            for (int x = 0; x < 4; ++x) corr[x] = __shfl_sync(0xffffffffu, dlt, 4 * g + x) * wsn;
+            for (int x = 0; x < 4; ++x) {  // row my_r of token g + 8x (lane 4g + x made it)
+              float c = __shfl_sync(0xffffffffu, dlt[0], 4 * g + x);
+              if constexpr (R == 2) {
+                const float c1 = __shfl_sync(0xffffffffu, dlt[1], 4 * g + x);
+                c = my_r ? c1 : c;
+              }
+              corr[x] = c * wsn;
+            }
             if (nmod == 0) {  // every channel of the tokens with (omod + tg) % 11 == 10 is narrow
 #pragma unroll
               for (int x = 0; x < 4; ++x) {
@@ -1343,8 +1355,8 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
 
 template <int D, int KB, int VB, int R>
 int dispatch_gs(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
-  if constexpr (KB == 3 && (D != 128 || R != 1)) {
-    return 0;  // 3-bit Keys: one query row per pass (attend_mma never asks for two)
+  if constexpr (KB == 3 && D != 128) {
+    return 0;  // 3-bit Keys: D = 128 (attend_mma never asks for another)
   } else {
     return p.gs == 32 ? launch<D, KB, VB, R, 32>(p, BH, ws, st) : launch<D, KB, VB, R, 0>(p, BH, ws, st);
   }
@@ -1374,11 +1386,10 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   if (gs % 32 != 0) return false;  // groups are processed in 32-token blocks
   if (D != 64 && D != 128) return false;
   if (kb == 3 && D != 128) return false;
-  // query rows per pass: 2 (the B operand holds two rows' four digits), 1 for 3-bit Keys
-  // (their narrow-slot table is per row); more rows (GQA G > 2, several query tokens) run
+  // query rows per pass: 2 (the B operand holds two rows' four digits); more rows (GQA G > 2, several query tokens) run
   // as row passes inside one launch, up to kMaxPasses per launch (their warps stream the
   // same records together, so the cache is read from DRAM about once per launch)
-  const int per_pass = rows == 1 ? 1 : kb == 3 ? 1 : 2;
+  const int per_pass = rows == 1 ? 1 : 2;
   const int npass_all = (rows + per_pass - 1) / per_pass;
   const int chunk = std::min(npass_all, kMaxPasses);
   const int BH = c->B * c->H;
