@@ -40,8 +40,12 @@ CONFIGS = {
     "llama2-7b-8k": (32, 16, 32, 32, 128, 8192, 6),          # configs[1]
     "layer-4k": (1, 1, 32, 32, 128, 4096, 0),                  # configs[0] shape
     "mistral-7b-32k": (32, 8, 8, 32, 128, 32768, 6),          # configs[2]
+    # configs[3] is B32 sharded batch x KV-head over 8 GPUs: one rank's shard is B4 (weak
+    # scaling: every rank holds its own B4 shard, ~140 GB of HBM with the fp16 windows)
+    "llama2-13b-128k-shard": (40, 4, 40, 40, 128, 131072, 8),  # configs[3], per-GPU shard
 }
-CONFIG_INDEX = {"llama2-7b-8k": "configs[1]", "layer-4k": "configs[0]", "mistral-7b-32k": "configs[2]"}
+CONFIG_INDEX = {"llama2-7b-8k": "configs[1]", "layer-4k": "configs[0]", "mistral-7b-32k": "configs[2]",
+                "llama2-13b-128k-shard": "configs[3] per-GPU shard (B32 / 8 ranks)"}
 
 
 def parse():
