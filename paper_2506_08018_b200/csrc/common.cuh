@@ -82,6 +82,31 @@ __device__ inline uint32_t encode(float x, float scale, float minv, int bits, bo
   return r >= (float)q_max ? (uint32_t)q_max : (uint32_t)r;
 }
 
+// encode() without the IEEE division on the common path. va = RN(x - min) * rcp(s) is
+// within 2 ulp of v = RN((x - min) / s) (rcp.approx: 1 ulp, the product 0.5), i.e. within
+// 2^-19 for every v below 16, so the rounding of va and v can differ only when va lies
+// within that distance of a half-integer: there (and for NaN, infinities and |va| >= 2^62)
+// the exact encode() decides. s_eff / rc / qm are the slot's scale (wide for Mixed3 narrow
+// slots), its approximate reciprocal and code range; bit-exact with encode(x, scale, ...).
+__device__ inline float rcp_approx(float s) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+  return r;
+}
+__device__ inline uint32_t encode_fast(float x, float scale, float minv, float s_eff, float rc, int qm, int bits,
+                                       bool narrow) {
+  constexpr float kTie = 0x1p-14f;  // 32x the worst-case distance between va and v
+  if (s_eff == 0.0f) return 0u;
+  const float va = __fmul_rn(__fsub_rn(x, minv), rc);
+  if (va < 0.5f - kTie) return 0u;  // v < 0.5: rounds to <= 0 (also -inf)
+  if (va > (float)qm - 0.5f + kTie && va < 0x1p62f) return (uint32_t)qm;
+  const float t = va + 0.5f;  // va in [0.5 - kTie, qm - 0.5 + kTie]: error <= 2^-20
+  const float r = floorf(t);
+  const float f = t - r;
+  if (f >= kTie && f <= 1.0f - kTie) return (uint32_t)r;
+  return encode(x, scale, minv, bits, narrow);  // near a tie, NaN or huge: exact path
+}
+
 // decode_code (quant.cpp:49-53): code*scale then +min, two rounded ops.
 __device__ inline float decode(uint32_t code, float scale, float minv, bool narrow) {
   const float s = narrow ? wide_scale(scale) : scale;

@@ -128,7 +128,12 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;                  // stream index mod 11
     int g = tt / gs, gend = (g + 1) * gs;                       // current group and its end
     uint32_t m = ms[d * gpt + g];
-    float sc = meta_scale(m), mnv = meta_min(m);
+    float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
+    float ws = 0.f, rcw = 0.f;  // Mixed3 narrow slots: wide scale and its reciprocal
+    if (bits == 3) {
+      ws = wide_scale(sc);
+      rcw = rcp_approx(ws);
+    }
     int k = 0;
     for (; k < cpw && tt < nt; ++k, ++tt) {
       if (tt == gend) {
@@ -137,8 +142,14 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
         m = ms[d * gpt + g];
         sc = meta_scale(m);
         mnv = meta_min(m);
+        rc = rcp_approx(sc);
+        if (bits == 3) {
+          ws = wide_scale(sc);
+          rcw = rcp_approx(ws);
+        }
       }
-      const uint32_t code = encode(xs[tt * D + d], sc, mnv, bits, bits == 3 && r11 == 10);
+      const bool nar = bits == 3 && r11 == 10;
+      const uint32_t code = encode_fast(xs[tt * D + d], sc, mnv, nar ? ws : sc, nar ? rcw : rc, nar ? 3 : q_max, bits, nar);
       word |= code << field_shift(bits, (uint32_t)k);
       if (++r11 == 11) r11 = 0;
     }
@@ -230,15 +241,21 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
     int g = d / gs, gend = min((g + 1) * gs, D);
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;
     uint32_t m = rr < nr ? ms[rr * gpt + g] : 0u;
-    float sc = meta_scale(m), mnv = meta_min(m);
+    float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
+    float ws = 0.f, rcw = 0.f;  // Mixed3 narrow slots: wide scale and its reciprocal
+    if (bits == 3) {
+      ws = wide_scale(sc);
+      rcw = rcp_approx(ws);
+    }
     size_t cached = ~(size_t)0;
     float sc2 = 0.f, mn2 = 0.f;
     for (int k = 0; k < cpw; ++k) {
       const size_t p = p0 + k;
       if (p >= n_total) break;
-      float xv;
+      const bool nar = bits == 3 && r11 == 10;
+      uint32_t code;
       if (p < s1) {
-        xv = xs[rr * Dp + d];
+        code = encode_fast(xs[rr * Dp + d], sc, mnv, nar ? ws : sc, nar ? rcw : rc, nar ? 3 : q_max, bits, nar);
       } else {  // codes of the next span (only at span ends): group meta once per group
         const size_t row = p / D;
         const int dd = (int)(p % D);
@@ -256,11 +273,9 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
           mn2 = meta_min(m2);
           cached = grp;
         }
-        sc = sc2;
-        mnv = mn2;
-        xv = gload(x, p);
+        code = encode(gload(x, p), sc2, mn2, bits, nar);
       }
-      word |= encode(xv, sc, mnv, bits, bits == 3 && r11 == 10) << field_shift(bits, (uint32_t)k);
+      word |= code << field_shift(bits, (uint32_t)k);
       if (++r11 == 11) r11 = 0;
       if (++d == gend) {  // next channel group (or next row)
         if (d == D) {
@@ -273,11 +288,74 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
           m = ms[rr * gpt + g];
           sc = meta_scale(m);
           mnv = meta_min(m);
+          rc = rcp_approx(sc);
+          if (bits == 3) {
+            ws = wide_scale(sc);
+            rcw = rcp_approx(ws);
+          }
         }
       }
     }
     words[w] = word;
   }
+}
+
+// ---- Values, uniform 1/2/4-bit words inside whole groups --------------------------------
+// When D % gs == 0 and a word's codes (32 / b channels) never leave their group, every word
+// is independent: one thread per output word loads its 32/b inputs (16-byte vectors,
+// consecutive threads -> consecutive bytes), the L = gs * b / 32 threads of a group reduce
+// min/max with L-lane butterflies, and the word is encoded with the group's meta in
+// registers. No shared memory, no run bookkeeping. The reference's sequential min/max
+// (mn = v < mn ? v : mn from the first element, quant.hpp:93-98 callers) is reproduced
+// exactly: lanes fold their values skipping NaN, segments combine in order keeping the
+// earlier of equal values, and a NaN first element makes the result NaN.
+__device__ __forceinline__ float fold_min(float a, float b) { return (isnan(a) || b < a) ? b : a; }
+__device__ __forceinline__ float fold_max(float a, float b) { return (isnan(a) || b > a) ? b : a; }
+
+template <typename T, int N>
+__device__ __forceinline__ void load_n(const T* p, float (&o)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; i += Vec<T>::N) Vec<T>::load(p + i, o + i);
+}
+
+template <typename T, int BITS>
+__global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T* __restrict__ x, size_t nw, int L,
+                                                                         uint32_t* __restrict__ words,
+                                                                         uint32_t* __restrict__ meta) {
+  constexpr int CPW = 32 / BITS;
+  static_assert(CPW % Vec<T>::N == 0, "word = whole input vectors");
+  const size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool ok = w < nw;  // groups are whole L-lane blocks: idle lanes form whole blocks
+  float v[CPW];
+  if (ok) load_n<T, CPW>(x + w * CPW, v);
+  else {
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) v[i] = 0.f;
+  }
+  float mn = NAN, mx = NAN;
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    mn = fold_min(mn, v[i]);
+    mx = fold_max(mx, v[i]);
+  }
+  for (int o = 1; o < L; o <<= 1) {
+    const float omn = __shfl_xor_sync(0xffffffffu, mn, o), omx = __shfl_xor_sync(0xffffffffu, mx, o);
+    const bool hi = lane & o;  // the other lane holds the earlier segment
+    mn = hi ? fold_min(omn, mn) : fold_min(mn, omn);
+    mx = hi ? fold_max(omx, mx) : fold_max(mx, omx);
+  }
+  const int lead = lane & ~(L - 1);
+  if (__shfl_sync(0xffffffffu, isnan(v[0]) ? 1 : 0, lead)) mn = mx = NAN;  // NaN first element
+  constexpr int q_max = BITS == 1 ? 1 : BITS == 2 ? 3 : 15;
+  const uint32_t m = make_meta(mn, mx, q_max);
+  if (!ok) return;
+  if (lane == lead) meta[w / L] = m;
+  const float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
+  uint32_t word = 0;
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) word |= encode_fast(v[i], sc, mnv, sc, rc, q_max, BITS, false) << (BITS * i);
+  words[w] = word;
 }
 
 // ---- dequantize (QuantizedGroups::value_at for every element) ----------------------------
@@ -394,6 +472,25 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
       else go(quantize_key_kernel<__half, 4>, xh);
     }
     after_launch("quantize_key_kernel");
+  } else if (bits != 3 && vec && D % gs == 0 && gs % (32 / bits) == 0 && gs / (32 / bits) <= 32 &&
+             ((gs / (32 / bits)) & (gs / (32 / bits) - 1)) == 0) {
+    // whole-group words: one thread per word (the common KVmix shapes: gs 32/64/128)
+    const int cpw = 32 / bits, L = gs / cpw;
+    const size_t nw = n / cpw;
+    const unsigned grid = (unsigned)((nw + kQThreads - 1) / kQThreads);
+    const float* xf = static_cast<const float*>(x);
+    const __half* xh = static_cast<const __half*>(x);
+#define KVB_QVW(TT, XP)                                                                             \
+    if (bits == 1) quantize_value_words_kernel<TT, 1><<<grid, kQThreads, 0, st>>>(XP, nw, L, words, m32); \
+    else if (bits == 2) quantize_value_words_kernel<TT, 2><<<grid, kQThreads, 0, st>>>(XP, nw, L, words, m32); \
+    else quantize_value_words_kernel<TT, 4><<<grid, kQThreads, 0, st>>>(XP, nw, L, words, m32);
+    if (dt == KVMIX_F32) {
+      KVB_QVW(float, xf)
+    } else {
+      KVB_QVW(__half, xh)
+    }
+#undef KVB_QVW
+    after_launch("quantize_value_words_kernel");
   } else {
     const int gpt = (D + gs - 1) / gs;
     int R = std::max(1, 8192 / std::max(D, 1));

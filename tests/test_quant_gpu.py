@@ -74,6 +74,24 @@ def test_quantize_edge_values(cuda):
             assert np.array_equal(_u16(qg.meta), m), (bits, key)
 
 
+@pytest.mark.parametrize("gs", [8, 32, 128])
+def test_quantize_tie_dense(cuda, gs):
+    """Inputs on a 1/8 grid: (x - min) / scale lands exactly on, or one rounding away from,
+    half-integers for a large share of the codes -- the quantizers' reciprocal fast path
+    must hand every such code to the exact IEEE-division path (half away from zero)."""
+    rng = np.random.default_rng(11 + gs)
+    x = (rng.integers(-16, 17, size=(2, 3, 256, 128)) / 8.0).astype(np.float32)
+    x[0, 0, :, :7] = rng.integers(0, 4, size=(256, 7)) * 0.5 - 0.75  # 4 levels: ties for 2/3 bits
+    x[1, 2, 3, :] = np.float32(1.0) + np.float32(2.0 ** -20) * rng.integers(-3, 4, size=128)  # near-constant
+    for bits in (2, 3, 4):
+        for key in (True, False):
+            w, m = O.quantize(x, bits, gs, key)
+            f = K.quantize_key_tensor if key else K.quantize_value_tensor
+            qg = f(torch.from_numpy(x).cuda(), K.QuantSpec(bits, K.Grouping(0 if key else 1), gs))
+            assert np.array_equal(_u32(qg.codes.words), w), (bits, key)
+            assert np.array_equal(_u16(qg.meta), m), (bits, key)
+
+
 def test_known_words(cuda):
     # test_bitpack.cpp:77-96 / :133-142
     assert K.pack_uniform([0] * 16, 2).words_u32().tolist() == [0]
