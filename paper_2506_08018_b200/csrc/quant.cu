@@ -333,17 +333,35 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
 #pragma unroll
     for (int i = 0; i < CPW; ++i) v[i] = 0.f;
   }
-  float mn = NAN, mx = NAN;
+  // fminf/fmaxf skip NaN like the fold; they differ from it only in the sign of a zero
+  // extremum (the fold keeps the first of -0 / +0), so groups whose min or max is zero redo
+  // the ordered fold
+  float mn = v[0], mx = v[0];
 #pragma unroll
-  for (int i = 0; i < CPW; ++i) {
-    mn = fold_min(mn, v[i]);
-    mx = fold_max(mx, v[i]);
+  for (int i = 1; i < CPW; ++i) {
+    mn = fminf(mn, v[i]);
+    mx = fmaxf(mx, v[i]);
   }
   for (int o = 1; o < L; o <<= 1) {
-    const float omn = __shfl_xor_sync(0xffffffffu, mn, o), omx = __shfl_xor_sync(0xffffffffu, mx, o);
-    const bool hi = lane & o;  // the other lane holds the earlier segment
-    mn = hi ? fold_min(omn, mn) : fold_min(mn, omn);
-    mx = hi ? fold_max(omx, mx) : fold_max(mx, omx);
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (__any_sync(0xffffffffu, mn == 0.f || mx == 0.f)) {  // (every group of the warp redoes:
+    mn = NAN;                                               //  same values where no zero)
+    mx = NAN;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+      mn = fold_min(mn, v[i]);
+      mx = fold_max(mx, v[i]);
+    }
+    for (int o = 1; o < L; o <<= 1) {
+      const float omn = __shfl_xor_sync(0xffffffffu, mn, o), omx = __shfl_xor_sync(0xffffffffu, mx, o);
+      const bool hi = lane & o;  // the other lane holds the earlier segment
+      const float fmn = hi ? fold_min(omn, mn) : fold_min(mn, omn);
+      const float fmx = hi ? fold_max(omx, mx) : fold_max(mx, omx);
+      mn = fmn;
+      mx = fmx;
+    }
   }
   const int lead = lane & ~(L - 1);
   if (__shfl_sync(0xffffffffu, isnan(v[0]) ? 1 : 0, lead)) mn = mx = NAN;  // NaN first element
@@ -352,9 +370,34 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
   if (!ok) return;
   if (lane == lead) meta[w / L] = m;
   const float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
-  uint32_t word = 0;
+  // branch-free encode_fast: codes whose va lies near a half-integer (or is NaN / huge)
+  // are flagged and redone by the exact encode() afterwards (rare)
+  constexpr float kTie = 0x1p-14f;
+  uint32_t word = 0, slow = 0;
 #pragma unroll
-  for (int i = 0; i < CPW; ++i) word |= encode_fast(v[i], sc, mnv, sc, rc, q_max, BITS, false) << (BITS * i);
+  for (int i = 0; i < CPW; ++i) {
+    const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
+    const float r = floorf(va + 0.5f);
+    const float f = va + 0.5f - r;
+    const bool tie = fabsf(f - 0.5f) > 0.5f - kTie;                          // near an integer t
+    const bool inr = fabsf(va - 0.5f * q_max) <= 0.5f * q_max - 0.5f + kTie;  // not clamped
+    const bool bad = !(fabsf(va) < 0x1p62f);                                  // NaN, inf, huge
+    slow |= (uint32_t)((inr && tie) || bad) << i;
+    word |= (uint32_t)fminf(fmaxf(r, 0.f), (float)q_max) << (BITS * i);
+  }
+  if (sc == 0.0f) {
+    word = 0;
+    slow = 0;
+  }
+  while (slow) {
+    const int i = __ffs(slow) - 1;
+    slow &= slow - 1;
+    float xi = v[0];
+#pragma unroll
+    for (int k = 1; k < CPW; ++k)
+      if (k == i) xi = v[k];
+    word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(xi, sc, mnv, BITS, false) << (BITS * i));
+  }
   words[w] = word;
 }
 

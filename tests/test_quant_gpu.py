@@ -83,6 +83,11 @@ def test_quantize_tie_dense(cuda, gs):
     x = (rng.integers(-16, 17, size=(2, 3, 256, 128)) / 8.0).astype(np.float32)
     x[0, 0, :, :7] = rng.integers(0, 4, size=(256, 7)) * 0.5 - 0.75  # 4 levels: ties for 2/3 bits
     x[1, 2, 3, :] = np.float32(1.0) + np.float32(2.0 ** -20) * rng.integers(-3, 4, size=128)  # near-constant
+    # zero extremes of both signs: the reference keeps the FIRST of -0 / +0
+    x[1, 0, 5, :] = np.abs(x[1, 0, 5, :]); x[1, 0, 5, 0::4] = 0.0; x[1, 0, 5, 1::4] = -0.0
+    x[1, 0, 6, :] = np.abs(x[1, 0, 6, :]); x[1, 0, 6, 0::4] = -0.0; x[1, 0, 6, 2::4] = 0.0
+    x[1, 0, 7, :] = -np.abs(x[1, 0, 7, :]); x[1, 0, 7, 3::8] = -0.0; x[1, 0, 7, 5::8] = 0.0
+    x[1, 1, :, 4] = np.abs(x[1, 1, :, 4]); x[1, 1, 0::3, 4] = -0.0; x[1, 1, 1::3, 4] = 0.0
     for bits in (2, 3, 4):
         for key in (True, False):
             w, m = O.quantize(x, bits, gs, key)
