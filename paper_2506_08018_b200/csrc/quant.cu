@@ -60,6 +60,38 @@ struct Vec<float> {
   }
 };
 
+// One uniform 1/2/4-bit word of CPW codes sharing a group's (scale, min), bit-exact with
+// encode(): branch-free reciprocal path; codes whose va lies near a half-integer (or is NaN
+// or huge) are flagged and redone by the exact encode() afterwards (rare).
+template <int BITS, int CPW>
+__device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc, float mnv, int q_max) {
+  constexpr float kTie = 0x1p-14f;
+  const float rc = rcp_approx(sc);
+  uint32_t word = 0, slow = 0;
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
+    const float r = floorf(va + 0.5f);
+    const float f = va + 0.5f - r;
+    const bool tie = fabsf(f - 0.5f) > 0.5f - kTie;                          // near an integer t
+    const bool inr = fabsf(va - 0.5f * q_max) <= 0.5f * q_max - 0.5f + kTie;  // not clamped
+    const bool bad = !(fabsf(va) < 0x1p62f);                                  // NaN, inf, huge
+    slow |= (uint32_t)((inr && tie) || bad) << i;
+    word |= (uint32_t)fminf(fmaxf(r, 0.f), (float)q_max) << (BITS * i);
+  }
+  if (sc == 0.0f) return 0u;
+  while (slow) {
+    const int i = __ffs(slow) - 1;
+    slow &= slow - 1;
+    float xi = v[0];
+#pragma unroll
+    for (int k = 1; k < CPW; ++k)
+      if (k == i) xi = v[k];
+    word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(xi, sc, mnv, BITS, false) << (BITS * i));
+  }
+  return word;
+}
+
 // ---- Keys -------------------------------------------------------------------------------
 // x: [B,H,T,D]; words/meta in reference order. Tile: n tokens (multiple of gs), all D.
 template <typename T, int BITS>
@@ -108,6 +140,22 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   }
   __syncthreads();
 
+  if constexpr (BITS != 3) {
+    constexpr int CPW = 32 / BITS;
+    if (gs % CPW == 0) {  // whole-group words (T % gs == 0): one meta per word, no run ends
+      const int nwr = nt / CPW;
+      for (int i = threadIdx.x; i < D * nwr; i += blockDim.x) {
+        const int d = i % D, j = i / D;  // a warp reads 32 consecutive channels of a token row
+        float v[CPW];
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) v[k] = xs[(j * CPW + k) * D + d];
+        const uint32_t m = ms[d * gpt + (j * CPW) / gs];
+        const size_t w = (((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j;
+        words[w] = encode_word<BITS, CPW>(v, meta_scale(m), meta_min(m), q_max);
+      }
+      return;
+    }
+  }
   const int cpw = codes_per_word(bits);
   // every thread emits words: thread i -> channel d = i % D (a warp reads 32 consecutive
   // channels of one token row: conflict-free), word j = i / D of that channel's run. A
@@ -370,34 +418,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
   if (!ok) return;
   if (lane == lead) meta[w / L] = m;
   const float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
-  // branch-free encode_fast: codes whose va lies near a half-integer (or is NaN / huge)
-  // are flagged and redone by the exact encode() afterwards (rare)
-  constexpr float kTie = 0x1p-14f;
-  uint32_t word = 0, slow = 0;
-#pragma unroll
-  for (int i = 0; i < CPW; ++i) {
-    const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
-    const float r = floorf(va + 0.5f);
-    const float f = va + 0.5f - r;
-    const bool tie = fabsf(f - 0.5f) > 0.5f - kTie;                          // near an integer t
-    const bool inr = fabsf(va - 0.5f * q_max) <= 0.5f * q_max - 0.5f + kTie;  // not clamped
-    const bool bad = !(fabsf(va) < 0x1p62f);                                  // NaN, inf, huge
-    slow |= (uint32_t)((inr && tie) || bad) << i;
-    word |= (uint32_t)fminf(fmaxf(r, 0.f), (float)q_max) << (BITS * i);
-  }
-  if (sc == 0.0f) {
-    word = 0;
-    slow = 0;
-  }
-  while (slow) {
-    const int i = __ffs(slow) - 1;
-    slow &= slow - 1;
-    float xi = v[0];
-#pragma unroll
-    for (int k = 1; k < CPW; ++k)
-      if (k == i) xi = v[k];
-    word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(xi, sc, mnv, BITS, false) << (BITS * i));
-  }
+  const uint32_t word = encode_word<BITS, CPW>(v, sc, mnv, q_max);
   words[w] = word;
 }
 
