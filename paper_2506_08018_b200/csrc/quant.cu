@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
                                                                  size_t n_total) {
   constexpr int bits = BITS;
   (void)bits_rt;
-  extern __shared__ float smem[];
-  float* xs = smem;                                   // [n][D]
-  uint32_t* ms = reinterpret_cast<uint32_t*>(xs + (size_t)n * D);  // [D][n/gs]
+  extern __shared__ __align__(16) uint8_t qsm[];
+  T* xs = reinterpret_cast<T*>(qsm);  // [n][D] in the input type (fp16 staging: 6 CTAs/SM)
+  uint32_t* ms = reinterpret_cast<uint32_t*>(qsm + ((size_t)n * D * sizeof(T) + 15) / 16 * 16);  // [D][n/gs]
   const int bh = blockIdx.y;
   const int t0 = blockIdx.x * n;
   const int nt = min(n, T_ - t0);  // always a multiple of gs (T % gs == 0)
@@ -113,23 +113,19 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   const int q_max = q_max_for_bits(bits);
   const T* src = x + ((size_t)bh * T_ + t0) * D;
 
-  if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked)
-    for (int i = threadIdx.x; i < nt * D / Vec<T>::N; i += blockDim.x) {
-      float v[Vec<T>::N];
-      Vec<T>::load(src + (size_t)i * Vec<T>::N, v);
-#pragma unroll
-      for (int e = 0; e < Vec<T>::N; ++e) xs[i * Vec<T>::N + e] = v[e];
-    }
+  if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked): raw 16-byte copies
+    for (int i = threadIdx.x; i < nt * D / Vec<T>::N; i += blockDim.x)
+      reinterpret_cast<uint4*>(xs)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
   } else {
-    for (int i = threadIdx.x; i < nt * D; i += blockDim.x) xs[i] = gload(src, i);
+    for (int i = threadIdx.x; i < nt * D; i += blockDim.x) xs[i] = src[i];
   }
   __syncthreads();
 
   for (int i = threadIdx.x; i < D * gpt; i += blockDim.x) {
     const int d = i % D, g = i / D;  // d fastest: conflict-free smem columns
-    float mn = xs[(g * gs) * D + d], mx = mn;
+    float mn = ld_f(&xs[(g * gs) * D + d]), mx = mn;
     for (int j = 1; j < gs; ++j) {
-      const float v = xs[(g * gs + j) * D + d];
+      const float v = ld_f(&xs[(g * gs + j) * D + d]);
       mn = v < mn ? v : mn;
       mx = v > mx ? v : mx;
     }
@@ -148,7 +144,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
         const int d = i % D, j = i / D;  // a warp reads 32 consecutive channels of a token row
         float v[CPW];
 #pragma unroll
-        for (int k = 0; k < CPW; ++k) v[k] = xs[(j * CPW + k) * D + d];
+        for (int k = 0; k < CPW; ++k) v[k] = ld_f(&xs[(j * CPW + k) * D + d]);
         const uint32_t m = ms[d * gpt + (j * CPW) / gs];
         const size_t w = (((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j;
         words[w] = encode_word<BITS, CPW>(v, meta_scale(m), meta_min(m), q_max);
@@ -197,7 +193,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
         }
       }
       const bool nar = bits == 3 && r11 == 10;
-      const uint32_t code = encode_fast(xs[tt * D + d], sc, mnv, nar ? ws : sc, nar ? rcw : rc, nar ? 3 : q_max, bits, nar);
+      const uint32_t code = encode_fast(ld_f(&xs[tt * D + d]), sc, mnv, nar ? ws : sc, nar ? rcw : rc, nar ? 3 : q_max, bits, nar);
       word |= code << field_shift(bits, (uint32_t)k);
       if (++r11 == 11) r11 = 0;
     }
@@ -512,7 +508,8 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
   if (grouping == KVMIX_PER_CHANNEL_KEY) {
     // tile of k groups of gs tokens: aim for ~128 tokens, bounded by shared memory
     int k = std::max(1, 128 / gs);
-    auto smem_of = [&](int kk) { return (size_t)kk * gs * D * 4 + (size_t)D * kk * 4; };
+    const size_t esz = dt == KVMIX_F16 ? 2 : 4;  // staged in the input type
+    auto smem_of = [&](int kk) { return ((size_t)kk * gs * D * esz + 15) / 16 * 16 + (size_t)D * kk * 4; };
     while (k > 1 && smem_of(k) > (size_t)max_smem) --k;
     if (smem_of(k) > (size_t)227 * 1024) invalid("quantize: group_size * head_dim too large for one tile");
     const int n_tok = k * gs;
