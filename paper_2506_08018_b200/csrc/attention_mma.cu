@@ -268,7 +268,8 @@ struct MmaParams {
 // are small to keep the stream-K ranges balanced (KVMIX_TAIL_UNIT overrides, for tuning).
 constexpr int kTailUnit = 1;
 constexpr int kGroupCost = 1;
-constexpr int kMaxPasses = 8;  // row passes per launch  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
+constexpr int kMaxPasses = 8;  // row passes per launch
+constexpr int kMinCost = 8;    // minimum cost units per warp (KVMIX_MIN_COST overrides)  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
 
 // first unit whose start cost is >= c (units: Gf groups of cost Qc, then window units of 1)
 __device__ __forceinline__ int unit_at_cost(const MmaParams& p, int64_t c) {
@@ -1335,7 +1336,12 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   // never more warps than units so every range is non-empty
   // (the npass warps of a unit range count once per pass)
   const int64_t wave = (int64_t)std::max(1, occ) * num_sms() * kMmaWarps;
-  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(p.N, wave / p.npass));
+  // small problems: at least kMinCost cost units per warp (a warp's prologue and the merge
+  // of a head split over many warps cost more than a few groups)
+  int64_t min_cost = kMinCost;
+  if (const char* e = getenv("KVMIX_MIN_COST")) min_cost = std::max(1, atoi(e));
+  const int64_t w_cap = std::max<int64_t>(1, p.Nc / min_cost);
+  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(p.N, wave / p.npass), w_cap));
   // partial slots x * pslots + w + bh (w + bh < W + BH): scratch depends on (B, H, rows, D,
   // SM count) only
   p.pslots = (int)(wave + BH);
