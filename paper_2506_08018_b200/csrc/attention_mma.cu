@@ -267,9 +267,9 @@ struct MmaParams {
 // token (lane-parallel dequantization of partially aged Values, no TMA staging), so units
 // are small to keep the stream-K ranges balanced (KVMIX_TAIL_UNIT overrides, for tuning).
 constexpr int kTailUnit = 1;
-constexpr int kGroupCost = 1;
+constexpr int kGroupCost = 1;  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
 constexpr int kMaxPasses = 8;  // row passes per launch
-constexpr int kMinCost = 8;    // minimum cost units per warp (KVMIX_MIN_COST overrides)  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
+constexpr int kMinCost = 8;    // minimum cost units per warp (KVMIX_MIN_COST overrides)
 
 // first unit whose start cost is >= c (units: Gf groups of cost Qc, then window units of 1)
 __device__ __forceinline__ int unit_at_cost(const MmaParams& p, int64_t c) {
