@@ -271,9 +271,13 @@ int attend_splits(int BH) {
   return std::max(1, std::min(64, (4 * sms + BH - 1) / std::max(1, BH)));
 }
 
-void check_attend(const kvmix_cache* c, int q_heads, int t) {
+static void check_query_shape(const kvmix_cache* c, int q_heads, int t) {
   if (t < 1) invalid("attention: need at least one query row");
   if (q_heads < c->H || q_heads % c->H != 0) invalid("attention: query shape does not match cache");
+}
+
+void check_attend(const kvmix_cache* c, int q_heads, int t) {
+  check_query_shape(c, q_heads, t);
   if (c->total() < 1) invalid("softmax over an empty row");
 }
 
@@ -361,7 +365,8 @@ void append_attend(kvmix_cache* c, const void* k, const void* v, kvmix_dtype kv_
   if (c->total() + t > c->cap || t < 1) {
     cache_append(c, k, v, kv_dt, t, st);  // raises the reference's errors
   } else {
-    check_attend(c, Hq, tq);  // shape errors before any state changes
+    check_query_shape(c, Hq, tq);  // shape errors before any state changes (the append makes
+                                   // the cache non-empty)
     DecodeAppend da;
     if (cache_append_decode_plan(c, k, v, kv_dt, t, &da)) {
       if (attend_mma(c, q, q_dt, Hq, tq, out, checksum, ws, st, &da)) return;

@@ -295,6 +295,25 @@ def test_append_attend_matches_separate_calls(cuda, kb, vb, D, G, tail):
     assert n_fused >= 60  # steady-state steps ran as one launch
 
 
+def test_append_attend_from_an_empty_cache(cuda):
+    """The first decode step of an empty cache: the append makes it non-empty, so
+    append_attend must not raise the empty-softmax error (attend alone does)."""
+    k = torch.from_numpy(O.random_h16(90, (1, 2, 1, 64))).cuda()
+    v = torch.from_numpy(O.random_h16(91, (1, 2, 1, 64))).cuda()
+    q = torch.from_numpy(O.random_h16(92, (1, 2, 1, 64))).cuda()
+    for kb, vb, r in ((2, 2, 0.1), (4, 4, 1.0)):
+        mk = lambda: K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), 1, 2, 64, capacity_tokens=64)
+        c, sep = mk(), mk()
+        with pytest.raises(K.KvmixInvalidArgument):
+            K.attend(q, c)
+        out = K.append_attend(c, k, v, q).output
+        sep.append(k, v)
+        assert torch.equal(out, K.attend(q, sep, checksum=False).output)
+        assert c.total_tokens() == 1
+        if r == 1.0:  # one full-precision token: softmax weight 1, out == v
+            assert torch.equal(out, v.float())
+
+
 @pytest.mark.parametrize("kb,vb,gs,rk,rv,tail", [(2, 2, 32, 0.1, 0.1, torch.float32), (3, 4, 32, 0.2, 0.2, torch.float16),
                                                  (2, 4, 64, 0.1, 0.1, torch.float16), (4, 2, 32, 0.1, 0.3, torch.float32)])
 def test_attend_window_blocks_through_a_cycle(cuda, kb, vb, gs, rk, rv, tail):
