@@ -418,6 +418,97 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
   words[w] = word;
 }
 
+// ---- Values, Mixed3 (3-bit), D % gs == 0 and gs % 32 == 0 ------------------------------
+// A chunk of 11*gs stream elements holds exactly gs Mixed3 words (11 codes each) and 11
+// groups, both aligned. One warp per chunk: the chunk is staged in shared memory (16-byte
+// loads), lanes 0..10 fold one group each in stream order (the reference's sequential
+// min/max, exactly), and every lane emits gs/32 words; a lane's 11 codes sit at stride 11
+// in shared memory (odd: conflict-free). Slot 10 of every word is the narrow slot.
+constexpr int kM3Warps = 8;
+
+template <typename T, int GS>
+__global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const T* __restrict__ x, size_t n,
+                                                                         uint32_t* __restrict__ words,
+                                                                         uint32_t* __restrict__ meta) {
+  constexpr int gs = GS;
+  extern __shared__ __align__(16) float m3s[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int CE = 11 * gs;  // chunk elements
+  float* xs = m3s + (size_t)warp * (CE + 4 * 11);
+  float* gm = xs + CE;  // [11] scale, [11] min, [11] rcp(scale), [11] rcp(wide scale)
+  const size_t chunk = (size_t)blockIdx.x * kM3Warps + warp;
+  const size_t e0 = chunk * CE;
+  if (e0 >= n) return;
+  const int ne = (int)min((size_t)CE, n - e0);  // a multiple of gs (n % gs == 0)
+  // stage (fp32 in shared memory)
+  if (ne == CE && (reinterpret_cast<uintptr_t>(x + e0) & 15) == 0) {
+    for (int i = lane; i < CE / Vec<T>::N; i += 32) {
+      float v[Vec<T>::N];
+      Vec<T>::load(x + e0 + (size_t)i * Vec<T>::N, v);
+#pragma unroll
+      for (int k = 0; k < Vec<T>::N; ++k) xs[i * Vec<T>::N + k] = v[k];
+    }
+  } else {
+    for (int i = lane; i < ne; i += 32) xs[i] = ld_f(x + e0 + i);
+  }
+  __syncwarp();
+  const int ng = ne / gs;
+  if (lane < ng) {
+    const float* g = xs + lane * gs;
+    float mn = g[0], mx = mn;
+    for (int j = 1; j < gs; ++j) {
+      const float v = g[j];
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+    const uint32_t m = make_meta(mn, mx, 7);
+    meta[chunk * 11 + lane] = m;
+    const float sc = meta_scale(m);
+    gm[lane] = sc;
+    gm[11 + lane] = meta_min(m);
+    gm[22 + lane] = rcp_approx(sc);
+    gm[33 + lane] = rcp_approx(wide_scale(sc));
+  }
+  __syncwarp();
+  const size_t nw = (n + 10) / 11;
+#pragma unroll
+  for (int i = 0; i < gs / 32; ++i) {
+    const int wl = lane + 32 * i;
+    const size_t w = chunk * gs + wl;
+    if (w >= nw) break;
+    uint32_t word = 0;
+    if (11 * wl + 11 <= ne) {  // every chunk but the stream's last
+      // a word spans at most two groups: j0 for its first codes, j0 + 1 after the boundary
+      const int j0 = (11 * wl) / gs, kb = (j0 + 1) * gs - 11 * wl;  // first code of group j0 + 1
+      const float s0 = gm[j0], m0 = gm[11 + j0], r0 = gm[22 + j0];
+      const float s1 = kb < 11 ? gm[j0 + 1] : s0, m1 = kb < 11 ? gm[11 + j0 + 1] : m0;
+      const float r1 = kb < 11 ? gm[22 + j0 + 1] : r0;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const bool hi = k >= kb;
+        word |= encode_fast(xs[11 * wl + k], hi ? s1 : s0, hi ? m1 : m0, hi ? s1 : s0, hi ? r1 : r0, 7, 3, false) << (3 * k);
+      }
+      const int j10 = kb <= 10 ? j0 + 1 : j0;  // the narrow slot (k = 10)
+      const float sn = gm[j10];
+      word |= encode_fast(xs[11 * wl + 10], sn, gm[11 + j10], wide_scale(sn), gm[33 + j10], 3, 3, true) << 30;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 11; ++k) {
+        const int e = 11 * wl + k;
+        if (e < ne) {
+          const int j = e / gs;
+          const float sc = gm[j], mnv = gm[11 + j];
+          const bool nar = k == 10;
+          const uint32_t code = encode_fast(xs[e], sc, mnv, nar ? wide_scale(sc) : sc, gm[(nar ? 33 : 22) + j],
+                                            nar ? 3 : 7, 3, nar);
+          word |= code << (nar ? 30u : 3u * k);
+        }
+      }
+    }
+    words[w] = word;
+  }
+}
+
 // ---- dequantize (QuantizedGroups::value_at for every element) ----------------------------
 __global__ void dequantize_kernel(int grouping, const uint32_t* __restrict__ words,
                                   const uint32_t* __restrict__ meta, int H, int T_, int D, int bits,
@@ -552,6 +643,27 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     }
 #undef KVB_QVW
     after_launch("quantize_value_words_kernel");
+  } else if (bits == 3 && D % gs == 0 && (gs == 32 || gs == 64 || gs == 128)) {
+    // Mixed3 chunks of 11 * gs elements, one warp each
+    const size_t chunks = (n + 11 * (size_t)gs - 1) / (11 * (size_t)gs);
+    const unsigned grid = (unsigned)((chunks + kM3Warps - 1) / kM3Warps);
+    const size_t smem = (size_t)kM3Warps * (11 * gs + 44) * 4;
+    auto go = [&](auto kern, const auto* xp) {
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      kern<<<grid, kM3Warps * 32, smem, st>>>(xp, n, words, m32);
+    };
+    const float* xf = static_cast<const float*>(x);
+    const __half* xh = static_cast<const __half*>(x);
+    if (dt == KVMIX_F32) {
+      if (gs == 32) go(quantize_value_m3_kernel<float, 32>, xf);
+      else if (gs == 64) go(quantize_value_m3_kernel<float, 64>, xf);
+      else go(quantize_value_m3_kernel<float, 128>, xf);
+    } else {
+      if (gs == 32) go(quantize_value_m3_kernel<__half, 32>, xh);
+      else if (gs == 64) go(quantize_value_m3_kernel<__half, 64>, xh);
+      else go(quantize_value_m3_kernel<__half, 128>, xh);
+    }
+    after_launch("quantize_value_m3_kernel");
   } else {
     const int gpt = (D + gs - 1) / gs;
     int R = std::max(1, 8192 / std::max(D, 1));
