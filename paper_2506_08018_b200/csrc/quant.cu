@@ -168,6 +168,26 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
     if (w >= w_end) continue;
     const size_t p0 = w * cpw;
     uint32_t word = 0;
+    if constexpr (BITS == 3) {
+      if (gs >= 11 && p0 + 11 <= s1) {  // interior Mixed3 word: <= two groups, slot 10 narrow
+        const int tt0 = (int)(p0 - s0);
+        const int j0 = tt0 / gs, kb = (j0 + 1) * gs - tt0;  // first code of group j0 + 1
+        const uint32_t ma = ms[d * gpt + j0], mb = kb < 11 ? ms[d * gpt + j0 + 1] : ma;
+        const float sa = meta_scale(ma), na = meta_min(ma), ra = rcp_approx(sa);
+        const float sb = meta_scale(mb), nb = meta_min(mb), rb = rcp_approx(sb);
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+          const bool hi = k >= kb;
+          word |= encode_fast(ld_f(&xs[(tt0 + k) * D + d]), hi ? sb : sa, hi ? nb : na, hi ? sb : sa, hi ? rb : ra, 7, 3,
+                              false) << (3 * k);
+        }
+        const float sn = kb <= 10 ? sb : sa, nn = kb <= 10 ? nb : na;
+        word |= encode_fast(ld_f(&xs[(tt0 + 10) * D + d]), sn, nn, wide_scale(sn), rcp_approx(wide_scale(sn)), 3, 3, true)
+                << 30;
+        words[w] = word;
+        continue;
+      }
+    }
     int tt = (int)(p0 - s0);                                    // token of the first code
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;                  // stream index mod 11
     int g = tt / gs, gend = (g + 1) * gs;                       // current group and its end
