@@ -118,7 +118,7 @@ def test_attend_gqa(cuda, G):
 @pytest.mark.parametrize("kb,vb,G,tq", [(3, 4, 2, 1), (4, 2, 4, 1), (2, 4, 1, 3), (2, 2, 4, 5), (3, 2, 2, 5), (4, 4, 8, 3)])
 def test_attend_multi_pass_rows(cuda, kb, vb, G, tq):
     """More than two query rows per KV head (GQA and/or several query tokens): row passes
-    (one row per pass for 3-bit Keys) inside one launch, up to 8 per launch (20 rows: two
+    (two rows per pass, 3-bit Keys included) inside one launch, up to 8 per launch (20 rows: two
     launches), a last pass with one row, checksums summed over the passes."""
     dev, ora = build(kb, vb, 0.2, 0.2, 32, 1, 4, 128, [900] + [1] * 12, seed=27)
     q = O.random_h16(28, (1, 4 * G, tq, 128), sigma=1.5)
