@@ -15,7 +15,10 @@ G = 1
 if os.environ.get("SHAPE"):
     B, H, G, CTX = (int(x) for x in os.environ["SHAPE"].split(","))
 torch.manual_seed(0)
-for kb, vb, r in ((2, 2, 0.1), (3, 4, 0.2)):
+TIERS = ((2, 2, 0.1), (3, 4, 0.2))
+if os.environ.get("TIERS"):  # e.g. TIERS=2:3:0.1,3:3:0.2
+    TIERS = tuple((int(a), int(b), float(r)) for a, b, r in (t.split(":") for t in os.environ["TIERS"].split(",")))
+for kb, vb, r in TIERS:
     c = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), B, H, D, capacity_tokens=CTX + 64, tail_dtype=torch.float16)
     c.append(torch.randn(B, H, CTX - 64, D, device="cuda", dtype=torch.float16),
              torch.randn(B, H, CTX - 64, D, device="cuda", dtype=torch.float16))
