@@ -16,9 +16,10 @@ B, H, D, CTX = 16, 32, 128, 8192
 G = 1
 if os.environ.get("SHAPE"):  # B,H,G,CTX (e.g. 8,8,4,32768: the Mistral-7B GQA config)
     B, H, G, CTX = (int(x) for x in os.environ["SHAPE"].split(","))
-tiers = [(2, 2, 0.1), (3, 4, 0.2)]
+ALL = [(2, 2, 0.1), (3, 4, 0.2), (2, 3, 0.1)]  # index 2: 3-bit Values (generic kernel)
+tiers = ALL[:2]
 if len(sys.argv) > 1:
-    tiers = [tiers[int(i)] for i in sys.argv[1].split(",")]
+    tiers = [ALL[int(i)] for i in sys.argv[1].split(",")]
 torch.manual_seed(0)
 for kb, vb, r in tiers:
     c = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), B, H, D, capacity_tokens=CTX + 64, tail_dtype=torch.float16)
