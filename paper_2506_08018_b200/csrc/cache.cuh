@@ -64,9 +64,10 @@ inline SideView view(const kvmix_cache::Side& s) {
 }
 
 // Word offsets into a side's tiles / meta (group-record layout above).
+// (32-bit index math: tokens per (b, kv-head) < 2^31, enforced at cache creation)
 __host__ __device__ inline size_t tile_index(const SideView& s, int bh, int64_t tile) {
-  const int64_t gi = tile / s.tpg;
-  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(tile - gi * s.tpg) * s.tile_words;
+  const unsigned t = (unsigned)tile, tp = (unsigned)s.tpg, gi = t / tp;
+  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(t - gi * tp) * s.tile_words;
 }
 // Key meta row of group grp (D words, one per channel)
 __host__ __device__ inline size_t kmeta_index(const SideView& s, int bh, int64_t grp) {
@@ -74,9 +75,8 @@ __host__ __device__ inline size_t kmeta_index(const SideView& s, int bh, int64_t
 }
 // Value meta row of token j (ceil(D/gs) words, one per channel group)
 __host__ __device__ inline size_t vmeta_index(const SideView& s, int bh, int64_t j) {
-  const int gs = s.tpg * 16;
-  const int64_t gi = j / gs;
-  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(j - gi * gs) * s.mrow;
+  const unsigned gs = (unsigned)s.tpg * 16u, jj = (unsigned)j, gi = jj / gs;
+  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(jj - gi * gs) * s.mrow;
 }
 
 template <typename TT>

@@ -164,6 +164,7 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
     if (cfg->group_size % 16 != 0)
       invalid("device cache: group_size must be a multiple of 16 (got " + std::to_string(cfg->group_size) + ")");
     if (capacity_tokens < 1) invalid("device cache: capacity_tokens must be positive");
+    if (capacity_tokens >= (int64_t)1 << 31) invalid("device cache: capacity_tokens must be below 2^31");
     if (tail_dtype != KVMIX_F32 && tail_dtype != KVMIX_F16) invalid("unsupported tail dtype");
     c = new kvmix_cache();
     c->cfg = *cfg;

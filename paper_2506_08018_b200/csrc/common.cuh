@@ -189,6 +189,8 @@ __host__ __device__ constexpr int tile_words(int D, int bits) {
 // per lane so a warp's 128-bit loads are contiguous)
 __host__ __device__ inline int plane_addr(int lane, int w, int wpl) {
   const int cw = wpl < 4 ? wpl : 4;
+  const int sh = cw == 4 ? 2 : cw == 2 ? 1 : cw == 1 ? 0 : -1;  // D in {64, 128}: shifts
+  if (sh >= 0) return ((w >> sh) << (5 + sh)) + (lane << sh) + (w & (cw - 1));
   return (w / cw) * (32 * cw) + lane * cw + (w % cw);
 }
 
