@@ -381,6 +381,12 @@ def main():
         if rank != 0:
             return 0
         threads = args.cpu_threads or os.cpu_count() or 1
+        warm = 0  # untimed warm-up samples (bounded: each one is seconds of CPU work)
+        tw = time.time()
+        while warm < args.warmup and time.time() - tw < 30:
+            if cpu_reference_sample(args.config, threads)[0] is None:
+                break
+            warm += 1
         t0 = time.time()
         times = []
         value = desc = cores = None
@@ -397,7 +403,7 @@ def main():
         L, B, H, Hq, D, ctx, high = CONFIGS[args.config]
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": len(times), "warmup": 0, "ms_per_step": B / value * 1e3, "higher_is_better": True,
+            "steps": len(times), "warmup": warm, "ms_per_step": B / value * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (reference CPU)", "data": "synthetic",
             "config": {"workload": args.config, "global_batch": B, "seq_len": ctx, "parallelism": "cpu"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": desc},
