@@ -7,23 +7,31 @@ the fused dequant attention for the step's query. Default workload = BASELINE.js
 configs[1]: Llama-2-7B (32 layers, 32 heads x 128), KVmix tiering (layers 0-5 K3/V4 r=0.2,
 6-31 K2/V2 r=0.1, gs 32), batch 16, ~8k context, synthetic KV on the binary16 grid.
 
-value  = tokens/s over all ranks (batch x steps / max-over-ranks device time), inputs
-         resident in HBM; the per-step cache (14 GB) is far larger than L2.
-e2e    = the same through the public API with pinned HOST buffers (H2D of q/k/v, D2H of
-         the attention output, every layer, every step, inside the timed region).
-roofline = the dominant kernel (attend_mma_kernel + its split-K combine, timed together
-         with CUDA events on the launch stream inside the timed steps): algorithmic bytes
-         (MemoryReport total bits / 8 + q + out) / launch time vs MEASURED_PEAKS hbm_gbs.
+value  = tokens/s over all ranks (global batch x steps / max-over-ranks device time),
+         inputs resident in HBM; the per-step cache (14 GB) is far larger than L2.
+e2e    = the same through the public API (DecodeStep: kvmix_append_attend_layers) with
+         pinned HOST buffers: H2D of q/k/v and D2H of every layer's attention output, every
+         step, inside the timed region.
+roofline = the dominant kernel (attend_mma_kernel, which also runs the 1-token append in
+         its prologue): algorithmic bytes (MemoryReport total bits / 8 + q + out) per launch
+         / launch time from CUDA events on the launch stream inside the timed steps, vs
+         MEASURED_PEAKS hbm_gbs. `step_frac` is the same over the whole step time.
 cpu_baseline = the UNMODIFIED reference (oracle/_ref) timed on this host's cores on a
-         bounded sample (one (layer, batch element) unit per tier), extrapolated.
-Multi-GPU (torchrun): weak scaling -- every rank holds the full batch of its own shard of
-(batch x kv-head) work (no data-path collective); max-over-ranks timing.
+         bounded sample (one (layer, batch rows) unit per tier), extrapolated.
+Multi-GPU (--gpus N, or under torchrun): the global batch is sharded batch x kv-head with
+         ShardPlan (no data-path collective); strong scaling for configs[1]/[2] (fixed global
+         batch), weak scaling for the configs[3] shard (B4 per GPU, as BASELINE.md 2 says).
+--check validates two sampled (layer, b, head) outputs of the last timed step against an
+         fp64 evaluation over the cache's bit-exact snapshot (outside the timed region).
+--config quant-sweep: BASELINE configs[4], the quantize/pack sweep (bits x group size,
+         Keys + Values, [16,32,4096,128] fp16 per GPU, weak scaling).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,18 +42,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode-attention tokens/s and achieved HBM GB/s (compressed bytes) at 1/2/4/8 B200"
+QMETRIC = "quantize/pack throughput (elements/s) and achieved HBM GB/s over 2/3/4 bits x gs 32/64/128"
 
 CONFIGS = {
-    # name: (layers, batch, kv_heads, q_heads, head_dim, context, high_layers)
-    "llama2-7b-8k": (32, 16, 32, 32, 128, 8192, 6),          # configs[1]
-    "layer-4k": (1, 1, 32, 32, 128, 4096, 0),                  # configs[0] shape
-    "mistral-7b-32k": (32, 8, 8, 32, 128, 32768, 6),          # configs[2]
-    # configs[3] is B32 sharded batch x KV-head over 8 GPUs: one rank's shard is B4 (weak
-    # scaling: every rank holds its own B4 shard, ~140 GB of HBM with the fp16 windows)
-    "llama2-13b-128k-shard": (40, 4, 40, 40, 128, 131072, 8),  # configs[3], per-GPU shard
+    # name: (layers, global batch, kv_heads, q_heads, head_dim, context, high layers, scaling)
+    "llama2-7b-8k": (32, 16, 32, 32, 128, 8192, 6, "strong"),           # configs[1]
+    "layer-4k": (1, 1, 32, 32, 128, 4096, 0, "strong"),                   # configs[0] shape
+    "mistral-7b-32k": (32, 8, 8, 32, 128, 32768, 6, "strong"),          # configs[2]
+    # configs[3] is B32 sharded batch x KV-head over 8 GPUs; it does not fit below ~4 GPUs,
+    # so every rank holds the 1/8 shard (B4, ~140 GB with the fp16 windows): weak scaling
+    "llama2-13b-128k-shard": (40, 4, 40, 40, 128, 131072, 8, "weak"),   # configs[3], per-GPU shard
 }
 CONFIG_INDEX = {"llama2-7b-8k": "configs[1]", "layer-4k": "configs[0]", "mistral-7b-32k": "configs[2]",
-                "llama2-13b-128k-shard": "configs[3] per-GPU shard (B32 / 8 ranks)"}
+                "llama2-13b-128k-shard": "configs[3] per-GPU shard (B32 / 8 ranks)", "quant-sweep": "configs[4]"}
 
 
 def parse():
@@ -54,9 +63,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="llama2-7b-8k", choices=list(CONFIGS))
+    ap.add_argument("--config", default="llama2-7b-8k", choices=list(CONFIGS) + ["quant-sweep"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     return ap.parse_args()
 
@@ -114,12 +124,22 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
 # ---------------------------------------------------------------------------------------
 # reference CPU arm (oracle/_ref: the unmodified reference compiled from its sources)
 # ---------------------------------------------------------------------------------------
 def cpu_reference_sample(cfg_name: str, threads: int):
-    """Times the reference's own append+attend on one (layer, batch element) unit per tier
-    at full context; returns (tokens/s extrapolated to the whole step, description)."""
+    """Times the reference's own append+attend on one (layer, batch rows) unit per tier at
+    full context; returns (tokens/s extrapolated to the whole step, description, cores).
+    The unit holds enough batch rows that the reference's OpenMP row loop
+    (attention.cpp:38-41, one row per (b, head, query)) has work for every thread."""
     import numpy as np
 
     import oracle as O
@@ -129,40 +149,74 @@ def cpu_reference_sample(cfg_name: str, threads: int):
     if threads > 0:
         R.ref_set_threads(threads)
     cores = R.ref_max_threads()
-    L, B, H, Hq, D, ctx, high = CONFIGS[cfg_name]
+    L, Bg, H, Hq, D, ctx, high, _ = CONFIGS[cfg_name]
     G = Hq // H
+    bu = max(1, min(Bg, -(-cores // H)))  # batch rows per unit: >= one row per thread
     tiers = [(3, 4, 0.2, high), (2, 2, 0.1, L - high)] if high else [(2, 2, 0.1, L)]
     t_units = {}
     rng = np.random.default_rng(0)
     for kb, vb, r, count in tiers:
         if count == 0:
             continue
-        cache = O.RefCache(kb, vb, r, r, 32, 1, H, D)
+        cache = O.RefCache(kb, vb, r, r, 32, bu, H, D)
         pre = ctx - 64
-        k = rng.standard_normal((1, H, pre, D), dtype=np.float32).astype(np.float16).astype(np.float32)
-        v = rng.standard_normal((1, H, pre, D), dtype=np.float32).astype(np.float16).astype(np.float32)
+        k = rng.standard_normal((bu, H, pre, D), dtype=np.float32).astype(np.float16).astype(np.float32)
+        v = rng.standard_normal((bu, H, pre, D), dtype=np.float32).astype(np.float16).astype(np.float32)
         cache.append(k, v)
+        del k, v
         for _ in range(64):
-            k1 = rng.standard_normal((1, H, 1, D), dtype=np.float32).astype(np.float16).astype(np.float32)
+            k1 = rng.standard_normal((bu, H, 1, D), dtype=np.float32).astype(np.float16).astype(np.float32)
             cache.append(k1, k1)
-        q = rng.standard_normal((1, H, G, D), dtype=np.float32).astype(np.float16).astype(np.float32)
+        q = rng.standard_normal((bu, H, G, D), dtype=np.float32).astype(np.float16).astype(np.float32)
         times = []
         for _ in range(3):
-            k1 = rng.standard_normal((1, H, 1, D), dtype=np.float32).astype(np.float16).astype(np.float32)
+            k1 = rng.standard_normal((bu, H, 1, D), dtype=np.float32).astype(np.float16).astype(np.float32)
             t0 = time.perf_counter()
             cache.append(k1, k1)
             cache.attend(q)  # GQA: the reference's equivalent is t = G query rows per KV head
             times.append(time.perf_counter() - t0)
         t_units[(kb, vb)] = (min(times), count)
-    t_step = sum(t * n for t, n in t_units.values()) * B
-    desc = (f"reference append(1 token)+attend timed on one (layer, batch element) unit per tier "
-            f"({', '.join(f'K{kb}V{vb}: {t*1e3:.1f} ms' for (kb, vb), (t, _) in t_units.items())}) at "
-            f"{ctx} context, {H} KV heads, best of 3, extrapolated x layers x batch {B}")
-    return B / t_step, desc, cores
+    t_step = sum(t * n for t, n in t_units.values()) * Bg / bu
+    desc = (f"reference append(1 token)+attend timed on one (layer, {bu} batch row{'s' if bu > 1 else ''}) unit per "
+            f"tier ({', '.join(f'K{kb}V{vb}: {t*1e3:.1f} ms' for (kb, vb), (t, _) in t_units.items())}) at {ctx} "
+            f"context, {H} KV heads x {G} query rows, best of 3, extrapolated x {L} layers x batch {Bg}")
+    return Bg / t_step, desc, cores
+
+
+def cpu_quant_sample(threads: int):
+    """The reference's quantize_key_tensor + quantize_value_tensor (quant.cpp:102-124) on
+    [1,32,4096,128] (one of the 16 batch rows of a configs[4] tensor) for one setting per bit
+    width at gs 32; returns (elements/s, description, cores)."""
+    import numpy as np
+
+    import oracle as O
+    R = O.ref()
+    if R is None:
+        return None, "oracle/_ref not built", 0
+    if threads > 0:
+        R.ref_set_threads(threads)
+    cores = R.ref_max_threads()
+    import ctypes as C
+    x = np.random.default_rng(0).standard_normal((1, 32, 4096, 128), dtype=np.float32).astype(np.float16).astype(np.float32)
+    tot_t, tot_n, parts = 0.0, 0, []
+    for bits in (2, 3, 4):
+        nw = O.words_for(x.size, bits)
+        bufs = [(np.zeros(nw, np.uint32), np.zeros(2 * (x.size // 32), np.uint16)) for _ in range(2)]
+        cnt = C.c_uint64(0)
+        t0 = time.perf_counter()
+        for key, (w, m) in zip((0, 1), bufs):  # one reference call per side (outputs preallocated)
+            if R.ref_quantize(key, x, *x.shape, bits, 32, w.ctypes.data, m.ctypes.data, C.byref(cnt), C.byref(cnt)):
+                raise RuntimeError(R.ref_last_error().decode())
+        dt = time.perf_counter() - t0
+        tot_t += dt
+        tot_n += 2 * x.size
+        parts.append(f"{bits}-bit {dt * 1e3:.0f} ms")
+    return tot_n / tot_t, (f"reference quantize_key_tensor + quantize_value_tensor on [1,32,4096,128] fp32 "
+                           f"(binary16 grid), gs 32, bits 2/3/4 ({', '.join(parts)})"), cores
 
 
 # ---------------------------------------------------------------------------------------
-# B200 arm
+# B200 arm: decode step
 # ---------------------------------------------------------------------------------------
 def run_b200(args, rank, world, local_rank):
     import numpy as np
@@ -170,10 +224,17 @@ def run_b200(args, rank, world, local_rank):
 
     import paper_2506_08018_b200 as K
     from paper_2506_08018_b200 import _lib
+    from paper_2506_08018_b200.shard import ShardPlan
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    L, B, H, Hq, D, ctx, high = CONFIGS[args.config]
+    L, Bg, H, Hq, D, ctx, high, scaling = CONFIGS[args.config]
+    if scaling == "weak":  # every rank holds its own shard of the global batch
+        plan = ShardPlan(Bg * world, H, Hq, world, rank, mode="batch")
+    else:
+        plan = ShardPlan(Bg, H, Hq, world, rank)
+    B, Hl, Hql = plan.local_batch, plan.local_heads, plan.local_heads * (Hq // H)
+    B_glob = plan.B
     cfg = K.tiered_config(L, high) if high else K.uniform_config(L, 2, 0.1)
     total_steps = args.warmup + args.steps
     pre = ctx - 64
@@ -182,14 +243,15 @@ def run_b200(args, rank, world, local_rank):
 
     caches = []
     for l in range(L):
-        c = K.KVLayerCache(cfg.layers[l], B, H, D, capacity_tokens=cap, tail_dtype=torch.float16)
-        k = torch.randn(B, H, pre, D, device=dev, dtype=torch.float16)
-        v = torch.randn(B, H, pre, D, device=dev, dtype=torch.float16)
+        c = K.KVLayerCache(cfg.layers[l], B, Hl, D, capacity_tokens=cap, tail_dtype=torch.float16)
+        plan.place(c)
+        k = torch.randn(B, Hl, pre, D, device=dev, dtype=torch.float16)
+        v = torch.randn(B, Hl, pre, D, device=dev, dtype=torch.float16)
         c.append(k, v)
         del k, v
         caches.append(c)
     # 64 decode appends to reach the steady-state window (trajectory table)
-    kd = torch.randn(64, B, H, 1, D, device=dev, dtype=torch.float16)
+    kd = torch.randn(64, B, Hl, 1, D, device=dev, dtype=torch.float16)
     for s in range(64):
         for c in caches:
             c.append(kd[s], kd[(s + 1) % 64])
@@ -197,28 +259,24 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     # per-step inputs resident in HBM
-    qs = torch.randn(total_steps, L, B, Hq, 1, D, device=dev, dtype=torch.float16)
-    kn = torch.randn(total_steps, L, B, H, 1, D, device=dev, dtype=torch.float16)
-    vn = torch.randn(total_steps, L, B, H, 1, D, device=dev, dtype=torch.float16)
-    outs = torch.empty(L, B, Hq, 1, D, device=dev, dtype=torch.float32)
+    qs = torch.randn(total_steps, L, B, Hql, 1, D, device=dev, dtype=torch.float16)
+    kn = torch.randn(total_steps, L, B, Hl, 1, D, device=dev, dtype=torch.float16)
+    vn = torch.randn(total_steps, L, B, Hl, 1, D, device=dev, dtype=torch.float16)
+    outs = torch.empty(L, B, Hql, 1, D, device=dev, dtype=torch.float32)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     lib = _lib.lib()
-    import ctypes as C
+    steps = [K.DecodeStep(caches, list(kn[s]), list(vn[s]), list(qs[s]), list(outs)) for s in range(total_steps)]
 
-    def step(s, ev=None):
-        # per layer: append(1 token) + attend, one kvmix_append_attend call (the append runs in
-        # the attention launch's prologue in the steady state; Key-group age-out steps launch
-        # the general append first)
+    def step_instrumented(s, ev):
+        # per layer append_attend with CUDA events around each launch (same kernels as step())
         for l, c in enumerate(caches):
-            if ev is not None:
-                ev[l][0].record(stream)
+            ev[l][0].record(stream)
             st = lib.kvmix_append_attend(c.handle, kn[s, l].data_ptr(), vn[s, l].data_ptr(), _lib.F16, 1,
-                                         qs[s, l].data_ptr(), _lib.F16, Hq, 1, outs[l].data_ptr(), None, sp)
+                                         qs[s, l].data_ptr(), _lib.F16, Hql, 1, outs[l].data_ptr(), None, sp)
             if st:
                 _lib.check(st)
-            if ev is not None:
-                ev[l][1].record(stream)
+            ev[l][1].record(stream)
 
     def barrier():
         if world > 1:
@@ -226,13 +284,10 @@ def run_b200(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     for s in range(args.warmup):
-        step(s)
+        steps[s].step(sp)
     barrier()
-    bytes_layer = []
-    for c in caches:  # algorithmic bytes of one attend launch at the timed state
-        bytes_layer.append(c.algorithmic_bytes() + B * Hq * D * (2 + 4))
+    bytes_layer = [c.algorithmic_bytes() + B * Hql * D * (2 + 4) for c in caches]  # one attend launch each
     # CUDA events around every layer's launch on the launch stream, on every 4th timed step
-    # (each event record costs the stream a few microseconds; value carries 1/4 of it)
     inst = list(range(0, args.steps, 4))
     evs = {i: [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
            for i in inst}
@@ -242,27 +297,24 @@ def run_b200(args, rank, world, local_rank):
         barrier()
         start.record(stream)
         for i, s in enumerate(range(args.warmup, total_steps)):
-            step(s, evs.get(i))
+            if i in evs:
+                step_instrumented(s, evs[i])
+            else:
+                steps[s].step(sp)
         end.record(stream)
         end.synchronize()
     launches = _lib.launch_count() - launches0
     elapsed = start.elapsed_time(end)  # ms for K steps
-    # per-layer attend launch time, averaged over the instrumented timed steps
     attn_ms = [statistics.mean(evs[i][l][0].elapsed_time(evs[i][l][1]) for i in inst) for l in range(L)]
     t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     elapsed = float(t.item())
     ms_per_step = elapsed / args.steps
-    value = world * B * args.steps / (elapsed / 1e3)
+    value = B_glob * args.steps / (elapsed / 1e3)
 
-    # ---- roofline of the dominant kernel ----
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    if os.path.exists(peaks_path):
-        with open(peaks_path) as f:
-            peak = float(json.load(f)["hbm_gbs"])
-        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    # ---- roofline of the dominant kernel (this rank's launches) ----
+    peak, peak_src = peak_hbm()
     tot_bytes = sum(bytes_layer)
     tot_ms = sum(attn_ms)
     achieved = tot_bytes / (tot_ms / 1e3) / 1e9
@@ -270,24 +322,31 @@ def run_b200(args, rank, world, local_rank):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(args.config)
+            traffic = json.load(f).get(args.config) if world == 1 else None
+
+    # ---- --check: two sampled (layer, b, head) outputs of the last timed step ----
+    check = None
+    if not args.no_check:
+        check = check_outputs(caches, qs[total_steps - 1], outs, Hq // H, rank)
 
     # ---- e2e through the public API with pinned host buffers ----
-    # Every step copies that step's q/k/v from pinned host memory and reads the outputs back;
-    # the copies run on a second stream, double-buffered (step s+1's inputs upload while step
-    # s computes, step s's outputs download while step s+1 computes), as a serving loop would.
+    # Every step copies that step's q/k/v from pinned host memory and reads every layer's
+    # output back; the copies run on a second stream, double-buffered (step s+1's inputs
+    # upload while step s computes, step s's outputs download while step s+1 computes), as a
+    # serving loop would. The step itself is DecodeStep.step() (public API).
     e2e = None
     if not args.no_e2e:
         q_h = qs.cpu().pin_memory()
         k_h = kn.cpu().pin_memory()
         v_h = vn.cpu().pin_memory()
         n_e2e = min(args.steps, total_steps)
-        o_h = torch.empty(n_e2e, L, B, Hq, 1, D, dtype=torch.float32).pin_memory()
+        o_h = torch.empty(n_e2e, L, B, Hql, 1, D, dtype=torch.float32).pin_memory()
         cp = torch.cuda.Stream(device=dev)
         qb = [torch.empty_like(qs[0]) for _ in range(2)]
         kb = [torch.empty_like(kn[0]) for _ in range(2)]
         vb = [torch.empty_like(vn[0]) for _ in range(2)]
         ob = [torch.empty_like(outs) for _ in range(2)]
+        dsteps = [K.DecodeStep(caches, list(kb[i]), list(vb[i]), list(qb[i]), list(ob[i])) for i in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
         done = [torch.cuda.Event() for _ in range(2)]
         drained = [torch.cuda.Event() for _ in range(2)]
@@ -311,8 +370,7 @@ def run_b200(args, rank, world, local_rank):
                     upload(s + 1, 1 - i)
                 stream.wait_event(ready[i])
                 stream.wait_event(drained[i])  # ob[i] of step s-2 has been read back
-                for l, c in enumerate(caches):
-                    K.append_attend(c, kb[i][l], vb[i][l], qb[i][l], out=ob[i][l])
+                dsteps[i].step()
                 done[i].record(stream)
                 with torch.cuda.stream(cp):
                     cp.wait_event(done[i])
@@ -330,12 +388,16 @@ def run_b200(args, rank, world, local_rank):
         te = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": world * B * n_e2e / (float(te.item()) / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(L * (qs[0, 0].numel() + kn[0, 0].numel() + vn[0, 0].numel()) * 2),
-               "d2h_bytes_per_step": int(L * outs[0].numel() * 4),
-               "path": "per layer append_attend (Python API: KVLayerCache.append + attend) on pinned-host inputs; "
-                       "H2D/D2H double-buffered on a copy stream"}
+        e2e = {"value": B_glob * n_e2e / (float(te.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(L * (qs[0, 0].numel() + kn[0, 0].numel() + vn[0, 0].numel()) * 2) * world,
+               "d2h_bytes_per_step": int(L * outs[0].numel() * 4) * world,
+               "path": "DecodeStep.step() (public API, kvmix_append_attend_layers) on pinned-host inputs, every "
+                       "layer's output read back; H2D/D2H double-buffered on a copy stream"}
 
+    launches_t = torch.tensor([launches], device=dev, dtype=torch.int64)
+    if world > 1:
+        torch.distributed.all_reduce(launches_t)
+    hi = f"0-{high - 1} K3/V4 r0.2, rest K2/V2 r0.1" if high else "all K2/V2 r0.1"
     res = {
         "metric": METRIC,
         "value": value,
@@ -345,30 +407,204 @@ def run_b200(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "u8 codes x s8/u8 fixed-point digits -> s32 (IMMA), f32 softmax (KV bit-packed 2/3/4-bit)",
         "data": "synthetic (randn on the binary16 grid, on device)",
-        "config": {"workload": f"{CONFIG_INDEX[args.config]} {args.config}: {L} layers, B{B}, Hq{Hq}/Hkv{H}, D{D}, ~{ctx} ctx, "
-                               f"KVmix tiers (0-{high - 1} K3/V4 r0.2, rest K2/V2 r0.1), gs32, fp16 window",
-                   "global_batch": B * world, "seq_len": ctx, "parallelism": f"dp{world} (batch x kv-head shards)",
-                   "l2": (f"per-step cache bytes ({tot_bytes / 1e9:.2f} GB) >> 126 MB L2; no flush needed"
+        "config": {"workload": f"{CONFIG_INDEX[args.config]} {args.config}: {L} layers, global B{B_glob}, Hq{Hq}/Hkv{H}, "
+                               f"D{D}, ~{ctx} ctx, KVmix tiers ({hi}), gs32, fp16 window",
+                   "global_batch": B_glob, "seq_len": ctx,
+                   "parallelism": f"{plan.mode} shards x{world} (rank 0: b {plan.b0}-{plan.b1 - 1}, kv heads "
+                                  f"{plan.h0}-{plan.h1 - 1}); no data-path collective",
+                   "l2": (f"per-step cache bytes per GPU ({tot_bytes / 1e9:.2f} GB) >> 126 MB L2; no flush needed"
                           if tot_bytes > 1e9 else f"per-step cache bytes {tot_bytes / 1e6:.0f} MB: partly L2-resident"),
                    "timed_step": "per layer: append(1 token) + attend = kvmix_append_attend"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "attend_mma_kernel (IMMA; append in its prologue, split partials merged in-kernel), one launch per layer",
-                     "traffic_unit": "DRAM bytes per step (profiles/ncu_traffic.json)",
+                     "kernel": "attend_mma_kernel (IMMA; 1-token append in its prologue, split partials merged "
+                               "in-kernel), one launch per layer",
+                     "step_frac": tot_bytes / (ms_per_step / 1e3) / 1e9 / peak,
+                     "traffic_unit": "DRAM bytes per step (profiles/ncu_traffic.json, 1 GPU)",
                      "algorithmic_bytes_per_step": tot_bytes, "attend_ms_per_step": tot_ms,
                      "attend_share_of_step": tot_ms / ms_per_step},
         "e2e": e2e,
-        "gpu_launches": launches,
+        "gpu_launches": int(launches_t.item()),
         "clocks": clk.summary(),
-        "memory": {"compressed_bytes_per_step": tot_bytes,
+        "check": check,
+        "memory": {"compressed_bytes_per_step_per_gpu": tot_bytes,
                    "compression_ratio": sum(c.memory_usage().fp16_baseline_bits for c in caches) /
                    max(1, sum(c.memory_usage().total_bits for c in caches))},
     }
     return res
+
+
+def check_outputs(caches, q_last, outs, G, rank):
+    """fp64 attention over the bit-exact snapshot (tests pin it against the reference) of two
+    sampled (layer, b, kv-head) slices vs the device output of the last timed step; the
+    tolerance is the parity tests' 2e-6 * max|V|."""
+    import torch
+    res = []
+    L = len(caches)
+    gen = torch.Generator().manual_seed(7 + rank)
+    for l in (0, L - 1) if L > 1 else (0,):
+        c = caches[l]
+        b = int(torch.randint(0, c.batch(), (1,), generator=gen))
+        h = int(torch.randint(0, c.heads(), (1,), generator=gen))
+        ks, vs = c.snapshot_dequantized()
+        k = ks[b, h].double()
+        v = vs[b, h].double()
+        del ks, vs
+        q = q_last[l, b, h * G:(h + 1) * G, 0].double()  # [G, D]
+        s = (q @ k.T) * (1.0 / float(k.shape[1]) ** 0.5)
+        ref = torch.softmax(s, dim=-1) @ v
+        got = outs[l, b, h * G:(h + 1) * G, 0].double()
+        err = float((got - ref).abs().max() / v.abs().max())
+        res.append({"layer": l, "b": b, "kv_head": h, "err_over_maxV": err, "ok": err <= 2e-6})
+    return {"samples": res, "ok": all(r["ok"] for r in res), "tolerance": "2e-6 * max|V| vs fp64 over the snapshot"}
+
+
+# ---------------------------------------------------------------------------------------
+# B200 arm: configs[4] quantize/pack sweep
+# ---------------------------------------------------------------------------------------
+def run_quant(args, rank, world, local_rank):
+    import torch
+
+    import paper_2506_08018_b200 as K
+    from paper_2506_08018_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    shape = (16, 32, 4096, 128)  # per GPU (weak scaling, BASELINE.md 2)
+    n = 1
+    for x in shape:
+        n *= x
+    torch.manual_seed(99 + rank)
+    x = torch.randn(shape, device=dev, dtype=torch.float16)
+    settings = [(b, gs, key) for b in (2, 3, 4) for gs in (32, 64, 128) for key in (True, False)]
+    lib = _lib.lib()
+    bufs = {}
+    for b, gs, key in settings:
+        nw = K.packed_word_count(n, b)
+        ng = (n // gs) if key else (n // 128) * ((128 + gs - 1) // gs)
+        bufs[(b, gs, key)] = (torch.empty(nw, dtype=torch.int32, device=dev),
+                              torch.empty((ng, 2), dtype=torch.int16, device=dev))
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def one(b, gs, key):
+        w, m = bufs[(b, gs, key)]
+        st = lib.kvmix_quantize(0 if key else 1, x.data_ptr(), _lib.F16, *shape, b, gs, w.data_ptr(), m.data_ptr(), sp)
+        if st:
+            _lib.check(st)
+
+    def sweep():
+        for s in settings:
+            one(*s)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sweep()
+    barrier()
+    # per-setting kernel time with CUDA events (inputs 1 GiB >> L2)
+    per = {}
+    ev = {s: [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for s in settings}
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launch_count()
+    with Clocks(local_rank) as clk:
+        barrier()
+        start.record(stream)
+        for it in range(args.steps):
+            for s in settings:
+                if it == args.steps - 1:
+                    ev[s][0].record(stream)
+                one(*s)
+                if it == args.steps - 1:
+                    ev[s][1].record(stream)
+        end.record(stream)
+        end.synchronize()
+    launches = _lib.launch_count() - launches0
+    elapsed = start.elapsed_time(end)
+    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    elapsed = float(t.item())
+    ms_per_step = elapsed / args.steps  # one step = the whole 18-setting sweep
+    elems = n * len(settings) * world
+    value = elems * args.steps / (elapsed / 1e3)
+    peak, peak_src = peak_hbm()
+    rows, tot_bytes, tot_ms = [], 0, 0.0
+    for b, gs, key in settings:
+        ms = ev[(b, gs, key)][0].elapsed_time(ev[(b, gs, key)][1])
+        payload = (4.0 / 11.0) if b == 3 else b / 8.0
+        byt = n * (2 + payload + 4.0 / gs)  # fp16 in + packed payload + binary16 (scale, min)
+        tot_bytes += byt
+        tot_ms += ms
+        rows.append({"bits": b, "gs": gs, "side": "K" if key else "V", "ms": ms, "GBps": byt / ms / 1e6,
+                     "frac": byt / ms / 1e6 / peak})
+    return {
+        "metric": QMETRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp16 in -> u32 packed words + binary16 meta",
+        "data": "synthetic (randn fp16, on device)",
+        "config": {"workload": "configs[4] quantize/pack sweep: bits {2,3,4} x gs {32,64,128} x {Keys per-channel, "
+                               "Values per-token}, [16,32,4096,128] fp16 per GPU (1 GiB input >> L2)",
+                   "global_batch": 16 * world, "seq_len": 4096, "parallelism": f"weak x{world}"},
+        "roofline": {"bound": "hbm", "achieved": tot_bytes / (tot_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": tot_bytes / (tot_ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "quantize_{key,value}_* kernels (one launch per setting)", "per_setting": rows},
+        "e2e": None, "gpu_launches": launches, "clocks": clk.summary(),
+    }
+
+
+def quant_e2e(args, local_rank):
+    """configs[4] end to end through the public API (quantize_key_tensor /
+    quantize_value_tensor from pinned host fp16, results read back to the host)."""
+    import torch
+
+    import paper_2506_08018_b200 as K
+    dev = torch.device("cuda", local_rank)
+    shape = (16, 32, 4096, 128)
+    xh = torch.randn(shape, dtype=torch.float16).pin_memory()
+    bits, gs = 2, 32
+    n = xh.numel()
+    stream = torch.cuda.current_stream()
+
+    def one():
+        x = xh.to(dev, non_blocking=True)
+        kq = K.quantize_key_tensor(x, K.QuantSpec(bits, K.Grouping.kPerChannelKey, gs))
+        vq = K.quantize_value_tensor(x, K.QuantSpec(bits, K.Grouping.kPerTokenValue, gs))
+        return [kq.codes.words.cpu(), kq.meta.cpu(), vq.codes.words.cpu(), vq.meta.cpu()]
+
+    one()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(1, min(args.steps, 5))
+    s0.record(stream)
+    outs = None
+    for _ in range(reps):
+        outs = one()
+    s1.record(stream)
+    s1.synchronize()
+    ms = s0.elapsed_time(s1) / reps
+    d2h = sum(o.numel() * o.element_size() for o in outs)
+    return {"value": 2 * n / (ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": int(n * 2),
+            "d2h_bytes_per_step": int(d2h),
+            "path": "quantize_key_tensor + quantize_value_tensor (public API), 2-bit gs32, fp16 [16,32,4096,128] "
+                    "uploaded from pinned host memory, words + meta read back (the input is uploaded once per "
+                    "step and quantized both ways)"}
+
+
+# ---------------------------------------------------------------------------------------
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -377,21 +613,28 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the JSON line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+
     if args.impl == "reference":
         if rank != 0:
             return 0
         threads = args.cpu_threads or os.cpu_count() or 1
+        sample = cpu_quant_sample if args.config == "quant-sweep" else (lambda th: cpu_reference_sample(args.config, th))
         warm = 0  # untimed warm-up samples (bounded: each one is seconds of CPU work)
         tw = time.time()
         while warm < args.warmup and time.time() - tw < 30:
-            if cpu_reference_sample(args.config, threads)[0] is None:
+            if sample(threads)[0] is None:
                 break
             warm += 1
         t0 = time.time()
         times = []
         value = desc = cores = None
         for _ in range(max(1, args.steps)):
-            out = cpu_reference_sample(args.config, threads)
+            out = sample(threads)
             if out[0] is None:
                 print(json.dumps({"impl": "reference", "unavailable": out[1]}))
                 return 0
@@ -400,30 +643,52 @@ def main():
             if time.time() - t0 > 120:
                 break
         value = statistics.median(times)
-        L, B, H, Hq, D, ctx, high = CONFIGS[args.config]
+        if args.config == "quant-sweep":
+            unit, metric, cfgd = "elements/s", QMETRIC, {"workload": "quant-sweep", "global_batch": 16, "seq_len": 4096,
+                                                          "parallelism": "cpu"}
+            msps = 16 * 32 * 4096 * 128 * 18 / value * 1e3
+        else:
+            L, Bg, H, Hq, D, ctx, high, scaling = CONFIGS[args.config]
+            unit, metric = "tokens/s", METRIC
+            cfgd = {"workload": args.config, "global_batch": Bg, "seq_len": ctx, "parallelism": "cpu"}
+            msps = Bg / value * 1e3
         print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": len(times), "warmup": warm, "ms_per_step": B / value * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (reference CPU)", "data": "synthetic",
-            "config": {"workload": args.config, "global_batch": B, "seq_len": ctx, "parallelism": "cpu"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": desc},
-            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+            "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus,
+            "steps": len(times), "warmup": warm, "ms_per_step": msps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (reference CPU)", "data": "synthetic",
+            "config": cfgd,
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference", "sample": desc},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return 0
 
     if world > 1:
         import torch
-        torch.distributed.init_process_group("nccl")
-    res = run_b200(args, rank, world, local_rank)
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.config == "quant-sweep":
+        res = run_quant(args, rank, world, local_rank)
+        if rank == 0 and not args.no_e2e:
+            res["e2e"] = quant_e2e(args, local_rank)
+            res["e2e"]["value"] *= world
+    else:
+        res = run_b200(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu:
             try:
-                v, desc, cores = cpu_reference_sample(args.config, args.cpu_threads or os.cpu_count() or 1)
-                res["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": desc}
+                th = args.cpu_threads or os.cpu_count() or 1
+                if args.config == "quant-sweep":
+                    v, desc, cores = cpu_quant_sample(th)
+                    unit = "elements/s"
+                else:
+                    v, desc, cores = cpu_reference_sample(args.config, th)
+                    unit = "tokens/s"
+                res["cpu_baseline"] = {"value": v, "unit": unit, "cores": cores, "kind": "reference", "sample": desc}
             except Exception as e:  # the baseline is reported, never required
                 res["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         print(json.dumps(res))
     if world > 1:
         import torch
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
 

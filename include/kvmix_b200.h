@@ -110,6 +110,15 @@ kvmix_status kvmix_rpc_target(int64_t current, double r, int64_t* out);
 kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int heads, int head_dim,
                                 int64_t capacity_tokens, kvmix_dtype tail_dtype, kvmix_cache** out);
 void kvmix_cache_destroy(kvmix_cache* cache);
+/* Multi-GPU placement (batch x KV-head shards): this cache holds batch rows
+ * [batch_offset, batch_offset + batch) and KV heads [head_offset, head_offset + heads) of a
+ * global [global_batch, global_heads] cache. The reference's Mixed3 narrow slots are a
+ * function of the GLOBAL stream index (quant.cpp:36-47, 77-95), so a placed shard holds
+ * bit-for-bit the unsharded cache's slice. Must precede the first append. Segment
+ * export/import of a 3-bit side of a sharded cache is refused (its words interleave with
+ * the other shards'). */
+kvmix_status kvmix_cache_set_shard(kvmix_cache* cache, int global_batch, int global_heads, int batch_offset,
+                                   int head_offset);
 /* Drops all tokens (device buffers are re-zeroed on `stream`). */
 kvmix_status kvmix_cache_reset(kvmix_cache* cache, void* stream);
 /* KVLayerCache::append (cache.cpp:45-80): k, v are [B,H,t,D] device tensors of `dtype`.
@@ -163,11 +172,16 @@ kvmix_status kvmix_attend(const kvmix_cache* cache, const void* q, kvmix_dtype d
 kvmix_status kvmix_append_attend(kvmix_cache* cache, const void* k, const void* v, kvmix_dtype kv_dtype, int t,
                                  const void* q, kvmix_dtype q_dtype, int q_heads, int tq, float* out,
                                  double* checksum, void* stream);
-/* Same, over several layers' caches in one call (one decode step of a model stack):
- * q[l], out[l] per layer. Used by the benchmark to keep host overhead off the step. */
+/* attend over several layers' caches in one call: q[l], out[l] per layer. */
 kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* q,
                                  kvmix_dtype dtype, int q_heads, int t, float* const* out,
                                  void* stream);
+/* One decode step of a model stack in one call: kvmix_append_attend for every layer l
+ * (k[l], v[l], q[l], out[l]) in order on `stream` -- the per-layer CachedDecoder::step pairs
+ * (toymodel.cpp:720-721, 746) without a host round trip per layer. No checksum. */
+kvmix_status kvmix_append_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* k,
+                                        const void* const* v, kvmix_dtype kv_dtype, int t, const void* const* q,
+                                        kvmix_dtype q_dtype, int q_heads, int tq, float* const* out, void* stream);
 /* fused_qk_scores (attention.cpp:28-81): scores [B,H,t,total] fp32 (already * 1/sqrt(D)). */
 kvmix_status kvmix_fused_qk_scores(const kvmix_cache* cache, const void* q, kvmix_dtype dtype, int t,
                                    float* scores, void* stream);
@@ -179,6 +193,19 @@ kvmix_status kvmix_fused_pv(const kvmix_cache* cache, const float* probs, int t,
  * (2*B*H*total*D floats, caller-provided) then dense attention. Oracle-style path. */
 kvmix_status kvmix_reference_attend(const kvmix_cache* cache, const void* q, kvmix_dtype dtype, int t,
                                     float* scratch, float* out, double* checksum, void* stream);
+
+/* scratch::reset / scratch::allocated (scratch.hpp:14-21): bytes of attention scratch the
+ * library requested since the last reset (split-K partials, merge counters, flags). The
+ * reference's contract is that the fused path's scratch does not depend on the cached token
+ * count (test_attention.cpp:182-205); here it depends on (B, H, query rows, D, SM count) only.
+ * The memory itself is persistent per (device, stream) and reused across calls. */
+void kvmix_scratch_reset(void);
+uint64_t kvmix_scratch_allocated(void);
+
+/* Tuning / test hook: overrides one kernel knob for later launches ("KVMIX_TAIL_UNIT",
+ * "KVMIX_GROUP_COST", "KVMIX_TEST_FLUSH_BLOCKS" (<= 0 restores the default), "KVMIX_MIN_COST").
+ * The same names are read once from the environment at the first launch. */
+kvmix_status kvmix_set_knob(const char* name, int value);
 
 /* Number of kernels this library has launched in this process (instrumentation for
  * the benchmark's gpu_launches count). */

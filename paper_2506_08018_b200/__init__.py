@@ -15,7 +15,7 @@ from .quant import (GroupMeta, Grouping, PackedBuffer, PackLayout, QuantizedGrou
 from .config import (BitAllocationParams, LayerQuantConfig, ModelQuantConfig, Provenance, allocate_bits,
                      average_bits, full_precision_config, read_config, tiered_config, uniform_config, write_config)
 from .cache import KVLayerCache, MemoryReport, rpc_target
-from .attention import (AttentionOutput, append_attend, attend, attend_layers, attention_inv_scale, dump_scores_csv, fused_pv,
+from .attention import (AttentionOutput, DecodeStep, append_attend, append_attend_layers, attend, attend_layers, attention_inv_scale, dump_scores_csv, fused_pv,
                         fused_qk_scores, reference_attend, softmax_rows)
 
 lib()  # fail at import time if the native library is missing

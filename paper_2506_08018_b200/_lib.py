@@ -85,6 +85,7 @@ def _declare(L):
         "kvmix_rpc_target": (i, [i64, C.c_double, C.POINTER(C.c_int64)]),
         "kvmix_cache_create": (i, [C.POINTER(LayerConfigC), i, i, i, i64, i, C.POINTER(vp)]),
         "kvmix_cache_destroy": (None, [vp]),
+        "kvmix_cache_set_shard": (i, [vp, i, i, i, i]),
         "kvmix_cache_reset": (i, [vp, vp]),
         "kvmix_cache_append": (i, [vp, vp, vp, i, i, vp]),
         "kvmix_cache_counters": (i, [vp, C.POINTER(C.c_int64)]),
@@ -101,10 +102,15 @@ def _declare(L):
         "kvmix_attend": (i, [vp, vp, i, i, i, vp, C.POINTER(C.c_double), vp]),
         "kvmix_append_attend": (i, [vp, vp, vp, i, i, vp, i, i, i, vp, C.POINTER(C.c_double), vp]),
         "kvmix_attend_layers": (i, [C.POINTER(vp), i, C.POINTER(vp), i, i, i, C.POINTER(vp), vp]),
+        "kvmix_append_attend_layers": (i, [C.POINTER(vp), i, C.POINTER(vp), C.POINTER(vp), i, i, C.POINTER(vp), i, i, i,
+                                           C.POINTER(vp), vp]),
         "kvmix_fused_qk_scores": (i, [vp, vp, i, i, vp, vp]),
         "kvmix_softmax_rows": (i, [vp, i64, i64, vp]),
         "kvmix_fused_pv": (i, [vp, vp, i, vp, vp]),
         "kvmix_reference_attend": (i, [vp, vp, i, i, vp, vp, C.POINTER(C.c_double), vp]),
+        "kvmix_scratch_reset": (None, []),
+        "kvmix_scratch_allocated": (u64, []),
+        "kvmix_set_knob": (i, [C.c_char_p, i]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -135,6 +141,20 @@ def check(status: int) -> None:
 
 def launch_count() -> int:
     return int(lib().kvmix_launch_count())
+
+
+def set_knob(name: str, value: int) -> None:
+    """Override one kernel tuning/test knob (kvmix_set_knob)."""
+    check(lib().kvmix_set_knob(name.encode(), int(value)))
+
+
+def scratch_reset() -> None:
+    lib().kvmix_scratch_reset()
+
+
+def scratch_allocated() -> int:
+    """Bytes of attention scratch requested since scratch_reset() (scratch.hpp:14-21)."""
+    return int(lib().kvmix_scratch_allocated())
 
 
 def launch_count_of(kernel: str) -> int:

@@ -38,6 +38,15 @@ def _check_query(q: torch.Tensor, cache: KVLayerCache, allow_gqa: bool) -> None:
         raise KvmixInvalidArgument("attention: need at least one query row")
 
 
+def _check_out(out: torch.Tensor, shape, device) -> None:
+    """A caller-supplied output must be exactly what the kernel writes: contiguous fp32
+    [B, Hq, t, D] on the cache's device (anything else would be written out of bounds)."""
+    if (not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or tuple(out.shape) != tuple(shape)
+            or not out.is_contiguous() or out.device != device):
+        raise KvmixInvalidArgument(f"attention: out must be a contiguous float32 tensor of shape {tuple(shape)} "
+                                   f"on {device}")
+
+
 def attend(query, cache: KVLayerCache, *, checksum: bool = True, out: torch.Tensor | None = None) -> AttentionOutput:
     """attend (attention.cpp:161-166). checksum=True synchronizes to return the double sum
     of all scaled scores like AttentionOutput::scores_checksum."""
@@ -46,6 +55,8 @@ def attend(query, cache: KVLayerCache, *, checksum: bool = True, out: torch.Tens
     B, Hq, t, D = (int(v) for v in q.shape)
     if out is None:
         out = torch.empty((B, Hq, t, D), dtype=torch.float32, device=q.device)
+    else:
+        _check_out(out, (B, Hq, t, D), q.device)
     cs = C.c_double(0.0)
     check(lib().kvmix_attend(cache.handle, _ptr(q), _dtype_code(q), Hq, t, _ptr(out), C.byref(cs) if checksum else None,
                              _stream()))
@@ -67,6 +78,8 @@ def append_attend(cache: KVLayerCache, new_keys, new_values, query, *, checksum:
     B, Hq, t, D = (int(x) for x in q.shape)
     if out is None:
         out = torch.empty((B, Hq, t, D), dtype=torch.float32, device=q.device)
+    else:
+        _check_out(out, (B, Hq, t, D), q.device)
     cs = C.c_double(0.0)
     check(lib().kvmix_append_attend(cache.handle, _ptr(k), _ptr(v), _dtype_code(k), int(k.shape[2]), _ptr(q),
                                     _dtype_code(q), Hq, t, _ptr(out), C.byref(cs) if checksum else None, _stream()))
@@ -137,9 +150,73 @@ def dump_scores_csv(os_, scores) -> None:
 def attend_layers(caches, queries, outs, *, stream: int | None = None) -> None:
     """One decode step's attention over a stack of layer caches in a single C call."""
     n = len(caches)
+    if len(queries) != n or len(outs) != n:
+        raise KvmixInvalidArgument("attend_layers: one query and one output per cache")
+    for c, q, o in zip(caches, queries, outs):
+        _check_query(q, c, allow_gqa=True)
+        if not q.is_cuda or not q.is_contiguous() or q.dtype not in (torch.float16, torch.float32) or q.dtype != queries[0].dtype \
+                or tuple(q.shape[1:]) != tuple(queries[0].shape[1:]):
+            raise KvmixInvalidArgument("attend_layers: queries must be contiguous device tensors of one dtype and shape")
+        _check_out(o, tuple(q.shape), q.device)
     hs = (C.c_void_p * n)(*[c.handle.value for c in caches])
     qs = (C.c_void_p * n)(*[q.data_ptr() for q in queries])
     os_ = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
     q0 = queries[0]
     check(lib().kvmix_attend_layers(hs, n, qs, _dtype_code(q0), int(q0.shape[1]), int(q0.shape[2]), os_,
                                     stream if stream is not None else _stream()))
+
+
+def _ptr_array(ts):
+    return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+
+def _check_layers(caches, keys, values, queries, outs):
+    n = len(caches)
+    if not (len(keys) == len(values) == len(queries) == len(outs) == n):
+        raise KvmixInvalidArgument("append_attend_layers: one key, value, query and output per cache")
+    for c, k, v, q, o in zip(caches, keys, values, queries, outs):
+        for x in (k, v, q):
+            if not isinstance(x, torch.Tensor) or not x.is_cuda or not x.is_contiguous() or \
+                    x.dtype not in (torch.float16, torch.float32):
+                raise KvmixInvalidArgument("append_attend_layers: inputs must be contiguous fp16/fp32 device tensors")
+        c._check_append(k, v)
+        if v.dtype != k.dtype or k.dtype != keys[0].dtype or tuple(k.shape) != tuple(keys[0].shape):
+            raise KvmixInvalidArgument("append_attend_layers: keys/values of one dtype and shape")
+        _check_query(q, c, allow_gqa=True)
+        if q.dtype != queries[0].dtype or tuple(q.shape) != tuple(queries[0].shape):
+            raise KvmixInvalidArgument("append_attend_layers: queries of one dtype and shape")
+        _check_out(o, tuple(q.shape), q.device)
+
+
+def append_attend_layers(caches, keys, values, queries, outs, *, stream: int | None = None) -> None:
+    """One decode step of a model stack: append_attend(caches[l], keys[l], values[l],
+    queries[l], out=outs[l]) for every layer, in one C call (kvmix_append_attend_layers)."""
+    _check_layers(caches, keys, values, queries, outs)
+    n = len(caches)
+    q0, k0 = queries[0], keys[0]
+    check(lib().kvmix_append_attend_layers((C.c_void_p * n)(*[c.handle.value for c in caches]), n, _ptr_array(keys),
+                                           _ptr_array(values), _dtype_code(k0), int(k0.shape[2]), _ptr_array(queries),
+                                           _dtype_code(q0), int(q0.shape[1]), int(q0.shape[2]), _ptr_array(outs),
+                                           stream if stream is not None else _stream()))
+
+
+class DecodeStep:
+    """A serving loop's decode step over a fixed stack of layer caches and fixed device
+    buffers (the caller refills them each step): shapes are validated and the pointer arrays
+    built once, so step() is a single C call (kvmix_append_attend_layers)."""
+
+    def __init__(self, caches, keys, values, queries, outs):
+        _check_layers(caches, keys, values, queries, outs)
+        n = len(caches)
+        self._n = n
+        self._keep = (list(caches), list(keys), list(values), list(queries), list(outs))
+        self._h = (C.c_void_p * n)(*[c.handle.value for c in caches])
+        self._k, self._v = _ptr_array(keys), _ptr_array(values)
+        self._q, self._o = _ptr_array(queries), _ptr_array(outs)
+        self._kdt, self._t = _dtype_code(keys[0]), int(keys[0].shape[2])
+        self._qdt, self._hq, self._tq = _dtype_code(queries[0]), int(queries[0].shape[1]), int(queries[0].shape[2])
+
+    def step(self, stream: int | None = None) -> None:
+        check(lib().kvmix_append_attend_layers(self._h, self._n, self._k, self._v, self._kdt, self._t, self._q,
+                                               self._qdt, self._hq, self._tq, self._o,
+                                               stream if stream is not None else _stream()))

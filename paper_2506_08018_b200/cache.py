@@ -76,6 +76,15 @@ class KVLayerCache:
                 pass
             self._h = None
 
+    def set_shard(self, global_batch: int, global_heads: int, batch_offset: int, head_offset: int) -> None:
+        """Place this cache as the [batch_offset:, head_offset:] slice of a global
+        [global_batch, global_heads] cache (multi-GPU shard): Mixed3 narrow slots then follow
+        the global stream index, so the shard equals the unsharded cache's slice bit for bit.
+        Must precede the first append (kvmix_cache_set_shard)."""
+        check(lib().kvmix_cache_set_shard(self._h, int(global_batch), int(global_heads), int(batch_offset),
+                                          int(head_offset)))
+        self._shard = (int(global_batch), int(global_heads), int(batch_offset), int(head_offset))
+
     # ---- accessors (cache.hpp:64-76) -------------------------------------------------------
     @property
     def handle(self):

@@ -7,51 +7,50 @@
 
 namespace kvb {
 
-// Stream-ordered scratch for split-K partials. Sizes depend on (B, H, rows, D) and the SM
-// count only -- never on the cached token count (the reference's scratch contract,
-// test_attention.cpp:182-205). Freed stream-ordered when the call returns, so concurrent
-// readers on different streams never share scratch.
+// Scratch for split-K partials, merge counters and append flags. Sizes depend on (B, H,
+// rows, D) and the SM count only -- never on the cached token count (the reference's
+// scratch contract, scratch.hpp:14-21, test_attention.cpp:182-205; kvmix_scratch_allocated
+// reports the bytes requested).
+//
+// The memory is persistent per (device, stream): an arena for partials (uninitialised) and
+// a zero-initialised buffer for arrival counters / flags, which the kernels return to zero
+// before they exit -- so no call pays an allocation, a memset or a clearing launch, and
+// calls on different streams never share scratch (concurrent readers). A call whose needs
+// exceed the current buffers takes stream-ordered allocations for the excess and records
+// the high-water mark; the next call on that stream grows the buffers (outside graph capture).
+struct ScratchPool;
 class Workspace {
  public:
-  Workspace() = default;
+  explicit Workspace(cudaStream_t st);
   Workspace(const Workspace&) = delete;
   Workspace& operator=(const Workspace&) = delete;
-  ~Workspace() {
-    for (auto& a : allocs_) cudaFreeAsync(a.first, a.second);
-  }
+  ~Workspace();
   template <typename T>
-  T* get(cudaStream_t st, size_t n) {
-    keep_pool();
-    void* p = nullptr;
-    check_cuda(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st), "cudaMallocAsync(workspace)");
-    allocs_.push_back({p, st});
-    bytes_ += n * sizeof(T);
-    return static_cast<T*>(p);
+  T* get(cudaStream_t, size_t n) {
+    return static_cast<T*>(take(std::max<size_t>(n, 1) * sizeof(T), false));
+  }
+  // zero on entry; the caller's kernels must leave it zero
+  template <typename T>
+  T* zeroed(size_t n) {
+    return static_cast<T*>(take(std::max<size_t>(n, 1) * sizeof(T), true));
   }
   float2* ml(cudaStream_t st, size_t n) { return get<float2>(st, n); }
   float* acc(cudaStream_t st, size_t n) { return get<float>(st, n); }
   double* cs(cudaStream_t st, size_t n) { return get<double>(st, n); }
   size_t bytes() const { return bytes_; }
 
-  // The default pool returns freed memory to the driver at every synchronization unless a
-  // release threshold is set; a decode loop that synchronizes per step would then remap
-  // its (tiny) scratch on every call (hundreds of microseconds). Keep it.
-  static void keep_pool() {
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    if (done_dev == dev) return;
-    cudaMemPool_t pool;
-    check_cuda(cudaDeviceGetDefaultMemPool(&pool, dev), "default mempool");
-    uint64_t thr = 256ull << 20;
-    check_cuda(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool threshold");
-    done_dev = dev;
-  }
-
  private:
-  std::vector<std::pair<void*, cudaStream_t>> allocs_;
+  void* take(size_t bytes, bool zero);
+  void grow();
+  cudaStream_t st_;
+  ScratchPool* pool_;
+  size_t off_[2] = {0, 0};  // bump offsets into the arena / the zeroed buffer
+  std::vector<void*> extra_;
   size_t bytes_ = 0;
 };
+
+// reference scratch counter (scratch.hpp:14-21): bytes of attention scratch requested
+void scratch_add(size_t bytes);
 
 void check_attend(const kvmix_cache* c, int q_heads, int t);
 // split count used by every attention path: ~4 CTAs per SM, independent of T

@@ -52,6 +52,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <string>
 
 #include "attention.cuh"
 
@@ -78,21 +79,13 @@ constexpr int kFlushBlocks = 1024;  // Value int32 accumulators: < 2^31 / (32 * 
 constexpr int kLazy = 3;
 constexpr int kEHead = 2;  // extra fixed-point headroom bits when the Value exponent is reset
 
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-
-// Epoch of one fused call: per-(b, kv-head) "append done" flags are published with it, so the
-// flag array needs no clearing (pool memory holds older epochs; the base is random).
-unsigned long long next_epoch() {
-  static std::atomic<unsigned long long> e{0x9e3779b97f4a7c15ull ^
-                                           (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count()};
-  return e.fetch_add(2) | 1ull;  // odd, distinct per call
 }
 
 // binary16 pair {scale (lo), min (hi)} of a meta word -> fp32
@@ -250,10 +243,12 @@ struct MmaParams {
   int want_cs;  // accumulate the double scores checksum (only when the caller asks)
   int fused;         // the call's 1-token append runs in the prologue (kvmix_append_attend)
   DecodeAppend da;
-  unsigned long long* flags;  // per (b, kv-head): epoch once its append is done
-  unsigned long long epoch;
-  unsigned long long* cnt;    // per (b, kv-head): {call tag, octets published} (merge by the last)
-  unsigned long long* cnt8;   // per (warp octet k, bh) at slot k + bh: {call tag, partials published}
+  // Arrival counters and flags live in zero-initialised scratch (Workspace::zeroed) and every
+  // launch leaves them zero again: the last arriver of a counter resets it, the final writer of
+  // a (pass, b, kv-head) resets its flag. No epochs or tags, so a launch is replayable.
+  unsigned* flags;  // per (pass, b, kv-head) at pass * nbh + bh: 1 once the append is done
+  unsigned* cnt;    // per (pass, b, kv-head): octets published (merge by the last)
+  unsigned* cnt8;   // per (pass, warp octet k, bh) at slot pass * pslots + k + bh: partials published
   float* out;
   int flush_blocks;  // fold the int32 Value accumulators at least every this many blocks
   int tail_unit;     // window tokens per work unit
@@ -270,6 +265,45 @@ constexpr int kTailUnit = 1;
 constexpr int kGroupCost = 1;  // cost of one fast group in window-token units (KVMIX_GROUP_COST)
 constexpr int kMaxPasses = 8;  // row passes per launch
 constexpr int kMinCost = 8;    // minimum cost units per warp (KVMIX_MIN_COST overrides)
+
+// Tuning / test knobs, read from the environment once per process.
+struct Knobs {
+  int tail_unit = kTailUnit, group_cost = kGroupCost, flush_blocks = kFlushBlocks, min_cost = kMinCost;
+  bool skip_tail = false, no_window = false;
+};
+Knobs& knobs() {
+  static Knobs k = [] {
+    Knobs x;
+    auto iv = [](const char* name, int lo, int hi, int dflt) {
+      const char* e = getenv(name);
+      return e ? std::max(lo, std::min(hi, atoi(e))) : dflt;
+    };
+    x.tail_unit = iv("KVMIX_TAIL_UNIT", 1, 64, kTailUnit);
+    x.group_cost = iv("KVMIX_GROUP_COST", 1, 64, kGroupCost);
+    x.flush_blocks = iv("KVMIX_TEST_FLUSH_BLOCKS", 1, kFlushBlocks, kFlushBlocks);
+    x.min_cost = iv("KVMIX_MIN_COST", 1, 1 << 20, kMinCost);
+    x.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
+    x.no_window = getenv("KVMIX_PROF_NO_WINDOW") != nullptr;
+    return x;
+  }();
+  return k;
+}
+
+}  // namespace
+
+// kvmix_set_knob (test / tuning hook): overrides one knob for later launches
+bool set_knob(const char* name, int v) {
+  Knobs& k = knobs();
+  const std::string n = name ? name : "";
+  if (n == "KVMIX_TAIL_UNIT") k.tail_unit = std::max(1, std::min(64, v));
+  else if (n == "KVMIX_GROUP_COST") k.group_cost = std::max(1, std::min(64, v));
+  else if (n == "KVMIX_TEST_FLUSH_BLOCKS") k.flush_blocks = std::max(1, std::min(kFlushBlocks, v <= 0 ? kFlushBlocks : v));
+  else if (n == "KVMIX_MIN_COST") k.min_cost = std::max(1, v);
+  else return false;
+  return true;
+}
+
+namespace {
 
 // first unit whose start cost is >= c (units: Gf groups of cost Qc, then window units of 1)
 __device__ __forceinline__ int unit_at_cost(const MmaParams& p, int64_t c) {
@@ -290,10 +324,10 @@ __device__ __forceinline__ float deq_lane(const SideView& s, int bh, int j, int 
   if (KEY) {
     const int grp = j / gs;
     m = s.meta[kmeta_index(s, bh, grp) + d];
-    if (BITS == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
+    if (BITS == 3) narrow = narrow_key(s.gbh(bh), d, D, s.info[grp], j - grp * gs);
   } else {
     m = s.meta[vmeta_index(s, bh, j) + d / gs];
-    if (BITS == 3) narrow = narrow_value(bh, d, D, s.info[j]);
+    if (BITS == 3) narrow = narrow_value(s.gbh(bh), d, D, s.info[j]);
   }
   return decode(code, meta_scale(m), meta_min(m), narrow);
 }
@@ -315,25 +349,14 @@ __device__ __forceinline__ void bh_warps(const MmaParams& p, int bh, int& w0, in
   w1 = warp_at_cost(p, s1);
 }
 
-// 64-bit CAS with acquire-release semantics at GPU scope
-__device__ __forceinline__ unsigned long long cas_acq_rel(unsigned long long* a, unsigned long long cmp,
-                                                          unsigned long long val) {
-  unsigned long long old;
-  asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;\n" : "=l"(old) : "l"(a), "l"(cmp), "l"(val) : "memory");
-  return old;
-}
-
-// Tagged arrival counter: returns true for the n-th arriver of this call (the word carries
-// the call's tag, so it needs no clearing between calls).
-__device__ __forceinline__ bool count_arrival(unsigned long long* cw, unsigned long long tag, int n) {
-  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cw), assumed;
-  unsigned int ct;
-  do {
-    assumed = old;
-    ct = (assumed >> 32) == tag ? (unsigned int)assumed : 0u;
-    old = cas_acq_rel(cw, assumed, (tag << 32) | (ct + 1u));
-  } while (old != assumed);
-  return (int)(ct + 1u) == n;
+// Arrival counter (zero at launch): returns true for the n-th arriver, which resets the word
+// to zero for the next launch (every arrival of this launch has happened).
+__device__ __forceinline__ bool count_arrival(unsigned* cw, int n) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(cw) : "memory");
+  if ((int)old + 1 != n) return false;
+  *reinterpret_cast<volatile unsigned*>(cw) = 0u;
+  return true;
 }
 
 // Publish this warp's partial of bh; returns true for the last of the bh's warps to arrive.
@@ -347,12 +370,11 @@ __device__ __forceinline__ bool arrive_last(const MmaParams& p, int bh, int lane
   if (lane == 0) {
     int w0, w1;
     bh_warps(p, bh, w0, w1);
-    const unsigned long long tag = p.epoch & 0xffffffffull;
     const int k = wg >> 3;
     const int a = max(w0, 8 * k), z = min(w1, 8 * k + 7);
-    last = z == a || count_arrival(p.cnt8 + (size_t)pass * p.pslots + k + bh, tag, z - a + 1);
+    last = z == a || count_arrival(p.cnt8 + (size_t)pass * p.pslots + k + bh, z - a + 1);
     const int nsub = (w1 >> 3) - (w0 >> 3) + 1;
-    if (last && nsub > 1) last = count_arrival(p.cnt + (size_t)pass * p.nbh + bh, tag, nsub);
+    if (last && nsub > 1) last = count_arrival(p.cnt + (size_t)pass * p.nbh + bh, nsub);
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   __syncwarp();
@@ -429,6 +451,8 @@ __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane, i
       o[3] = a.w * il;
     }
   }
+  // final writer of (pass, bh): every warp that waited on the append flag has arrived
+  if (p.fused && lane == 0) p.flags[(size_t)pass * p.nbh + bh] = 0u;
 }
 
 // Per-warp dynamic shared layout (bytes):
@@ -603,7 +627,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
         if ((bh + 1) * p.U > u_end || p.npass > 1) {  // other warps read this window too: publish
           __threadfence();
           __syncwarp();
-          if (lane == 0) st_release(p.flags + bh, p.epoch);
+          if (lane < p.npass) st_release(p.flags + (size_t)lane * p.nbh + bh, 1u);  // one flag per pass
         }
       }
     }
@@ -637,7 +661,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
     const int hi = min(u_end - bh * p.U, p.U);
     u = bh * p.U + hi;
     const int b = bh / p.H, h = bh % p.H;
-    const int cb11 = (int)(((unsigned)bh * (unsigned)D) % 11u);
+    const int cb11 = (int)(((unsigned)p.k.gbh(bh) * (unsigned)D) % 11u);  // global (b, kv-head)
     (void)cb11;
 
     // query rows at this lane's Key channels
@@ -1034,7 +1058,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
     // (Keys: lane = token fp32 dot products from the ring; Values: the IMMA block path on the
     // partial group's tiles). Waits for the fused append when an earlier warp made it.
     if (p.fused && (lo > p.Gf || pass != 0) && hi > p.Gf) {
-      while (ld_acquire(p.flags + bh) != p.epoch) __nanosleep(32);
+      while (ld_acquire(p.flags + (size_t)pass * p.nbh + bh) == 0u) __nanosleep(32);
     }
     if constexpr (R == 1) {
       const int wb_lo = max(lo, p.Gf) - p.Gf, wb_hi = min(hi, p.Gf + p.nwb) - p.Gf;
@@ -1273,6 +1297,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
           for (int c = 0; c < LC; ++c) o[c] = acct[r][c] * il;
         }
       }
+      if (p.fused && lane == 0) p.flags[(size_t)pass * p.nbh + bh] = 0u;  // final writer of (pass, bh)
     } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -1325,12 +1350,18 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   }
   p.stages = stages;
   const size_t smem = (size_t)kMmaWarps * WL::bytes(p.stages, p.stage_bytes);
-  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  // per device: the dynamic shared memory attribute and the residency at this ring size are
+  // set / queried once (host cost per call is a few table lookups)
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  static thread_local int occ_dev = -1;
   static thread_local size_t occ_smem = 0;
   static thread_local int occ = 0;
-  if (occ_smem != smem) {  // residency of this instantiation at this ring size (cached)
+  if (occ_smem != smem || occ_dev != dev) {
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMmaWarps * 32, smem), "occupancy");
     occ_smem = smem;
+    occ_dev = dev;
   }
   // one resident wave of independent warps (persistent): equal unit ranges, no stragglers;
   // never more warps than units so every range is non-empty
@@ -1338,8 +1369,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   const int64_t wave = (int64_t)std::max(1, occ) * num_sms() * kMmaWarps;
   // small problems: at least kMinCost cost units per warp (a warp's prologue and the merge
   // of a head split over many warps cost more than a few groups)
-  int64_t min_cost = kMinCost;
-  if (const char* e = getenv("KVMIX_MIN_COST")) min_cost = std::max(1, atoi(e));
+  const int64_t min_cost = knobs().min_cost;
   const int64_t w_cap = std::max<int64_t>(1, p.Nc / min_cost);
   p.W = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(p.N, wave / p.npass), w_cap));
   // partial slots x * pslots + w + bh (w + bh < W + BH): scratch depends on (B, H, rows, D,
@@ -1350,9 +1380,9 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.part_ml = ws.ml(st, slots * p.rows);
   p.part_acc = ws.acc(st, slots * p.rows * D);
   p.part_cs = ws.cs(st, slots + 1);
-  p.cnt = ws.get<unsigned long long>(st, (size_t)p.npass * BH);
-  p.cnt8 = ws.get<unsigned long long>(st, slots);
-  if (p.fused) p.flags = ws.get<unsigned long long>(st, (size_t)BH);
+  p.cnt = ws.zeroed<unsigned>((size_t)p.npass * BH);
+  p.cnt8 = ws.zeroed<unsigned>(slots);
+  p.flags = p.fused ? ws.zeroed<unsigned>((size_t)p.npass * BH) : nullptr;
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
   const int64_t warps = (int64_t)p.W * p.npass;
   kern<<<(unsigned)((warps + kMmaWarps - 1) / kMmaWarps), kMmaWarps * 32, smem, st>>>(p);
@@ -1427,13 +1457,11 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.inv = 1.0f / sqrtf((float)D);
   p.want_cs = checksum != nullptr;
   p.out = out;
-  p.tail_unit = kTailUnit;
-  p.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
-  if (const char* e = getenv("KVMIX_TAIL_UNIT")) p.tail_unit = std::max(1, std::min(64, atoi(e)));
-  p.Qc = kGroupCost;
-  if (const char* e = getenv("KVMIX_GROUP_COST")) p.Qc = std::max(1, std::min(64, atoi(e)));
-  p.flush_blocks = kFlushBlocks;
-  if (const char* e = getenv("KVMIX_TEST_FLUSH_BLOCKS")) p.flush_blocks = std::max(1, std::min(kFlushBlocks, atoi(e)));
+  const Knobs kn = knobs();
+  p.tail_unit = kn.tail_unit;
+  p.skip_tail = kn.skip_tail;
+  p.Qc = kn.group_cost;
+  p.flush_blocks = kn.flush_blocks;
   if (da) {  // fused append: only if the aged Value token is outside the fast groups
     if (da->v_age && da->v_j < p.P) return false;
     if (T <= p.P) return false;  // (cannot happen after an append: the new Key is in the window)
@@ -1442,7 +1470,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   auto layout = [&](int nrows) {
     p.Pw = p.P;
     p.nwb = 0;
-    if (nrows == 1 && c->k.quantized == p.P && !getenv("KVMIX_PROF_NO_WINDOW")) {
+    if (nrows == 1 && c->k.quantized == p.P && !kn.no_window) {
       p.Pw = std::min(T, c->v.quantized);
       if (p.Pw > p.P) p.nwb = (int)((p.Pw - p.P + 31) / 32);
       else p.Pw = p.P;
@@ -1463,7 +1491,6 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     p.N = BH * p.U;
     p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
     p.Nc = (int64_t)BH * p.cost_bh;
-    p.epoch = next_epoch();
     p.fused = 0;
     if (da && r0 == 0) {  // the first launch runs the append; later launches follow in stream order
       p.fused = 1;

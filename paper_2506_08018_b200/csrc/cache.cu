@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       a.k_meta[kmeta_index(a.kv, bh, gglob) + d] = m;
       const float sc = meta_scale(m), mnv = meta_min(m);
       // reference stream index inside this segment [B,H,n,D]: (bh*D + d)*n + t_local
-      const uint64_t sbase = ((uint64_t)bh * D + d) * (uint64_t)a.k_n + (uint64_t)j0;
+      const uint64_t sbase = ((uint64_t)a.kv.gbh(bh) * D + d) * (uint64_t)a.k_n + (uint64_t)j0;
       for (int jj = 0; jj < gs; ++jj) {
         const float x = xs[jj * D + d];
         codes[jj * D + d] = (uint8_t)encode(x, sc, mnv, a.kbits, is_narrow(a.kbits, sbase + jj));
@@ -245,18 +245,8 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     const int q_max = q_max_for_bits(a.vbits);
     float x[4];
     for (int c = 0; c < LC; ++c) x[c] = src.at(bh, tl, lane * LC + c, D);
-    float mn = x[0], mx = x[0];
-    for (int c = 1; c < LC; ++c) {
-      mn = x[c] < mn ? x[c] : mn;
-      mx = x[c] > mx ? x[c] : mx;
-    }
     const int glanes = min(gs, D) / LC;  // lanes per channel group (power of two)
-    for (int o = 1; o < glanes; o <<= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, mn, o), ox = __shfl_xor_sync(0xffffffffu, mx, o);
-      mn = om < mn ? om : mn;
-      mx = ox > mx ? ox : mx;
-    }
-    const uint32_t m = make_meta(mn, mx, q_max);
+    const uint32_t m = group_meta_warp(x, LC, glanes, lane, q_max);
     const int g0 = lane * LC / gs;
     if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + g0] = m;
     if (bh == 0 && lane == 0) a.v_info[j] = make_int2((int)a.v_n, (int)tl);
@@ -264,7 +254,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
     for (int c = 0; c < LC; ++c) {
       const int d = lane * LC + c;
-      const uint64_t si = ((uint64_t)bh * a.v_n + (uint64_t)tl) * D + d;
+      const uint64_t si = ((uint64_t)a.vv.gbh(bh) * a.v_n + (uint64_t)tl) * D + d;
       tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
     }
     return;
@@ -306,7 +296,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       const int i = i_lo + e / D, d = e % D;
       const uint32_t m = mrow[i * cg + d / gs];
       const int64_t tl = tile * 16 + i - a.v_q0;  // token index inside the segment
-      const uint64_t si = ((uint64_t)bh * a.v_n + (uint64_t)tl) * D + d;
+      const uint64_t si = ((uint64_t)a.vv.gbh(bh) * a.v_n + (uint64_t)tl) * D + d;
       codes[i * D + d] = (uint8_t)encode(xs[i * Dp + d], meta_scale(m), meta_min(m), a.vbits, is_narrow(a.vbits, si));
     }
     if (bh == 0) {
@@ -695,8 +685,12 @@ static int64_t seg_start(const kvmix_cache::Side& s, int idx) {
   return S;
 }
 
+static bool sharded(const kvmix_cache* c) { return c->k.Hg != c->H || c->k.b0 != 0 || c->k.h0 != 0; }
+
 void cache_export_segment(const kvmix_cache* c, int side, int idx, uint32_t* words, uint16_t* meta, cudaStream_t st) {
   const auto& s = side == 0 ? c->k : c->v;
+  if (s.bits == 3 && sharded(c) && words)
+    invalid("export: the Mixed3 words of a sharded cache follow the global stream index; gather the shards");
   if (idx < 0 || idx >= (int)s.segs.size()) throw Error(KVMIX_OUT_OF_RANGE, "segment index out of range");
   const int64_t S = seg_start(s, idx), n = s.segs[idx];
   const int BH = c->B * c->H;
@@ -726,6 +720,7 @@ void cache_export_tail(const kvmix_cache* c, int side, float* out, cudaStream_t 
 void cache_import_segment(kvmix_cache* c, int side, int t, const uint32_t* words, const uint16_t* meta, cudaStream_t st) {
   auto& s = side == 0 ? c->k : c->v;
   const int gs = c->cfg.group_size;
+  if (s.bits == 3 && sharded(c)) invalid("import: Mixed3 segments cannot be imported into a sharded cache");
   if (t < 1) invalid("import: empty segment");
   if (side == 0 && (t % gs != 0)) invalid("import: key segment length must be a multiple of group_size");
   if (s.tail_len != 0) invalid("import: segments must be imported before the tail");

@@ -31,6 +31,10 @@ struct kvmix_cache {
     int2* info = nullptr;
     size_t tile_words = 0, bh_stride = 0, grp_stride = 0;  // words
     int tpg = 0, mrow = 0;  // tiles per group; meta words per Key group / per Value token
+    // shard placement (kvmix_cache_set_shard): this cache holds heads [h0, h0 + H) of batch
+    // rows [b0, b0 + B) of a [Bg, Hg] model batch; Mixed3 narrow slots follow the GLOBAL
+    // (b, h) stream index, so a shard holds exactly the unsharded cache's slice
+    int Hl = 1, Hg = 1, b0 = 0, h0 = 0;
   };
   kvmix_layer_config cfg{};
   int B = 0, H = 0, D = 0;
@@ -56,11 +60,14 @@ struct SideView {
   int bits;
   size_t tile_words, bh_stride, grp_stride;
   int tpg, mrow;
+  int Hl, Hg, b0, h0;  // shard placement (Side)
+  // global (b, kv-head) index of local bh: the one the reference's stream index uses
+  __host__ __device__ int gbh(int bh) const { return (b0 + bh / Hl) * Hg + h0 + bh % Hl; }
 };
 
 inline SideView view(const kvmix_cache::Side& s) {
   return SideView{s.tiles, s.meta, s.tail, s.info, s.tail_cap, s.tail_start, s.tail_len, s.quantized,
-                  s.bits, s.tile_words, s.bh_stride, s.grp_stride, s.tpg, s.mrow};
+                  s.bits, s.tile_words, s.bh_stride, s.grp_stride, s.tpg, s.mrow, s.Hl, s.Hg, s.b0, s.h0};
 }
 
 // Word offsets into a side's tiles / meta (group-record layout above).
@@ -87,7 +94,8 @@ __device__ inline float tail_at(const SideView& s, int bh, int64_t j, int d, int
 }
 
 // Narrow-slot test for the Mixed3 layout from the segment info, in mod-11 arithmetic
-// (stream index = (bh*D + d)*n + t_local for Keys, (bh*n + t_local)*D + d for Values).
+// (stream index = (bh*D + d)*n + t_local for Keys, (bh*n + t_local)*D + d for Values; bh is
+// the GLOBAL (b, kv-head) index, SideView::gbh).
 __device__ inline bool narrow_key(int bh, int d, int D, int2 info, int t_in_group) {
   const int c = (int)(((unsigned)bh * (unsigned)D + (unsigned)d) % 11u);
   return (c * (info.x % 11) + (info.y + t_in_group) % 11) % 11 == 10;
@@ -108,10 +116,10 @@ __device__ inline float packed_value(bool key, const SideView& s, int bh, int64_
   if (key) {
     const int grp = j / gs;
     m = s.meta[kmeta_index(s, bh, grp) + d];
-    if (s.bits == 3) narrow = narrow_key(bh, d, D, s.info[grp], j - grp * gs);
+    if (s.bits == 3) narrow = narrow_key(s.gbh(bh), d, D, s.info[grp], j - grp * gs);
   } else {
     m = s.meta[vmeta_index(s, bh, j) + d / gs];
-    if (s.bits == 3) narrow = narrow_value(bh, d, D, s.info[j]);
+    if (s.bits == 3) narrow = narrow_value(s.gbh(bh), d, D, s.info[j]);
   }
   return decode(code, meta_scale(m), meta_min(m), narrow);
 }
@@ -139,6 +147,30 @@ struct DecodeAppend {
   int2* v_info;
   SideView vv;
 };
+
+// Meta of one Value channel group spread over `glanes` consecutive lanes (power of two) with
+// LC channels per lane in stream order: the ordered fold over the lanes' segments (the lower
+// lane holds the earlier segment), then the leader's result broadcast so every lane of the
+// group encodes with the stored meta.
+template <int LCMAX>
+__device__ inline uint32_t group_meta_warp(const float (&x)[LCMAX], int LC, int glanes, int lane, int q_max) {
+  float mn = NAN, mx = NAN;
+  for (int c = 0; c < LC; ++c) {
+    mn = fold_min(mn, x[c]);
+    mx = fold_max(mx, x[c]);
+  }
+  for (int o = 1; o < glanes; o <<= 1) {
+    const float omn = __shfl_xor_sync(0xffffffffu, mn, o), omx = __shfl_xor_sync(0xffffffffu, mx, o);
+    const bool hi = lane & o;  // the partner holds the earlier segment
+    const float fmn = hi ? fold_min(omn, mn) : fold_min(mn, omn);
+    const float fmx = hi ? fold_max(omx, mx) : fold_max(mx, omx);
+    mn = fmn;
+    mx = fmx;
+  }
+  const int lead = lane & ~(glanes - 1);
+  if (__shfl_sync(0xffffffffu, isnan(x[0]) ? 1 : 0, lead)) mn = mx = NAN;  // NaN first element
+  return __shfl_sync(0xffffffffu, make_meta(mn, mx, q_max), lead);
+}
 
 __device__ inline float da_load(const void* p, bool f16, size_t i) {
   return f16 ? __half2float(static_cast<const __half*>(p)[i]) : static_cast<const float*>(p)[i];
@@ -169,18 +201,8 @@ __device__ inline void decode_append_warp(const DecodeAppend& a, int bh, int lan
                        : (a.tail16 ? __half2float(__float2half_rn(da_load(a.vin, a.in16, (size_t)bh * D + d)))
                                    : da_load(a.vin, a.in16, (size_t)bh * D + d));
     }
-    float mn = x[0], mx = x[0];
-    for (int c = 1; c < LC; ++c) {
-      mn = x[c] < mn ? x[c] : mn;
-      mx = x[c] > mx ? x[c] : mx;
-    }
     const int glanes = min(gs, D) / LC;
-    for (int o = 1; o < glanes; o <<= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, mn, o), ox = __shfl_xor_sync(0xffffffffu, mx, o);
-      mn = om < mn ? om : mn;
-      mx = ox > mx ? ox : mx;
-    }
-    const uint32_t m = make_meta(mn, mx, q_max);
+    const uint32_t m = group_meta_warp(x, LC, glanes, lane, q_max);
     const int64_t j = a.v_j;
     if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + lane * LC / gs] = m;
     if (bh == 0 && lane == 0) a.v_info[j] = make_int2(1, 0);
@@ -188,7 +210,7 @@ __device__ inline void decode_append_warp(const DecodeAppend& a, int bh, int lan
     uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
     for (int c = 0; c < LC; ++c) {
       const int d = lane * LC + c;
-      const uint64_t si = (uint64_t)bh * D + d;  // segment [B,H,1,D]
+      const uint64_t si = (uint64_t)a.vv.gbh(bh) * D + d;  // segment [B,H,1,D], global bh
       tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
     }
   }

@@ -33,6 +33,7 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
               uint32_t* words, uint16_t* meta, cudaStream_t st);
 void dequantize(kvmix_grouping grouping, const uint32_t* words, const uint16_t* meta, int B, int H, int T, int D,
                 int bits, int gs, float* out, cudaStream_t st);
+bool set_knob(const char* name, int v);
 void pack(const uint32_t* codes, size_t n, int bits, uint32_t* words, cudaStream_t st);
 void unpack(const uint32_t* words, size_t n, int bits, uint32_t* codes, cudaStream_t st);
 
@@ -73,17 +74,26 @@ void alloc(void** p, size_t bytes) {
 
 void free_cache(kvmix_cache* c) {
   if (!c) return;
+  int prev = -1;  // (no throwing here: destroy is not status-returning)
+  if (cudaGetDevice(&prev) == cudaSuccess && prev != c->device) cudaSetDevice(c->device);
+  else prev = -1;
   for (auto* s : {&c->k, &c->v}) {
     cudaFree(s->tail);
     cudaFree(s->info);
   }
   cudaFree(c->rec);
   delete c;
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
 void check_cache(const kvmix_cache* c) {
   if (!c) invalid("null cache handle");
 }
+
+// every cache entry point runs on the cache's device (the caller's current device is restored)
+#define KVB_ON_CACHE_DEVICE(c) \
+  check_cache(c);              \
+  DeviceGuard dev_guard_((c)->device)
 }  // namespace
 
 }  // namespace kvb
@@ -95,6 +105,12 @@ extern "C" {
 const char* kvmix_last_error(void) { return g_err.c_str(); }
 int kvmix_abi_version(void) { return KVMIX_B200_ABI_VERSION; }
 uint64_t kvmix_launch_count(void) { return g_launches.load(); }
+
+kvmix_status kvmix_set_knob(const char* name, int value) {
+  return guard([&] {
+    if (!set_knob(name, value)) invalid(std::string("unknown knob ") + (name ? name : "(null)"));
+  });
+}
 
 uint64_t kvmix_launch_count_of(const char* kernel) {
   std::lock_guard<std::mutex> lk(kvb::g_names_mu);
@@ -203,6 +219,7 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
       // window bound: floor(r*cap) (+ gs-1 for whole-group key aging) plus decode slack
       const int64_t bound = (int64_t)std::floor((double)sp.r * (double)capacity_tokens) + (sp.key ? gs : 1);
       s.tail_cap = std::min<int64_t>(capacity_tokens, bound) + 64;
+      s.Hl = s.Hg = heads;
       if (sp.key) alloc((void**)&s.info, sizeof(int2) * (size_t)ngroups);
       else alloc((void**)&s.info, sizeof(int2) * (size_t)capacity_tokens);
       alloc(&s.tail, BH * (size_t)s.tail_cap * head_dim * esz);
@@ -218,16 +235,35 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
 
 void kvmix_cache_destroy(kvmix_cache* c) { free_cache(c); }
 
-kvmix_status kvmix_cache_reset(kvmix_cache* c, void* stream) {
+kvmix_status kvmix_cache_set_shard(kvmix_cache* c, int global_batch, int global_heads, int batch_offset,
+                                   int head_offset) {
   return guard([&] {
     check_cache(c);
+    if (c->total() != 0 || !c->k.segs.empty() || !c->v.segs.empty())
+      invalid("set_shard: the shard placement must be set before the first append");
+    if (batch_offset < 0 || head_offset < 0 || batch_offset + c->B > global_batch || head_offset + c->H > global_heads)
+      invalid("set_shard: shard [" + std::to_string(batch_offset) + ", " + std::to_string(batch_offset + c->B) + ") x [" +
+              std::to_string(head_offset) + ", " + std::to_string(head_offset + c->H) + ") outside the global batch " +
+              std::to_string(global_batch) + " x heads " + std::to_string(global_heads));
+    for (auto* s : {&c->k, &c->v}) {
+      s->Hl = c->H;
+      s->Hg = global_heads;
+      s->b0 = batch_offset;
+      s->h0 = head_offset;
+    }
+  });
+}
+
+kvmix_status kvmix_cache_reset(kvmix_cache* c, void* stream) {
+  return guard([&] {
+    KVB_ON_CACHE_DEVICE(c);
     cache_reset(c, as_stream(stream));
   });
 }
 
 kvmix_status kvmix_cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, int t, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     cache_append(c, k, v, dt, t, as_stream(stream));
   });
 }
@@ -293,7 +329,7 @@ kvmix_status kvmix_cache_algorithmic_bytes(const kvmix_cache* c, uint64_t* out) 
 
 kvmix_status kvmix_cache_snapshot(const kvmix_cache* c, float* keys, float* values, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     cache_snapshot(c, keys, values, as_stream(stream));
   });
 }
@@ -315,7 +351,7 @@ kvmix_status kvmix_cache_segment_info(const kvmix_cache* c, int side, int idx, i
 kvmix_status kvmix_cache_export_segment(const kvmix_cache* c, int side, int idx, uint32_t* words, uint16_t* meta,
                                         void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     if (side != 0 && side != 1) invalid("side must be 0 (keys) or 1 (values)");
     cache_export_segment(c, side, idx, words, meta, as_stream(stream));
   });
@@ -323,7 +359,7 @@ kvmix_status kvmix_cache_export_segment(const kvmix_cache* c, int side, int idx,
 
 kvmix_status kvmix_cache_export_tail(const kvmix_cache* c, int side, float* out, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     if (side != 0 && side != 1) invalid("side must be 0 (keys) or 1 (values)");
     cache_export_tail(c, side, out, as_stream(stream));
   });
@@ -332,7 +368,7 @@ kvmix_status kvmix_cache_export_tail(const kvmix_cache* c, int side, float* out,
 kvmix_status kvmix_cache_import_segment(kvmix_cache* c, int side, int t, const uint32_t* words, const uint16_t* meta,
                                         void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     if (side != 0 && side != 1) invalid("side must be 0 (keys) or 1 (values)");
     cache_import_segment(c, side, t, words, meta, as_stream(stream));
   });
@@ -340,7 +376,7 @@ kvmix_status kvmix_cache_import_segment(kvmix_cache* c, int side, int t, const u
 
 kvmix_status kvmix_cache_import_tail(kvmix_cache* c, int side, const float* tail, int64_t t, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     if (side != 0 && side != 1) invalid("side must be 0 (keys) or 1 (values)");
     cache_import_tail(c, side, tail, t, as_stream(stream));
   });
@@ -349,9 +385,9 @@ kvmix_status kvmix_cache_import_tail(kvmix_cache* c, int side, const float* tail
 kvmix_status kvmix_attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, int q_heads, int t, float* out,
                           double* checksum, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     if (dt != KVMIX_F32 && dt != KVMIX_F16) invalid("unsupported dtype");
-    Workspace ws;
+    Workspace ws(as_stream(stream));
     attend(c, q, dt, q_heads, t, out, checksum, ws, as_stream(stream));
   });
 }
@@ -359,9 +395,9 @@ kvmix_status kvmix_attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, i
 kvmix_status kvmix_append_attend(kvmix_cache* c, const void* k, const void* v, kvmix_dtype kv_dt, int t, const void* q,
                                  kvmix_dtype q_dt, int q_heads, int tq, float* out, double* checksum, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     if (q_dt != KVMIX_F32 && q_dt != KVMIX_F16) invalid("unsupported dtype");
-    Workspace ws;
+    Workspace ws(as_stream(stream));
     append_attend(c, k, v, kv_dt, t, q, q_dt, q_heads, tq, out, checksum, ws, as_stream(stream));
   });
 }
@@ -371,9 +407,23 @@ kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const
   return guard([&] {
     if (n_layers < 0) invalid("n_layers must be non-negative");
     for (int l = 0; l < n_layers; ++l) {
-      check_cache(caches[l]);
-      Workspace ws;
+      KVB_ON_CACHE_DEVICE(caches[l]);
+      Workspace ws(as_stream(stream));
       attend(caches[l], q[l], dt, q_heads, t, out[l], nullptr, ws, as_stream(stream));
+    }
+  });
+}
+
+kvmix_status kvmix_append_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* k,
+                                        const void* const* v, kvmix_dtype kv_dt, int t, const void* const* q,
+                                        kvmix_dtype q_dt, int q_heads, int tq, float* const* out, void* stream) {
+  return guard([&] {
+    if (n_layers < 0) invalid("n_layers must be non-negative");
+    if (q_dt != KVMIX_F32 && q_dt != KVMIX_F16) invalid("unsupported dtype");
+    for (int l = 0; l < n_layers; ++l) {
+      KVB_ON_CACHE_DEVICE(caches[l]);
+      Workspace ws(as_stream(stream));
+      append_attend(caches[l], k[l], v[l], kv_dt, t, q[l], q_dt, q_heads, tq, out[l], nullptr, ws, as_stream(stream));
     }
   });
 }
@@ -381,7 +431,7 @@ kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const
 kvmix_status kvmix_fused_qk_scores(const kvmix_cache* c, const void* q, kvmix_dtype dt, int t, float* scores,
                                    void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     fused_qk_scores(c, q, dt, t, scores, as_stream(stream));
   });
 }
@@ -392,7 +442,7 @@ kvmix_status kvmix_softmax_rows(float* scores, int64_t rows, int64_t cols, void*
 
 kvmix_status kvmix_fused_pv(const kvmix_cache* c, const float* probs, int t, float* out, void* stream) {
   return guard([&] {
-    check_cache(c);
+    KVB_ON_CACHE_DEVICE(c);
     fused_pv(c, probs, t, out, as_stream(stream));
   });
 }
@@ -400,8 +450,8 @@ kvmix_status kvmix_fused_pv(const kvmix_cache* c, const float* probs, int t, flo
 kvmix_status kvmix_reference_attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, int t, float* scratch,
                                     float* out, double* checksum, void* stream) {
   return guard([&] {
-    check_cache(c);
-    Workspace ws;
+    KVB_ON_CACHE_DEVICE(c);
+    Workspace ws(as_stream(stream));
     reference_attend(c, q, dt, t, scratch, out, checksum, ws, as_stream(stream));
   });
 }

@@ -60,6 +60,14 @@ __device__ inline uint32_t make_meta(float mn, float mx, int q_max) {
   const uint16_t sh = h16_bits(__fdiv_rn(__fsub_rn(mx, mn), (float)q_max));
   return (uint32_t)sh | ((uint32_t)mh << 16);
 }
+// The reference's group fold (quant.hpp:128-139, :170-182): mn = x0, then mn = v < mn ? v : mn
+// in stream order -- a NaN first element makes the meta NaN, a later NaN is skipped, and among
+// equal extrema (-0 / +0) the first occurrence wins. fold_min / fold_max start from NaN and
+// skip NaNs keeping first occurrences; segments combine in stream order; the NaN-first rule
+// is applied by the caller.
+__device__ __forceinline__ float fold_min(float a, float b) { return (isnan(a) || b < a) ? b : a; }
+__device__ __forceinline__ float fold_max(float a, float b) { return (isnan(a) || b > a) ? b : a; }
+
 __device__ inline float meta_scale(uint32_t m) { return h16_float((uint16_t)(m & 0xffffu)); }
 __device__ inline float meta_min(uint32_t m) { return h16_float((uint16_t)(m >> 16)); }
 
@@ -325,14 +333,27 @@ __device__ inline __half from_f<__half>(float x) { return __float2half_rn(x); }
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// SM count of the current device (cached per device)
 inline int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    check_cuda(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  }
-  return n;
+  static int n[64] = {};
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= 64) invalid("device ordinal out of range");
+  if (n[dev] == 0) check_cuda(cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev), "sm count");
+  return n[dev];
 }
+
+// Switches to a cache's device for the duration of a C ABI call (restores the caller's).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 }  // namespace kvb

@@ -373,8 +373,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
 // (mn = v < mn ? v : mn from the first element, quant.hpp:93-98 callers) is reproduced
 // exactly: lanes fold their values skipping NaN, segments combine in order keeping the
 // earlier of equal values, and a NaN first element makes the result NaN.
-__device__ __forceinline__ float fold_min(float a, float b) { return (isnan(a) || b < a) ? b : a; }
-__device__ __forceinline__ float fold_max(float a, float b) { return (isnan(a) || b > a) ? b : a; }
+// (fold_min / fold_max: common.cuh)
 
 template <typename T, int N>
 __device__ __forceinline__ void load_n(const T* p, float (&o)[N]) {

@@ -122,7 +122,15 @@ class PackedBuffer:
         """Bounds-checked read (bitpack.cpp:69-82)."""
         if idx < 0 or idx >= self.logical_len:
             raise KvmixOutOfRange(f"PackedBuffer::get: index {idx} out of bounds (logical_len {self.logical_len})")
-        return int(unpack(self)[idx])
+        # one word read (bitpack.cpp:69-82 field arithmetic), not an unpack of the buffer
+        if self.bits == 3:
+            w, pos = divmod(idx, kMixed3Block)
+            shift, mask = (30, 3) if pos == kMixed3Block - 1 else (3 * pos, 7)
+        else:
+            w, pos = divmod(idx, 32 // self.bits)
+            shift, mask = pos * self.bits, (1 << self.bits) - 1
+        word = int(self.words[w].item()) & 0xFFFFFFFF
+        return (word >> shift) & mask
 
 
 def _pack(codes, bits: int, layout: PackLayout) -> PackedBuffer:
@@ -210,7 +218,18 @@ class QuantizedGroups:
         return out
 
     def value_at(self, bi: int, hi: int, ti: int, di: int) -> float:
-        return float(self.dequantize()[bi, hi, ti, di])
+        """value_at (quant.cpp:97-100): one code and one meta pair read, decode_code
+        (quant.cpp:49-53) in fp32 -- code * scale' then + min, two rounded operations."""
+        s = self.shape
+        if not (0 <= bi < s.b and 0 <= hi < s.nh and 0 <= ti < s.t and 0 <= di < s.d):
+            raise KvmixOutOfRange("QuantizedGroups::value_at: index out of range")
+        si = self.stream_index(bi, hi, ti, di)
+        code = self.codes.get(si)
+        pair = self.meta[self.meta_index(bi, hi, ti, di)].cpu().numpy().view(np.float16).astype(np.float32)
+        scale, mn = np.float32(pair[0]), np.float32(pair[1])
+        if self.spec.bits == 3 and si % kMixed3Block == kMixed3Block - 1:
+            scale = np.float32(scale * np.float32(7.0 / 3.0))
+        return float(np.float32(np.float32(code) * scale) + mn)
 
 
 def _quantize(x, spec: QuantSpec, grouping: Grouping) -> QuantizedGroups:
@@ -225,8 +244,9 @@ def _quantize(x, spec: QuantSpec, grouping: Grouping) -> QuantizedGroups:
     n = B * H * T * D
     nw = packed_word_count(n, spec.bits)
     ng = int(lib().kvmix_group_count(int(grouping), B, H, T, D, spec.group_size)) if spec.group_size > 0 else 0
-    words = torch.zeros(max(1, nw), dtype=torch.int32, device=x.device)
-    meta = torch.zeros((max(1, ng), 2), dtype=torch.int16, device=x.device)
+    # the kernels write every word and every meta pair: no zero fill
+    words = torch.empty(max(1, nw), dtype=torch.int32, device=x.device)
+    meta = torch.empty((max(1, ng), 2), dtype=torch.int16, device=x.device)
     check(lib().kvmix_quantize(int(grouping), _ptr(x), _dtype_code(x), B, H, T, D, spec.bits, spec.group_size,
                                _ptr(words), _ptr(meta), _stream()))
     layout = PackLayout.kMixed3 if spec.bits == 3 else PackLayout.kUniform

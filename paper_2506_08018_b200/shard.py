@@ -2,9 +2,12 @@
 
 Every (b, kv-head) pair's append and attend touch only its own packed store and
 full-precision window, and the shrink rule is uniform across (b, h), so a rank holding a
-shard replays identical host bookkeeping and needs no data-path collective. Query heads
-travel with their KV head (GQA). The only exchange is the optional all-gather of the
-attention output for a downstream projection (one [B, Hq, t, D] tensor per layer).
+shard replays identical host bookkeeping and needs no data-path collective. One thing is
+NOT local: the reference's Mixed3 narrow slots (3-bit layers) are a function of the global
+stream index (quant.cpp:36-47, 77-95), so a shard's cache is placed in the global batch
+(ShardPlan.place -> kvmix_cache_set_shard) to hold the unsharded cache's slice bit for bit.
+Query heads travel with their KV head (GQA). The only exchange is the optional all-gather of
+the attention output for a downstream projection (one [B, Hq, t, D] tensor per layer).
 """
 from __future__ import annotations
 
@@ -86,3 +89,9 @@ class ShardPlan:
         for (b0, b1, h0, h1), t in zip(parts, buf):
             out[b0:b1, h0 * self.G:h1 * self.G] = t[:b1 - b0, :(h1 - h0) * self.G]
         return out
+
+    def place(self, cache) -> None:
+        """Mark a freshly created device cache as this rank's slice (kvmix_cache_set_shard):
+        its Mixed3 narrow slots then follow the global stream index, so the shard holds the
+        unsharded cache's slice bit for bit (also for 3-bit layers)."""
+        cache.set_shard(self.B, self.H, self.b0, self.h0)

@@ -20,8 +20,8 @@ import paper_2506_08018_b200 as K
 
 pytestmark = pytest.mark.gpu
 
-ATTN_TOL_F64 = 2e-5
-ATTN_TOL_F32 = 4e-5
+ATTN_TOL_F64 = 2e-6
+ATTN_TOL_F32 = 4e-6
 CHECKSUM_RTOL = 2e-7
 
 
@@ -149,14 +149,18 @@ def test_attend_scale_ramp(cuda):
         check_attend(dev, ora, q, expect_mma=True)
 
 
-def test_attend_forced_folds(cuda, monkeypatch):
+def test_attend_forced_folds(cuda):
     """The int32 Value accumulators are folded every N blocks (N = 1024 in production,
     lowered here so that path runs): same result within the stated tolerance."""
+    from paper_2506_08018_b200 import _lib
     dev, ora = build(2, 2, 0.1, 0.1, 32, 1, 2, 128, [2000] + [1] * 5, seed=17)
     q = O.random_h16(18, (1, 2, 1, 128), sigma=2.0)
-    for n in ("1", "3"):
-        monkeypatch.setenv("KVMIX_TEST_FLUSH_BLOCKS", n)
-        check_attend(dev, ora, q, expect_mma=True)
+    try:
+        for n in (1, 3):
+            _lib.set_knob("KVMIX_TEST_FLUSH_BLOCKS", n)
+            check_attend(dev, ora, q, expect_mma=True)
+    finally:
+        _lib.set_knob("KVMIX_TEST_FLUSH_BLOCKS", 0)
 
 
 def test_attend_d64_two_rows(cuda):

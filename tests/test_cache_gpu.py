@@ -207,3 +207,64 @@ def test_against_compiled_reference(cuda):
         dev.append(k, v)
         ref.append(k, v)
     assert dev.dump() == ref.dump()
+
+
+def _special_token(rng, B, H, D, step):
+    """One [B,H,1,D] token on the binary16 grid with NaN / +-0 / inf / tiny values placed at
+    the group first element and at the first element of a non-leader lane's slice."""
+    x = O.random_h16(1000 + step, (B, H, 1, D))
+    kind = step % 6
+    for h in range(H):
+        if kind == 0:
+            x[0, h, 0, 4] = np.nan          # first element of lane 1's slice (channels 4..7)
+            x[0, h, 0, 5] = -30.0           # only visible if the fold skips the NaN and goes on
+        elif kind == 1:
+            x[0, h, 0, 0] = np.nan          # group first element: meta NaN
+        elif kind == 2:
+            x[0, h, 0, :32] = 0.0
+            x[0, h, 0, 3] = -0.0            # zero extrema: the first occurrence's sign wins
+            x[0, h, 0, 9] = -0.0
+        elif kind == 3:
+            x[0, h, 0, 0] = -0.0
+            x[0, h, 0, 1:32] = np.abs(x[0, h, 0, 1:32])
+        elif kind == 4:
+            x[0, h, 0, 36] = np.inf
+            x[0, h, 0, 40] = np.nan
+        else:
+            x[0, h, 0, 64] = np.nan
+            x[0, h, 0, 65] = -np.inf
+    return x.astype(np.float32)
+
+
+@pytest.mark.parametrize("vb", [2, 3, 4])
+@pytest.mark.parametrize("fused", [False, True])
+def test_decode_append_special_values(cuda, vb, fused):
+    """Single-token decode appends whose aged Value tokens hold NaN at a group's first element
+    or at the start of a non-leader lane's slice, +-0 extrema and infinities: meta and codes
+    equal the reference's sequential fold (quant.hpp:170-182) -- through the decode-append
+    kernel and through the attention kernel's fused prologue (append_attend)."""
+    B, H, D = 1, 2, 128
+    rng = np.random.default_rng(vb)
+    dev, ora = make_pair(2, vb, 0.1, 0.1, 32, B, H, D, cap=512)
+    k = O.random_h16(7, (B, H, 64, D))
+    v = O.random_h16(8, (B, H, 64, D))
+    dev.append(k, v)
+    ora.append(k, v)
+    q = torch.from_numpy(O.random_h16(9, (B, H, 1, D))).cuda()
+    for step in range(40):
+        kn = O.random_h16(2000 + step, (B, H, 1, D))
+        vn = _special_token(rng, B, H, D, step)
+        if fused:
+            K.append_attend(dev, torch.from_numpy(kn).cuda(), torch.from_numpy(vn).cuda(), q)
+        else:
+            dev.append(torch.from_numpy(kn).cuda(), torch.from_numpy(vn).cuda())
+        ora.append(kn, vn)
+    torch.cuda.synchronize()
+    assert dev.dump() == ora.dump()
+    if O.ref_available():
+        ref = O.RefCache(2, vb, 0.1, 0.1, 32, B, H, D)
+        ref.append(k, v)
+        rng = np.random.default_rng(vb)
+        for step in range(40):
+            ref.append(O.random_h16(2000 + step, (B, H, 1, D)), _special_token(rng, B, H, D, step))
+        assert dev.dump() == ref.dump()

@@ -192,3 +192,24 @@ def test_oracle_vs_live_reference():
         r.append(k, v)
         assert c.counters() == r.counters()
     assert c.dump() == r.dump()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built in this container")
+@pytest.mark.parametrize("vb", [2, 3, 4])
+def test_oracle_special_values_vs_live_reference(vb):
+    """NaN / +-0 / inf in aged tokens (group first element, mid-group): the oracle's fold
+    equals the reference's (quant.hpp:170-182) -- pins the oracle for the GPU special-value
+    tests (tests/test_cache_gpu.py::test_decode_append_special_values)."""
+    from test_cache_gpu import _special_token
+    B, H, D = 1, 2, 128
+    ora = O.CacheOracle(2, vb, 0.1, 0.1, 32, B, H, D)
+    ref = O.RefCache(2, vb, 0.1, 0.1, 32, B, H, D)
+    k, v = O.random_h16(7, (B, H, 64, D)), O.random_h16(8, (B, H, 64, D))
+    ora.append(k, v)
+    ref.append(k, v)
+    rng = np.random.default_rng(vb)
+    for step in range(40):
+        kn, vn = O.random_h16(2000 + step, (B, H, 1, D)), _special_token(rng, B, H, D, step)
+        ora.append(kn, vn)
+        ref.append(kn, vn)
+    assert ora.dump() == ref.dump()

@@ -170,3 +170,24 @@ def test_kvqg_golden_bytes(cuda):
         K.deserialize_quantized_groups(b"X" + golden[1:])
     with pytest.raises(K.KvmixRuntimeError):
         K.deserialize_quantized_groups(golden[:-1])
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+@pytest.mark.parametrize("key", [True, False])
+def test_value_at_and_get_per_element(cuda, bits, key):
+    """QuantizedGroups::value_at / PackedBuffer::get (quant.cpp:97-100, bitpack.cpp:69-82) read
+    one word and one meta pair each, bit-exact with the bulk dequantize / oracle decode."""
+    shape = (2, 3, 64, 40)
+    x = O.random_h16(bits * 7 + key, shape, sigma=1.3)
+    spec = K.QuantSpec(bits, K.Grouping.kPerChannelKey if key else K.Grouping.kPerTokenValue, 32)
+    qg = (K.quantize_key_tensor if key else K.quantize_value_tensor)(torch.from_numpy(x).cuda(), spec)
+    full = qg.dequantize().cpu().numpy()
+    w, _ = O.quantize(x, bits, 32, key)
+    rng = np.random.default_rng(bits)
+    for _ in range(40):
+        b, h, t, d = (int(rng.integers(0, n)) for n in shape)
+        assert np.float32(qg.value_at(b, h, t, d)).view(np.uint32) == full[b, h, t, d].view(np.uint32)
+        si = qg.stream_index(b, h, t, d)
+        assert qg.codes.get(si) == O.get(w, si, bits)
+    with pytest.raises(K.KvmixOutOfRange):
+        qg.codes.get(qg.codes.logical_len)
