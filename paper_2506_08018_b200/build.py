@@ -10,14 +10,14 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libkvmix_b200.so")
+LIB = os.environ.get("KVMIX_BUILD_OUT") or os.path.join(HERE, "libkvmix_b200.so")
 SOURCES = ["capi.cu", "quant.cu", "cache.cu", "attention.cu", "attention_mma.cu", "scratch.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("KVMIX_EXTRA_NVCC", "").split()  # A/B variants (e.g. -DKVB_WARPS=1)
 
 
 def needs_build() -> bool:
@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = os.path.join(os.path.dirname(LIB), os.path.basename(LIB) + "." + src.replace(".cu", ".o"))
         cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))

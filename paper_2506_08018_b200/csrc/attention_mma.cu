@@ -60,15 +60,17 @@ namespace kvb {
 
 namespace {
 
-constexpr int kMmaWarps = 4;
-#ifndef KVB_MIN_CTAS
-#ifndef KVB_MIN_CTAS_N
-#define KVB_MIN_CTAS_N 4
+#ifndef KVB_WARPS
+#define KVB_WARPS 4
 #endif
-// CTAs per SM the register budget is sized for: 3-bit Keys with two query rows (GQA) get 3
-// (their B staging leaves shared memory for 3 CTAs with a two-stage ring anyway)
-#define KVB_MIN_CTAS(KB, R) ((KB) == 3 && (R) == 2 ? 3 : KVB_MIN_CTAS_N)
+constexpr int kMmaWarps = KVB_WARPS;  // independent warps per CTA (no CTA barriers)
+#ifndef KVB_MIN_WARPS_N
+#define KVB_MIN_WARPS_N 16
 #endif
+// resident warps per SM the register budget is sized for: 3-bit Keys with two query rows
+// (GQA) get 12 (their B staging leaves shared memory for 12 warps with a two-stage ring anyway)
+#define KVB_MIN_WARPS(KB, R) ((KB) == 3 && (R) == 2 ? 12 : KVB_MIN_WARPS_N)
+#define KVB_MIN_CTAS(KB, R) (KVB_MIN_WARPS(KB, R) / KVB_WARPS)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kFlushBlocks = 1024;  // Value int32 accumulators: < 2^31 / (32 * 240 * 255)
@@ -486,14 +488,16 @@ struct StageGeo {
   static constexpr uint32_t kKM = (uint32_t)(D * 4);
   static constexpr uint32_t kStage = kKT + kVT + kVM + kKM;
   static constexpr long kStatic = (long)kMmaWarps * R * D * 4;  // s_acc
+  // ring depth at `occ` resident CTAs per SM (the per-CTA reservation is 1 KB)
   static constexpr int stages_for(int occ) {
     return (int)(((227L * 1024 / occ - 1024 - kStatic) / kMmaWarps - (long)WarpLayout<D, KB, R>::bytes(0, 0) - 32 - 128) /
                  (long)(kStage ? kStage : 1));
   }
+  static constexpr int kOcc = KVB_MIN_CTAS(KB, R);
   static constexpr int kStages = GS == 0 ? 0
-                                 : stages_for(4) >= 2 ? (stages_for(4) < 4 ? stages_for(4) : 4)
-                                 : stages_for(3) >= 2 ? (stages_for(3) < 4 ? stages_for(3) : 4)
-                                                      : 2;
+                                 : stages_for(kOcc) >= 2 ? (stages_for(kOcc) < 4 ? stages_for(kOcc) : 4)
+                                 : stages_for(kOcc * 3 / 4) >= 2 ? (stages_for(kOcc * 3 / 4) < 4 ? stages_for(kOcc * 3 / 4) : 4)
+                                                                 : 2;
 };
 
 // GS: 0 = runtime group size (a multiple of 32), else compile-time (32 is the KVmix default).
@@ -1333,7 +1337,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   }
   const size_t fixed = WL::bytes(0, 0);
   int stages = 2;
-  for (int occ_target = 4; occ_target >= 2; --occ_target) {
+  for (int occ_target = KVB_MIN_CTAS(KB, R); occ_target >= 1; occ_target = occ_target * 3 / 4) {
     const long per_cta = 227L * 1024 / occ_target - 1024 - static_smem;
     const long per_warp = per_cta / kMmaWarps - (long)fixed - 4 * 8 - 128;
     const long s_fit = per_warp / (long)p.stage_bytes;
