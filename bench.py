@@ -124,6 +124,22 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _share_gpu() -> bool:
+    """KVMIX_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo for the host-side reductions -- the
+    N-rank code path on a 1-GPU box (numbers are not a scaling measurement then)."""
+    return os.environ.get("KVMIX_BENCH_SHARE_GPU") == "1"
+
+
+def reduce_max(x: float, world: int, dev, op="max") -> float:
+    """max (or sum) over ranks of a host scalar, through the process group."""
+    import torch
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if _share_gpu() else dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX if op == "max" else torch.distributed.ReduceOp.SUM)
+    return float(t.item())
+
+
 def peak_hbm():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -279,6 +295,7 @@ def run_b200(args, rank, world, local_rank):
             ev[l][1].record(stream)
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -306,10 +323,7 @@ def run_b200(args, rank, world, local_rank):
     launches = _lib.launch_count() - launches0
     elapsed = start.elapsed_time(end)  # ms for K steps
     attn_ms = [statistics.mean(evs[i][l][0].elapsed_time(evs[i][l][1]) for i in inst) for l in range(L)]
-    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    elapsed = float(t.item())
+    elapsed = reduce_max(elapsed, world, dev)
     ms_per_step = elapsed / args.steps
     value = B_glob * args.steps / (elapsed / 1e3)
 
@@ -385,18 +399,14 @@ def run_b200(args, rank, world, local_rank):
         run(n_e2e)
         s1.record(stream)
         s1.synchronize()
-        te = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
-        if world > 1:
-            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": B_glob * n_e2e / (float(te.item()) / 1e3), "unit": "tokens/s",
+        te = reduce_max(s0.elapsed_time(s1), world, dev)
+        e2e = {"value": B_glob * n_e2e / (te / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(L * (qs[0, 0].numel() + kn[0, 0].numel() + vn[0, 0].numel()) * 2) * world,
                "d2h_bytes_per_step": int(L * outs[0].numel() * 4) * world,
                "path": "DecodeStep.step() (public API, kvmix_append_attend_layers) on pinned-host inputs, every "
                        "layer's output read back; H2D/D2H double-buffered on a copy stream"}
 
-    launches_t = torch.tensor([launches], device=dev, dtype=torch.int64)
-    if world > 1:
-        torch.distributed.all_reduce(launches_t)
+    launches_all = int(reduce_max(float(launches), world, dev, op="sum"))
     hi = f"0-{high - 1} K3/V4 r0.2, rest K2/V2 r0.1" if high else "all K2/V2 r0.1"
     res = {
         "metric": METRIC,
@@ -428,7 +438,7 @@ def run_b200(args, rank, world, local_rank):
                      "algorithmic_bytes_per_step": tot_bytes, "attend_ms_per_step": tot_ms,
                      "attend_share_of_step": tot_ms / ms_per_step},
         "e2e": e2e,
-        "gpu_launches": int(launches_t.item()),
+        "gpu_launches": launches_all,
         "clocks": clk.summary(),
         "check": check,
         "memory": {"compressed_bytes_per_step_per_gpu": tot_bytes,
@@ -528,10 +538,7 @@ def run_quant(args, rank, world, local_rank):
         end.synchronize()
     launches = _lib.launch_count() - launches0
     elapsed = start.elapsed_time(end)
-    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    elapsed = float(t.item())
+    elapsed = reduce_max(elapsed, world, dev)
     ms_per_step = elapsed / args.steps  # one step = the whole 18-setting sweep
     elems = n * len(settings) * world
     value = elems * args.steps / (elapsed / 1e3)
@@ -661,10 +668,15 @@ def main():
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return 0
 
+    if _share_gpu():
+        local_rank = 0
     if world > 1:
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if _share_gpu():
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.config == "quant-sweep":
         res = run_quant(args, rank, world, local_rank)
         if rank == 0 and not args.no_e2e:

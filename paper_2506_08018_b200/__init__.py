@@ -7,7 +7,8 @@ same names, same argument meaning, same error behaviour, over torch CUDA tensors
 There is no CPU fallback: importing without the built library fails loudly.
 """
 from ._lib import (KvmixCudaError, KvmixError, KvmixInvalidArgument, KvmixOutOfMemory, KvmixOutOfRange,
-                   KvmixRuntimeError, launch_count, launch_count_of, lib)
+                   KvmixRuntimeError, launch_count, launch_count_of, lib, scratch_allocated, scratch_reset,
+                   set_knob, tensor_core_launches)
 from .quant import (GroupMeta, Grouping, PackedBuffer, PackLayout, QuantizedGroups, QuantSpec, TensorShape,
                     deserialize_quantized_groups, feat_per_word, kMixed3Block, mixed3_q_max, mixed3_wide_scale,
                     pack_mixed3, pack_uniform, packed_word_count, q_max_for_bits, quantize_key_tensor,

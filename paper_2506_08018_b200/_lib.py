@@ -157,6 +157,11 @@ def scratch_allocated() -> int:
     return int(lib().kvmix_scratch_allocated())
 
 
+def tensor_core_launches() -> int:
+    """Launches of the tensor-core attention kernels (warp-specialized or single-warp)."""
+    return launch_count_of("attend_ws_kernel") + launch_count_of("attend_mma_kernel")
+
+
 def launch_count_of(kernel: str) -> int:
     """Launches of one device kernel by name (which path served a call)."""
     return int(lib().kvmix_launch_count_of(kernel.encode()))

@@ -45,27 +45,11 @@ struct Src {
   }
 };
 
-// Inverse of key_coord/value_coord (3-bit HMMA layout): element (token-in-tile i,
-// channel d) of the field (lane, w, half, sl) of a b-bit plane.
-__device__ inline void field_element(bool key, int D, int b, int lane, int w, int half, int sl, int* i, int* d) {
-  const int sph = 16 / b;
-  const int vs = w * sph + sl;
-  const int nslot = D >> 4;
-  const int r = vs / nslot, slot = vs % nslot;
-  const int g = lane >> 2, t = lane & 3;
-  if (key) {
-    *i = g + 8 * (r & 1);
-    *d = slot * 16 + 2 * t + half + 8 * (r >> 1);
-  } else {
-    *i = 2 * t + half + 8 * (r >> 1);
-    *d = slot * 16 + g + 8 * (r & 1);
-  }
-}
-
 // Assemble one tile from codes[16][D] (u8, shared). For partial value tiles only rows in
 // [i_lo, i_hi) contribute and words are OR-merged.
 __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes, uint32_t* tile, bool atomic,
                                  int i_lo, int i_hi) {
+  if (!key) bits = vstore_bits(bits);  // 3-bit Values: 4-bit fields
   if (bits != 3) {  // IMMA layout: 4 bytes x C classes per word
     const int wpl = plane_wpl(D, bits), cw = wpl < 4 ? wpl : 4;
     const int nf = 32 / bits;
@@ -87,7 +71,7 @@ __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes
     }
     return;
   }
-  if (key) {  // 3-bit Keys: IMMA 2-bit plane of the low bits, then the 1-bit plane
+  {  // 3-bit Keys: IMMA 2-bit plane of the low bits, then the 1-bit plane
     const int wpl2 = plane_wpl(D, 2), cw2 = wpl2 < 4 ? wpl2 : 4;
     for (int pw = threadIdx.x; pw < 32 * wpl2; pw += blockDim.x) {
       const int chunk = pw / (32 * cw2), within = pw % (32 * cw2);
@@ -124,34 +108,6 @@ __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes
       }
     }
     return;
-  }
-  int off = 0;
-  for (int pl = 0; pl < 2; ++pl) {
-    const int b = pl == 0 ? 2 : 1;
-    const int wpl = plane_wpl(D, b);
-    const int cw = wpl < 4 ? wpl : 4;
-    const int sph = 16 / b;
-    for (int pw = threadIdx.x; pw < 32 * wpl; pw += blockDim.x) {
-      const int chunk = pw / (32 * cw), within = pw % (32 * cw);
-      const int lane = within / cw, w = chunk * cw + within % cw;
-      uint32_t word = 0;
-      for (int half = 0; half < 2; ++half) {
-        for (int sl = 0; sl < sph; ++sl) {
-          int i, d;
-          field_element(key, D, b, lane, w, half, sl, &i, &d);
-          if (i < i_lo || i >= i_hi) continue;
-          uint32_t code = codes[i * D + d];
-          code = pl == 0 ? (code & 3u) : (code >> 2);
-          word |= code << (half * 16 + sl * b);
-        }
-      }
-      if (atomic) {
-        if (word) atomicOr(tile + off + pw, word);
-      } else {
-        tile[off + pw] = word;
-      }
-    }
-    off += 32 * wpl;
   }
 }
 
@@ -248,7 +204,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     const int glanes = min(gs, D) / LC;  // lanes per channel group (power of two)
     const uint32_t m = group_meta_warp(x, LC, glanes, lane, q_max);
     const int g0 = lane * LC / gs;
-    if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + g0] = m;
+    if ((lane % glanes) == 0) a.v_meta[vmeta_at(a.vv, bh, j, g0)] = m;
     if (bh == 0 && lane == 0) a.v_info[j] = make_int2((int)a.v_n, (int)tl);
     const float sc = meta_scale(m), mnv = meta_min(m);
     uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);
@@ -289,7 +245,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       }
       const uint32_t m = make_meta(mn, mx, q_max);
       mrow[i * cg + gi] = m;
-      a.v_meta[vmeta_index(a.vv, bh, tile * 16 + i) + gi] = m;
+      a.v_meta[vmeta_at(a.vv, bh, tile * 16 + i, gi)] = m;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < (i_hi - i_lo) * D; e += blockDim.x) {
@@ -406,7 +362,7 @@ __global__ void export_meta_kernel(SideView s, bool key, int D, int gs, int BH, 
       const int g = (int)(mi % cg);
       const int bh = (int)(tok / n);
       const int64_t tl = (int64_t)(tok % n);
-      meta[mi] = s.meta[vmeta_index(s, bh, S + tl) + g];
+      meta[mi] = s.meta[vmeta_at(s, bh, S + tl, g)];
     }
   }
 }
@@ -455,7 +411,7 @@ __global__ void import_kernel(SideView s, uint32_t* tiles, uint32_t* dmeta, int2
         if (bh == 0 && d == 0) info[j / gs] = make_int2((int)n, (int)tl);
       }
     } else if (d % gs == 0) {
-      dmeta[vmeta_index(s, bh, j) + d / gs] = meta[((size_t)bh * n + tl) * cg + d / gs];
+      dmeta[vmeta_at(s, bh, j, d / gs)] = meta[((size_t)bh * n + tl) * cg + d / gs];
       if (bh == 0 && d == 0) info[j] = make_int2((int)n, (int)tl);
     }
   }

@@ -11,7 +11,7 @@
 // and both metas) with a single bulk copy:
 //   rec      [bh][group = token/gs] { K tiles [gs/16][tile_words(D, key_bits)]   fragment-native codes (common.cuh)
 //                                     V tiles [gs/16][tile_words(D, value_bits)]
-//                                     V meta  [gs][ceil(D/gs)]  u32 {scale_f16 | min_f16 << 16}
+//                                     V meta  [ceil(D/gs)][gs]  u32 {scale_f16 | min_f16 << 16}
 //                                     K meta  [D] }
 //   K tail   [bh][ring slot][D]               fp32 or fp16 full-precision window (ring)
 //   V tail   [bh][ring slot][D]
@@ -80,10 +80,12 @@ __host__ __device__ inline size_t tile_index(const SideView& s, int bh, int64_t 
 __host__ __device__ inline size_t kmeta_index(const SideView& s, int bh, int64_t grp) {
   return (size_t)bh * s.bh_stride + (size_t)grp * s.grp_stride;
 }
-// Value meta row of token j (ceil(D/gs) words, one per channel group)
-__host__ __device__ inline size_t vmeta_index(const SideView& s, int bh, int64_t j) {
+// Value meta word of token j, channel group g. Inside a group record the Value meta is
+// [channel group][token] (gs words per channel group), so the metas of consecutive tokens of
+// one channel group are contiguous (one 16-byte load for a token quad in the attention kernel).
+__host__ __device__ inline size_t vmeta_at(const SideView& s, int bh, int64_t j, int g) {
   const unsigned gs = (unsigned)s.tpg * 16u, jj = (unsigned)j, gi = jj / gs;
-  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)(jj - gi * gs) * s.mrow;
+  return (size_t)bh * s.bh_stride + (size_t)gi * s.grp_stride + (size_t)g * gs + (jj - gi * gs);
 }
 
 template <typename TT>
@@ -118,7 +120,7 @@ __device__ inline float packed_value(bool key, const SideView& s, int bh, int64_
     m = s.meta[kmeta_index(s, bh, grp) + d];
     if (s.bits == 3) narrow = narrow_key(s.gbh(bh), d, D, s.info[grp], j - grp * gs);
   } else {
-    m = s.meta[vmeta_index(s, bh, j) + d / gs];
+    m = s.meta[vmeta_at(s, bh, j, d / gs)];
     if (s.bits == 3) narrow = narrow_value(s.gbh(bh), d, D, s.info[j]);
   }
   return decode(code, meta_scale(m), meta_min(m), narrow);
@@ -204,7 +206,7 @@ __device__ inline void decode_append_warp(const DecodeAppend& a, int bh, int lan
     const int glanes = min(gs, D) / LC;
     const uint32_t m = group_meta_warp(x, LC, glanes, lane, q_max);
     const int64_t j = a.v_j;
-    if ((lane % glanes) == 0) a.v_meta[vmeta_index(a.vv, bh, j) + lane * LC / gs] = m;
+    if ((lane % glanes) == 0) a.v_meta[vmeta_at(a.vv, bh, j, lane * LC / gs)] = m;
     if (bh == 0 && lane == 0) a.v_info[j] = make_int2(1, 0);
     const float sc = meta_scale(m), mnv = meta_min(m);
     uint32_t* tp = a.v_tiles + tile_index(a.vv, bh, j >> 4);

@@ -194,7 +194,7 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
     const size_t BH = (size_t)batch * heads;
     const int64_t ngroups = (capacity_tokens + gs - 1) / gs;  // group records per (b, kv-head)
     const int tpg = gs / 16, cg = (head_dim + gs - 1) / gs;
-    const size_t ktw = (size_t)tile_words(head_dim, cfg->key_bits), vtw = (size_t)tile_words(head_dim, cfg->value_bits);
+    const size_t ktw = (size_t)tile_words(head_dim, cfg->key_bits), vtw = (size_t)tile_words(head_dim, vstore_bits(cfg->value_bits));
     const size_t rec_words = tpg * (ktw + vtw) + (size_t)gs * cg + head_dim;  // 16-byte multiple
     c->rec_bytes = BH * (size_t)ngroups * rec_words * 4;
     alloc((void**)&c->rec, c->rec_bytes);

@@ -157,35 +157,15 @@ __host__ __device__ inline size_t words_for(size_t n, int bits) {
 // 3-bit Keys -- two IMMA planes: the low 2 bits in the 2-bit Key layout above, then the high
 // bit in a 1-bit plane (C = 8 classes per byte): z = q + 2 NK rb, word z / 8, bit 8e + z % 8
 // (for D = 128 the class z % 8 = q depends on the channel only).
-// 3-bit Values -- HMMA layout, mma.sync m16n8k16 f16 A fragments (rows g, g+8; cols 2t,2t+1,
-// 2t+8,2t+9), A = [channel][token] (m-tile mt = d/16). Register r holds a pair (lo half =
-// first element); within a lane, register r at slot s lives at virtual slot vs = r*(D/16) + s
-// of a per-half bit stream with 16/b slots per half. Stored as a 2-bit plane (low bits)
-// followed by a 1-bit plane.
+// 3-bit Values -- the 4-bit IMMA Value layout (codes 0..7 in 4-bit fields): the class of a
+// Value code depends on its channel (the accumulator row), so a dense 1-bit high plane cannot
+// share the low plane's accumulators; 4-bit fields keep the Value side a plain IMMA k-step.
+// (The reference's Mixed3 words are rebuilt bit-exactly on export; its byte accounting --
+// MemoryReport, the roofline's algorithmic bytes -- stays the 3-bit one.)
 // ---------------------------------------------------------------------------------------
-struct TileCoord {
-  int lane, r, slot, half;
-};
 
-__host__ __device__ inline TileCoord key_coord(int i, int d) {
-  const int kk = d >> 4, dc = d & 15;
-  TileCoord c;
-  c.half = dc & 1;
-  c.r = (i >= 8 ? 1 : 0) + (dc >= 8 ? 2 : 0);
-  c.lane = (i & 7) * 4 + ((dc & 7) >> 1);
-  c.slot = kk;
-  return c;
-}
-
-__host__ __device__ inline TileCoord value_coord(int i, int d) {
-  const int mt = d >> 4, dc = d & 15;
-  TileCoord c;
-  c.half = i & 1;
-  c.r = (dc >= 8 ? 1 : 0) + (i >= 8 ? 2 : 0);
-  c.lane = (dc & 7) * 4 + ((i & 7) >> 1);
-  c.slot = mt;
-  return c;
-}
+// storage bits of a Value code: 3-bit Values use 4-bit fields (see above)
+__host__ __device__ constexpr int vstore_bits(int bits) { return bits == 3 ? 4 : bits; }
 
 // words per lane of one b-bit plane
 __host__ __device__ constexpr int plane_wpl(int D, int b) { return D * b / 64; }
@@ -202,14 +182,6 @@ __host__ __device__ inline int plane_addr(int lane, int w, int wpl) {
   return (w / cw) * (32 * cw) + lane * cw + (w % cw);
 }
 
-// Location (word offset within tile, bit shift) of a b-bit field of one HMMA-layout plane.
-__host__ __device__ inline void plane_field(const TileCoord& c, int D, int b, int* word, int* shift) {
-  const int sph = 16 / b;
-  const int vs = c.r * (D >> 4) + c.slot;
-  const int w = vs / sph;
-  *shift = c.half * 16 + (vs % sph) * b;
-  *word = plane_addr(c.lane, w, plane_wpl(D, b));
-}
 
 // IMMA layout (b in {2, 4}): word offset / bit shift of (token-in-tile i, channel d).
 __host__ __device__ inline void imma_field(bool key, int D, int b, int i, int d, int* word, int* shift) {
@@ -284,13 +256,8 @@ __host__ __device__ inline CodeLoc code_loc(bool key, int D, int bits, int i, in
     imma_field(true, D, 2, i, d, &c.w0, &c.s0);
     imma_key_hi_field(D, i, d, &c.w1, &c.s1);
     c.w1 += 32 * plane_wpl(D, 2);
-  } else if (bits == 3) {
-    const TileCoord tc = key ? key_coord(i, d) : value_coord(i, d);
-    plane_field(tc, D, 2, &c.w0, &c.s0);
-    plane_field(tc, D, 1, &c.w1, &c.s1);
-    c.w1 += 32 * plane_wpl(D, 2);
   } else {
-    imma_field(key, D, bits, i, d, &c.w0, &c.s0);
+    imma_field(key, D, key ? bits : vstore_bits(bits), i, d, &c.w0, &c.s0);
   }
   return c;
 }
@@ -298,15 +265,16 @@ __host__ __device__ inline CodeLoc code_loc(bool key, int D, int bits, int i, in
 // Read a code from a tile (bits in {2,3,4}).
 __device__ inline uint32_t tile_get(const uint32_t* tile, bool key, int D, int bits, int i, int d) {
   const CodeLoc c = code_loc(key, D, bits, i, d);
-  if (bits == 3) return ((tile[c.w0] >> c.s0) & 3u) | (((tile[c.w1] >> c.s1) & 1u) << 2);
-  return (tile[c.w0] >> c.s0) & ((1u << bits) - 1u);
+  if (bits == 3 && key) return ((tile[c.w0] >> c.s0) & 3u) | (((tile[c.w1] >> c.s1) & 1u) << 2);
+  const int sb = key ? bits : vstore_bits(bits);
+  return (tile[c.w0] >> c.s0) & ((1u << sb) - 1u);
 }
 
 // OR a code into a zero-initialised field (global or shared memory).
 __device__ inline void tile_or(uint32_t* tile, bool key, int D, int bits, int i, int d, uint32_t code) {
   if (code == 0) return;
   const CodeLoc c = code_loc(key, D, bits, i, d);
-  if (bits == 3) {
+  if (bits == 3 && key) {
     if (code & 3u) atomicOr(tile + c.w0, (code & 3u) << c.s0);
     if (code >> 2) atomicOr(tile + c.w1, (code >> 2) << c.s1);
   } else {

@@ -20,6 +20,15 @@ import paper_2506_08018_b200 as K
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, params=["ws", "single"])
+def tc_kernel(request):
+    """Every parity test runs on both tensor-core kernels: the warp-specialized one (default)
+    and the single-warp one it falls back to."""
+    K.set_knob("KVMIX_WS", 2 if request.param == "ws" else 0)
+    yield request.param
+    K.set_knob("KVMIX_WS", 1)
+
 ATTN_TOL_F64 = 2e-6
 ATTN_TOL_F32 = 4e-6
 CHECKSUM_RTOL = 2e-7
@@ -55,10 +64,10 @@ def check_attend(dev, ora, q, G=1, expect_mma=None):
     else:
         o64, cs64 = O.attend_f64(q, ks, vs)
         o32, cs32 = O.attend_f32(q, ks, vs)
-    n_mma, n_gen = K.launch_count_of("attend_mma_kernel"), K.launch_count_of("attend_generic_kernel")
+    n_mma, n_gen = K.tensor_core_launches(), K.launch_count_of("attend_generic_kernel")
     res = K.attend(torch.from_numpy(q).cuda(), dev)
     out = res.output.cpu().numpy()
-    used_mma = K.launch_count_of("attend_mma_kernel") - n_mma
+    used_mma = K.tensor_core_launches() - n_mma
     used_gen = K.launch_count_of("attend_generic_kernel") - n_gen
     assert (used_mma > 0) != (used_gen > 0)  # one path serves the call (the IMMA path in passes of rows)
     if expect_mma is not None:
@@ -72,7 +81,7 @@ def check_attend(dev, ora, q, G=1, expect_mma=None):
     return e64
 
 
-@pytest.mark.parametrize("kb,vb", [(2, 2), (3, 4), (4, 4), (3, 3), (2, 4), (4, 2)])
+@pytest.mark.parametrize("kb,vb", [(2, 2), (3, 4), (4, 4), (3, 3), (2, 4), (4, 2), (2, 3), (4, 3)])
 def test_attend_fill_states(cuda, kb, vb):
     rng = np.random.default_rng(kb * 7 + vb)
     for trial in range(4):
@@ -319,7 +328,8 @@ def test_append_attend_from_an_empty_cache(cuda):
 
 
 @pytest.mark.parametrize("kb,vb,gs,rk,rv,tail", [(2, 2, 32, 0.1, 0.1, torch.float32), (3, 4, 32, 0.2, 0.2, torch.float16),
-                                                 (2, 4, 64, 0.1, 0.1, torch.float16), (4, 2, 32, 0.1, 0.3, torch.float32)])
+                                                 (2, 4, 64, 0.1, 0.1, torch.float16), (4, 2, 32, 0.1, 0.3, torch.float32),
+                                                 (2, 3, 32, 0.1, 0.1, torch.float16), (3, 3, 32, 0.2, 0.2, torch.float32)])
 def test_attend_window_blocks_through_a_cycle(cuda, kb, vb, gs, rk, rv, tail):
     """The Key window (full precision, Values already packed) runs through the IMMA Value
     path in 32-token window blocks. Walk a whole Key age-out cycle one decode step at a time
@@ -333,4 +343,41 @@ def test_attend_window_blocks_through_a_cycle(cuda, kb, vb, gs, rk, rv, tail):
         dev.append(k, v)
         ora.append(k, v)
         if s % 3 == 0 or s > 34:
-            check_attend(dev, ora, q, expect_mma=True)
+            check_attend(dev, ora, q, expect_mma=True if vb != 3 else None)
+
+
+@pytest.mark.parametrize("kb,D,G,tq,gs", [(2, 128, 1, 1, 32), (3, 128, 1, 1, 32), (4, 64, 2, 1, 32), (2, 128, 4, 1, 32),
+                                         (3, 128, 1, 3, 32), (2, 64, 1, 2, 64), (4, 128, 2, 1, 128)])
+def test_attend_3bit_values_tensor_core(cuda, tc_kernel, kb, D, G, tq, gs):
+    """3-bit Values (Mixed3 in the reference, 4-bit fields on the device) run on the tensor cores
+    in the warp-specialized kernel: the IMMA sums code * scale and the narrow slots (stream index
+    % 11 == 10, decoded with scale * 7/3, quant.cpp:36-53) are corrected on the CUDA cores --
+    same tolerance as every other tier. The single-warp kernel leaves them to the generic one."""
+    H = 4
+    dev, ora = build(kb, 3, 0.15, 0.1, gs, 2, H, D, [1000, 37] + [1] * 25, seed=91 + kb)
+    q = O.random_h16(92, (2, H * G, tq, D), sigma=1.7)
+    check_attend(dev, ora, q, G=G, expect_mma=tc_kernel == "ws")
+
+
+@pytest.mark.parametrize("kb,vb", [(2, 2), (3, 4), (2, 3)])
+def test_scratch_independent_of_token_count(cuda, tc_kernel, kb, vb):
+    """The reference's scratch contract (scratch.hpp:14-21, test_attention.cpp:182-205): the
+    fused path's scratch does not grow with the cached tokens. kvmix_scratch_allocated counts
+    the bytes requested per call (split-K partials, counters, flags) -- equal at 128 and 32768
+    tokens, for attend and for the fused append + attend."""
+    from paper_2506_08018_b200 import _lib
+    B, H, D = 2, 4, 128
+    sizes = []
+    for T in (128, 32768):
+        dev = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, 0.1, 0.1, 32), B, H, D, capacity_tokens=T + 8,
+                             tail_dtype=torch.float16)
+        dev.append(torch.randn(B, H, T, D, device=cuda, dtype=torch.float16),
+                   torch.randn(B, H, T, D, device=cuda, dtype=torch.float16))
+        q = torch.randn(B, H, 1, D, device=cuda)
+        _lib.scratch_reset()
+        K.attend(q, dev, checksum=False)
+        a = _lib.scratch_allocated()
+        _lib.scratch_reset()
+        K.append_attend(dev, torch.randn(B, H, 1, D, device=cuda), torch.randn(B, H, 1, D, device=cuda), q)
+        sizes.append((a, _lib.scratch_allocated()))
+    assert sizes[0] == sizes[1] and sizes[0][0] > 0, sizes

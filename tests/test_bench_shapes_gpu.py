@@ -60,7 +60,7 @@ def _run_shape(kb, vb, r, B, H, G, ctx, samples, n_decode=44, checks=(20, 43), s
             o.append(k[b, h].float().cpu().numpy(), v[b, h].float().cpu().numpy())
         del k, v
     worst = 0.0
-    n_mma0 = K.launch_count_of("attend_mma_kernel")
+    n_mma0 = K.tensor_core_launches()
     qk0 = cache.quantized_key_tokens()
     for s in range(n_decode):
         k = torch.randn(B, H, 1, D, device=dev, dtype=torch.float16, generator=gen)
@@ -82,7 +82,7 @@ def _run_shape(kb, vb, r, B, H, G, ctx, samples, n_decode=44, checks=(20, 43), s
                 worst = max(worst, err)
                 assert err <= TOL, (b, h, s, err)
             del ks, vs
-    assert K.launch_count_of("attend_mma_kernel") > n_mma0  # the tensor-core kernel served the steps
+    assert K.tensor_core_launches() > n_mma0  # the tensor-core kernel served the steps
     assert cache.quantized_key_tokens() > qk0  # a Key group aged out during the decode steps
     return worst
 
