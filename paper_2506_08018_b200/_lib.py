@@ -158,7 +158,8 @@ def scratch_allocated() -> int:
 
 
 def tensor_core_launches() -> int:
-    """Launches of the tensor-core attention kernels (warp-specialized or single-warp)."""
+    """Launches of the tensor-core attention kernels (warp-specialized or single-warp IMMA;
+    attend_tc_kernel is always followed by an attend_mma_kernel window launch)."""
     return launch_count_of("attend_ws_kernel") + launch_count_of("attend_mma_kernel")
 
 

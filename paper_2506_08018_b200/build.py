@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("KVMIX_BUILD_OUT") or os.path.join(HERE, "libkvmix_b200.so")
-SOURCES = ["capi.cu", "quant.cu", "cache.cu", "attention.cu", "attention_mma.cu", "attention_ws.cu", "scratch.cu"]
+SOURCES = ["capi.cu", "quant.cu", "cache.cu", "attention.cu", "attention_mma.cu", "attention_ws.cu", "attention_tc.cu", "scratch.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -64,6 +64,7 @@ Knobs& knobs() {
     x.flush_blocks = iv("KVMIX_TEST_FLUSH_BLOCKS", 1, kFlushBlocks, kFlushBlocks);
     x.min_cost = iv("KVMIX_MIN_COST", 1, 1 << 20, kMinCost);
     x.ws = iv("KVMIX_WS", 0, 2, 1);
+    x.tc = iv("KVMIX_TC", 0, 1, 1);
     x.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
     x.no_window = getenv("KVMIX_PROF_NO_WINDOW") != nullptr;
     return x;
@@ -81,12 +82,58 @@ bool set_knob(const char* name, int v) {
   else if (n == "KVMIX_TEST_FLUSH_BLOCKS") k.flush_blocks = std::max(1, std::min(kFlushBlocks, v <= 0 ? kFlushBlocks : v));
   else if (n == "KVMIX_MIN_COST") k.min_cost = std::max(1, v);
   else if (n == "KVMIX_WS") k.ws = std::max(0, std::min(2, v));
+  else if (n == "KVMIX_TC") k.tc = std::max(0, std::min(1, v));
   else return false;
   return true;
 }
 
 
 namespace {
+
+// Window-only launch epilogue: this warp's window partial (m in log2 units, l, lane-parallel
+// accumulators) merged with attend_tc_kernel's fast-group partials of (b, kv-head) bh -- the
+// CTAs c0..c1 whose tile ranges hold bh's tiles, slot c + bh -- in CTA order (deterministic),
+// normalized and written to the output.
+template <int D, int R>
+__device__ __forceinline__ void ext_merge_write(const MmaParams& p, int bh, int lane, int pass, int prow0, int prows,
+                                                const float (&m_all)[R], const float (&l_all)[R],
+                                                const float (&acct)[R][D / 32]) {
+  constexpr int LC = D / 32;
+  int c0 = 0, c1 = -1;
+  if (p.ext_Tb > 0) {
+    const int64_t x0 = (int64_t)bh * p.ext_Tb, x1 = x0 + p.ext_Tb - 1;
+    c0 = (int)(((x0 + 1) * p.ext_C - 1) / p.ext_NT);
+    c1 = (int)(((x1 + 1) * p.ext_C - 1) / p.ext_NT);
+  }
+  const int b = bh / p.H, h = bh % p.H, G = p.Hq / p.H;
+  for (int r = 0; r < prows; ++r) {
+    const int er = prow0 + r;
+    const float mo = m_all[r] == -INFINITY ? -INFINITY : m_all[r] * kLn2;
+    float M = mo;
+    for (int c = c0; c <= c1; ++c) M = fmaxf(M, __ldcg(&p.ext_ml[((size_t)c + bh) * p.ext_R + er]).x);
+    const float fo = mo == -INFINITY ? 0.f : expf(mo - M);
+    float L = l_all[r] * fo;
+    float a[LC];
+#pragma unroll
+    for (int k = 0; k < LC; ++k) a[k] = acct[r][k] * fo;
+    for (int c = c0; c <= c1; ++c) {
+      const size_t si = ((size_t)c + bh) * p.ext_R + er;
+      const float2 ml = __ldcg(&p.ext_ml[si]);
+      if (ml.x == -INFINITY) continue;
+      const float f = expf(ml.x - M);
+      L += ml.y * f;
+      const float* src = p.ext_acc + si * D + lane * LC;
+#pragma unroll
+      for (int k = 0; k < LC; ++k) a[k] = fmaf(__ldcg(src + k), f, a[k]);
+    }
+    const int gi = er / p.tq, qi = er % p.tq;
+    float* o = p.out + (((size_t)b * p.Hq + h * G + gi) * p.tq + qi) * D + lane * LC;
+    const float il = 1.0f / L;
+#pragma unroll
+    for (int k = 0; k < LC; ++k) o[k] = a[k] * il;
+  }
+  if (p.fused && lane == 0) p.flags[(size_t)pass * p.nbh + bh] = 0u;  // final writer of (pass, bh)
+}
 
 // GS: 0 = runtime group size (a multiple of 32), else compile-time (32 is the KVmix default).
 template <int D, int KB, int VB, int R, int GS>
@@ -131,8 +178,23 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
   const uint32_t SB = GS ? SG::kStage : p.stage_bytes;            // bytes per group record
   const uint32_t KTB = GS ? SG::kKT : p.kt_bytes, VTB = GS ? SG::kVT : p.vt_bytes;
   const uint32_t VMB = GS ? SG::kVM : p.vm_bytes;
-  const int64_t c_beg = (int64_t)wg * p.Nc / p.W, c_end = (int64_t)(wg + 1) * p.Nc / p.W;
-  const int u_beg = unit_at_cost(p, c_beg), u_end = unit_at_cost(p, c_end);
+  const int64_t c_beg = p.wonly ? 0 : (int64_t)wg * p.Nc / p.W, c_end = p.wonly ? 0 : (int64_t)(wg + 1) * p.Nc / p.W;
+  // window-only launch: warp wg = (b, kv-head) wg, its window units [Gf, U)
+  const int u_beg = p.wonly ? wg * p.U + p.Gf : unit_at_cost(p, c_beg);
+  const int u_end = p.wonly ? (wg + 1) * p.U : unit_at_cost(p, c_end);
+  if (p.wonly && u_beg >= u_end) {  // no window: the fast-group partials alone
+    float m0[R], l0[R], a0[R][D / 32];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      m0[r] = -INFINITY;
+      l0[r] = 0.f;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) a0[r][c] = 0.f;
+    }
+    if (lane == 0 && p.want_cs) p.part_cs[pbase + wg + wg] = 0.0;
+    ext_merge_write<D, R>(p, wg, lane, pass, prow0, prows, m0, l0, a0);
+    return;
+  }
   if (u_beg >= u_end) {  // no unit starts in this cost range: neutral partial
     const int bh = (int)(c_beg / p.cost_bh);
     int w0, w1;
@@ -878,7 +940,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
       for (int o = 16; o > 0; o >>= 1) csl += __shfl_xor_sync(0xffffffffu, csl, o);
       if (lane == 0) p.part_cs[slot] = csl;
     }
-    if (lo == 0 && hi == p.U) {
+    if (p.wonly) {
+      ext_merge_write<D, R>(p, bh, lane, pass, prow0, prows, m_all, l_all, acct);
+    } else if (lo == 0 && hi == p.U) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r < prows) {
@@ -964,9 +1028,10 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   const int64_t min_cost = knobs().min_cost;
   const int64_t w_cap = std::max<int64_t>(1, p.Nc / min_cost);
   p.W = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(p.N, wave / p.npass), w_cap));
+  if (p.wonly) p.W = BH;  // one warp per (pass, b, kv-head)
   // partial slots x * pslots + w + bh (w + bh < W + BH): scratch depends on (B, H, rows, D,
   // SM count) only
-  p.pslots = (int)(wave + BH);
+  p.pslots = (int)(std::max<int64_t>(wave, p.W) + BH);
   p.nbh = BH;
   const size_t slots = (size_t)p.npass * p.pslots;
   p.part_ml = ws.ml(st, slots * p.rows);
@@ -1073,7 +1138,29 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   };
   if ((int64_t)BH * layout(per_pass) >= (int64_t)1 << 31) return false;
 
+  // tcgen05 kernel over the fast groups (all query rows in one pass), then ONE window launch
+  // (warp per (pass, b, kv-head)) that runs the fused append and the window and merges
+  TcExt ext;
+  const bool use_tc = npass_all <= kMaxPasses && p.Gf > 0 && attend_tc_eligible(c, rows) &&
+                      attend_tc_launch(c, q, dt == KVMIX_F16, Hq, tq, p.Gf, checksum != nullptr, ws, st, &ext);
   double cs_total = 0.0;
+  if (use_tc && checksum) {
+    checksum_kernel<<<1, 32, 0, st>>>(ext.cs, ext.slots, const_cast<double*>(ext.cs) + ext.slots);
+    after_launch("checksum_kernel");
+    double part = 0.0;
+    check_cuda(cudaMemcpyAsync(&part, ext.cs + ext.slots, 8, cudaMemcpyDeviceToHost, st), "memcpy");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    cs_total += part;
+  }
+  if (use_tc) {
+    p.wonly = 1;
+    p.ext_ml = ext.ml;
+    p.ext_acc = ext.acc;
+    p.ext_C = ext.C;
+    p.ext_NT = ext.NT;
+    p.ext_Tb = ext.Tb;
+    p.ext_R = ext.R;
+  }
   for (int x0 = 0; x0 < npass_all; x0 += chunk) {
     const int r0 = x0 * per_pass;
     const int nrows = per_pass;  // rows per pass (the last pass of a launch may hold fewer)
@@ -1094,7 +1181,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     const char* kname = "attend_mma_kernel";
     // the warp-specialized kernel serves 3-bit Values (KVMIX_WS = 1, default) or every tier
     // (KVMIX_WS = 2); the single-warp kernel is ~5% faster on the 2/4-bit tiers (profiles/r2)
-    if (knobs().ws == 2 || (knobs().ws == 1 && vb == 3)) {
+    if (!use_tc && (knobs().ws == 2 || (knobs().ws == 1 && vb == 3))) {
       W = attend_ws_launch(p, D, nrows, kb, vb, BH, ws, st);
       kname = "attend_ws_kernel";
     }
@@ -1110,7 +1197,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
 #undef KVB_DISPATCH_D
     }
     if (W == 0) {
-      if (r0 == 0) return false;  // nothing launched yet: the caller takes the generic path
+      if (r0 == 0 && !use_tc) return false;  // nothing launched yet: the caller takes the generic path
       throw Error(KVMIX_RUNTIME_ERROR, "attend: tensor-core pass unavailable after the first");
     }
     after_launch(kname);

@@ -186,6 +186,7 @@ constexpr int kMinCost = 8;    // minimum cost units per warp (KVMIX_MIN_COST ov
 struct Knobs {
   int tail_unit = kTailUnit, group_cost = kGroupCost, flush_blocks = kFlushBlocks, min_cost = kMinCost;
   int ws = 1;  // warp-specialized kernel (attention_ws.cu): 0 never, 1 for 3-bit Values, 2 always
+  int tc = 1;  // tcgen05 kernel (attention_tc.cu) for the fast groups where it applies
   bool skip_tail = false, no_window = false;
 };
 Knobs& knobs();
@@ -235,7 +236,31 @@ struct MmaParams {
   float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
   float* part_acc;
   double* part_cs;
+  // window-only launch (after attend_tc_kernel served the fast groups): warp = (pass, b,
+  // kv-head), its window units only; the fast-group partials of attend_tc_kernel (slot c + bh
+  // for the CTAs c whose tile ranges hold bh's tiles) are merged into the output here
+  int wonly;
+  const float2* ext_ml;
+  const float* ext_acc;
+  int ext_C;
+  int64_t ext_NT;
+  int ext_Tb, ext_R;
 };
+
+// Partials of the fast groups written by attend_tc_kernel (attention_tc.cu).
+struct TcExt {
+  const float2* ml = nullptr;
+  const float* acc = nullptr;
+  const double* cs = nullptr;
+  int C = 0;         // CTAs (tile ranges)
+  int64_t NT = 0;    // tiles
+  int Tb = 0;        // tiles per (b, kv-head)
+  int R = 0;         // rows per partial slot
+  size_t slots = 0;  // C + BH
+};
+bool attend_tc_launch(const kvmix_cache* c, const void* q, bool q16, int Hq, int tq, int Gf, bool want_cs,
+                      Workspace& ws, cudaStream_t st, TcExt* ext);
+bool attend_tc_eligible(const kvmix_cache* c, int rows);
 
 namespace {
 

@@ -21,12 +21,15 @@ import paper_2506_08018_b200 as K
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["ws", "single"])
+@pytest.fixture(autouse=True, params=["tc", "ws", "single"])
 def tc_kernel(request):
-    """Every parity test runs on both tensor-core kernels: the warp-specialized one (default)
-    and the single-warp one it falls back to."""
-    K.set_knob("KVMIX_WS", 2 if request.param == "ws" else 0)
+    """Every parity test runs on the three tensor-core paths: tcgen05 over the packed groups
+    (default where it applies: D = 128, gs = 32, 2/4-bit Values, <= 4 query rows), the
+    warp-specialized IMMA kernel and the single-warp IMMA kernel."""
+    K.set_knob("KVMIX_TC", 1 if request.param == "tc" else 0)
+    K.set_knob("KVMIX_WS", {"tc": 1, "ws": 2, "single": 0}[request.param])
     yield request.param
+    K.set_knob("KVMIX_TC", 1)
     K.set_knob("KVMIX_WS", 1)
 
 ATTN_TOL_F64 = 2e-6
@@ -356,7 +359,7 @@ def test_attend_3bit_values_tensor_core(cuda, tc_kernel, kb, D, G, tq, gs):
     H = 4
     dev, ora = build(kb, 3, 0.15, 0.1, gs, 2, H, D, [1000, 37] + [1] * 25, seed=91 + kb)
     q = O.random_h16(92, (2, H * G, tq, D), sigma=1.7)
-    check_attend(dev, ora, q, G=G, expect_mma=tc_kernel == "ws")
+    check_attend(dev, ora, q, G=G, expect_mma=tc_kernel in ("ws", "tc"))
 
 
 @pytest.mark.parametrize("kb,vb", [(2, 2), (3, 4), (2, 3)])
