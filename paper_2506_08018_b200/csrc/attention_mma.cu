@@ -64,7 +64,7 @@ Knobs& knobs() {
     x.flush_blocks = iv("KVMIX_TEST_FLUSH_BLOCKS", 1, kFlushBlocks, kFlushBlocks);
     x.min_cost = iv("KVMIX_MIN_COST", 1, 1 << 20, kMinCost);
     x.ws = iv("KVMIX_WS", 0, 2, 1);
-    x.tc = iv("KVMIX_TC", 0, 1, 1);
+    x.tc = iv("KVMIX_TC", 0, 1, 0);  // default off until it beats attend_mma_kernel end to end
     x.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
     x.no_window = getenv("KVMIX_PROF_NO_WINDOW") != nullptr;
     return x;

@@ -186,7 +186,7 @@ constexpr int kMinCost = 8;    // minimum cost units per warp (KVMIX_MIN_COST ov
 struct Knobs {
   int tail_unit = kTailUnit, group_cost = kGroupCost, flush_blocks = kFlushBlocks, min_cost = kMinCost;
   int ws = 1;  // warp-specialized kernel (attention_ws.cu): 0 never, 1 for 3-bit Values, 2 always
-  int tc = 1;  // tcgen05 kernel (attention_tc.cu) for the fast groups where it applies
+  int tc = 0;  // tcgen05 kernel (attention_tc.cu) for the fast groups where it applies
   bool skip_tail = false, no_window = false;
 };
 Knobs& knobs();

@@ -29,7 +29,7 @@ def tc_kernel(request):
     K.set_knob("KVMIX_TC", 1 if request.param == "tc" else 0)
     K.set_knob("KVMIX_WS", {"tc": 1, "ws": 2, "single": 0}[request.param])
     yield request.param
-    K.set_knob("KVMIX_TC", 1)
+    K.set_knob("KVMIX_TC", 0)
     K.set_knob("KVMIX_WS", 1)
 
 ATTN_TOL_F64 = 2e-6

@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 def tc_on():
     K.set_knob("KVMIX_TC", 1)
     yield
-    K.set_knob("KVMIX_TC", 1)
+    K.set_knob("KVMIX_TC", 0)
     K.set_knob("KVMIX_TEST_FLUSH_BLOCKS", 0)
 
 
