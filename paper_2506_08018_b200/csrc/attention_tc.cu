@@ -154,7 +154,7 @@ struct TcGeo {
   static constexpr int BK = KT * N;   // row k = 16 B, N / 16 chunks of KT rows
   static constexpr int BV = 128 * N;  // group x at x * 32 * N
   static constexpr int YT = K3 ? kTcCons * R * kTcD * 4 : 0;  // narrow-slot factors [warp][row][d]
-  static constexpr int XCH = 2048;  // words: [0, 128) reductions, [128, 136) f64 checksums, [256, 288) exchange
+  static constexpr int XCH = 2048;  // words: [0, 128) reductions, [128, 136) f64 checksums, [256, 288) exchange, [320, 322) counters
   static constexpr int NBAR = 4 + 2;  // full[<=4], sfull, vdone
   static constexpr int TFIXED = BK + BV + YT + XCH + NBAR * 8 + 8;
   static constexpr int NTB = K3 ? kTcD * 4 : 0;  // channel -> field of the 2-bit plane (shared by the teams)
@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
   uint64_t* full = bars;       // [S] TMA -> team
   uint64_t* sfull = bars + 4;  // scores in D_K
   uint64_t* vdone = bars + 5;  // Value k-steps done (A_V, B_V, D_V free)
+  uint32_t* cnt_k = xch + 320;  // arrival counters (zero between steps)
+  uint32_t* cnt_v = xch + 321;
 
   if (w == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
   {  // B buffers start zero (columns of absent groups / rows are never written)
     uint4* z = reinterpret_cast<uint4*>(bk);
     for (int i = threadIdx.x & 127; i < (G::BK + G::BV) / 16; i += 128) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    if ((threadIdx.x & 127) == 0) cnt_k[0] = cnt_v[0] = 0u;
   }
   if constexpr (K3) {
     for (int d = threadIdx.x; d < kTcD; d += G::THREADS) {
@@ -248,21 +251,36 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
   if (n > 0) {
     const int bh0 = t_beg / p.Tb, ti0 = t_beg - (t_beg / p.Tb) * p.Tb;
     const uint64_t pol = evict_first_policy();
-    int f_bh = bh0, f_ti = ti0;  // next tile to fetch
-    auto fetch = [&](int i) {    // leader: tile i (= (f_bh, f_ti)) -> stage i % S
+    // next tile to fetch, tracked by every thread (whichever thread closes a tile refills its stage)
+    int f_bh = bh0, f_ti = ti0;
+    auto fetch_next = [&]() {
+      if (++f_ti == p.Tb) {
+        f_ti = 0;
+        ++f_bh;
+      }
+    };
+    auto fetch = [&](int i) {  // tile i (= (f_bh, f_ti)) -> stage i % S
       const int s = i % S;
       const int nv = min(4, p.Gf - 4 * f_ti);
       const uint32_t bytes = (uint32_t)nv * G::SB;
       mbar_arrive_expect_tx(&full[s], bytes);
       bulk_g2s(ring + (size_t)s * G::STAGE, p.rec + ((size_t)f_bh * p.Grec + 4 * (size_t)f_ti) * G::SB, bytes, &full[s],
                pol);
-      if (++f_ti == p.Tb) {
-        f_ti = 0;
-        ++f_bh;
-      }
     };
-    if (leader)
-      for (int i = 0; i < min(S, n); ++i) fetch(i);
+    for (int i = 0; i < min(S, n); ++i) {
+      if (leader) fetch(i);
+      fetch_next();
+    }
+    // the last of the four warps to finish a step issues its MMAs (no team barrier): arrival
+    // counters in shared memory, acq_rel so every warp's TMEM / shared writes happen before
+    auto last_of_team = [&](uint32_t* cnt) {
+      uint32_t old = 0;
+      if (lane == 0) {
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_u32(cnt)) : "memory");
+        if (old == kTcCons - 1) *reinterpret_cast<volatile uint32_t*>(cnt) = 0u;
+      }
+      return old == kTcCons - 1;  // (lane 0 only)
+    };
 
     constexpr uint32_t idk = idesc_i8(G::N, true), idv = idesc_i8(G::N, false);
     const uint32_t bk_a = smem_u32(bk), bv_a = smem_u32(bv);
@@ -280,8 +298,14 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
     // B_V row of this lane's token j = lane inside its group's k-step: tile half y = j / 16,
     // token 4 t + e of the tile -> k = 8 t + 4 y + e
     const int kv_row = 8 * ((lane & 15) >> 2) + 4 * (lane >> 4) + (lane & 3);
-    // this thread as a Value accumulator row: channel d = 32 w + lane, class of its codes
-    const int vq = 2 * w + (lane >> 4) + 8 * ((lane >> 3) & 1);
+    // this thread as a Value accumulator row (TMEM lane 32 w + lane = 16 u + 8 rh + g). 2-bit
+    // Values: warp w unpacks m-tiles w and w + 4 (all four words of a lane's 16-byte chunk, one
+    // class w): channel d = 16 (w + 4 u) + 8 rh + g. 4-bit Values: m-tiles 2 w, 2 w + 1 (one
+    // word, both classes): d = 32 w + lane.
+    constexpr bool VALT = VB == 2;
+    const int vchan = VALT ? 16 * w + 64 * (lane >> 4) + (lane & 15) : 32 * w + lane;
+    const int vcg = vchan >> 5;  // its channel group (gs = 32)
+    const int vq = VALT ? w : 2 * w + (lane >> 4) + 8 * ((lane >> 3) & 1);
     const float vcls = pow2i(-VB * (vq % CV));
     const int Gq = p.Hq / p.H;
 
@@ -298,8 +322,19 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         int v[4];
-        ldtm_32x32_x4(tq_w + G::cDV + 16 * r + 4 * w, v);
-        tc_wait_ld();
+        if constexpr (VALT) {  // the two channel groups of this warp's rows: (w / 2) and 2 + (w / 2)
+          int v2[4];
+          ldtm_32x32_x4(tq_w + G::cDV + 16 * r + 4 * (w >> 1), v);
+          ldtm_32x32_x4(tq_w + G::cDV + 16 * r + 4 * (2 + (w >> 1)), v2);
+          tc_wait_ld();
+          if (lane >> 4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = v2[c];
+          }
+        } else {
+          ldtm_32x32_x4(tq_w + G::cDV + 16 * r + 4 * w, v);
+          tc_wait_ld();
+        }
         const float f = fmaf((float)v[3], 16777216.f, fmaf((float)v[2], 65536.f, fmaf((float)v[1], 256.f, (float)v[0])));
         acc[r] = fmaf(f, wsc, acc[r]) * alpha[r];
       }
@@ -372,9 +407,9 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
 #pragma unroll
         for (int ww = 0; ww < kTcCons; ++ww) {
           L += red[ww * R * 5 + r * 5 + 4];
-          bsum += red[ww * R * 5 + r * 5 + w];  // channel group of this thread's channel = w
+          bsum += red[ww * R * 5 + r * 5 + vcg];  // channel group of this thread's channel
         }
-        p.part_acc[(slot * R + r) * kTcD + 32 * w + lane] = acc[r] + bsum;
+        p.part_acc[(slot * R + r) * kTcD + vchan] = acc[r] + bsum;
         if (w == 0 && lane == 0)
           p.part_ml[slot * R + r] = make_float2(m_run[r] == -INFINITY ? -INFINITY : m_run[r] * kLn2, L);
       }
@@ -445,9 +480,7 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
               ytab[(w * R + r) * kTcD + dch[ii]] = qv[r][ii] * (wide_scale(sc[ii]) - sc[ii]);
             }
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
-          beta[r] = bt;
+          beta[r] = bt;  // lane partial (reduced after the Key arrival, off the MMA's critical path)
         }
         // A: the group's two 16-token Key tiles -> TMEM rows 32 w + 16 u + (g, g + 8)
 #pragma unroll
@@ -487,8 +520,8 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
       tc_wait_st();
       fence_async_smem();
       tc_fence_before();
-      team_sync(bar_id);
-      if (leader) {  // score MMAs: D_K = A_K (codes) x B_K (digits)
+      __syncwarp();
+      if (last_of_team(cnt_k)) {  // score MMAs: D_K = A_K (codes) x B_K (digits)
         tc_fence_after();
 #pragma unroll
         for (int x = 0; x < G::NKS; ++x)
@@ -496,26 +529,59 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
         mma_commit(sfull);
       }
 
-      // ---- Values of all four groups, channels 32 w .. 32 w + 31 -> A_V ----
+      // ---- min-term of the group's scores; this token's Value meta ----
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) beta[r] += __shfl_xor_sync(0xffffffffu, beta[r], o);
+      float vs[4], vmn[4];
+      int e_tok = 100;
+      if (gv) {
+        float smax = 0.f;
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg) {
+          const float2 f = meta_pair(vm[cg * kTcGS + lane]);
+          vs[cg] = f.x;
+          vmn[cg] = f.y;
+          smax = fmaxf(smax, f.x);
+        }
+        e_tok = min(156 - kLazy - (int)((__float_as_uint(smax) >> 23) & 0xffu), 100);
+      } else {
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg) vs[cg] = vmn[cg] = 0.f;
+      }
+
+      // ---- Values of all four groups -> A_V ----
       if (i >= 1) {  // the previous tile's Value k-steps are done with A_V / B_V / D_V
         mbar_wait(vdone, (i - 1) & 1);
         tc_fence_after();
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        uint32_t ra[16];
+      if constexpr (VALT) {
+        // 2-bit: q = mt + 8 rh with mt = w + 4 u -> word q / 4 = u + 2 rh, class w
+        uint32_t ra0[16], ra1[16];
+        const uint32_t msk = VMASK << (VB * w);
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 2; ++y) {
             const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + (size_t)x * G::SB + G::KTB) + y * G::VTW;
-            if constexpr (VWPL == 4) {  // 2-bit: the lane's 4 words are one 16-byte chunk
-              const uint4 v4 = *reinterpret_cast<const uint4*>(vt + 4 * lane);
-              // words q / 4 = w / 2 (rh 0) and 2 + w / 2 (rh 1); class (2 w + u) % 4
-              const uint32_t msk = VMASK << (VB * ((2 * w + u) & 3));
-              ra[4 * x + y] = ((w >> 1) ? v4.y : v4.x) & msk;
-              ra[4 * x + 2 + y] = ((w >> 1) ? v4.w : v4.z) & msk;
-            } else {
+            const uint4 v4 = *reinterpret_cast<const uint4*>(vt + 4 * lane);
+            ra0[4 * x + y] = v4.x & msk;      // u 0, rh 0
+            ra0[4 * x + 2 + y] = v4.z & msk;  // u 0, rh 1
+            ra1[4 * x + y] = v4.y & msk;      // u 1, rh 0
+            ra1[4 * x + 2 + y] = v4.w & msk;  // u 1, rh 1
+          }
+        sttm_16x256_x4(tq_w + G::cAV, ra0);
+        sttm_16x256_x4(tq_w + (16u << 16) + G::cAV, ra1);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          uint32_t ra[16];
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y) {
+              const uint32_t* vt = reinterpret_cast<const uint32_t*>(st + (size_t)x * G::SB + G::KTB) + y * G::VTW;
 #pragma unroll
               for (int rh = 0; rh < 2; ++rh) {
                 const int q = 2 * w + u + 8 * rh;
@@ -523,8 +589,8 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
                 ra[4 * x + 2 * rh + y] = word & (VMASK << (VB * (q % CV)));
               }
             }
-          }
-        sttm_16x256_x4(tq_w + ((uint32_t)(16 * u) << 16) + G::cAV, ra);
+          sttm_16x256_x4(tq_w + ((uint32_t)(16 * u) << 16) + G::cAV, ra);
+        }
       }
 
       // ---- scores of token j = lane of group w ----
@@ -574,23 +640,7 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
         }
       }
 
-      // ---- Value meta of this token, softmax bookkeeping (team-uniform max and exponent) ----
-      float vs[4], vmn[4];
-      int e_tok = 100;
-      if (gv) {
-        float smax = 0.f;
-#pragma unroll
-        for (int cg = 0; cg < 4; ++cg) {
-          const float2 f = meta_pair(vm[cg * kTcGS + lane]);
-          vs[cg] = f.x;
-          vmn[cg] = f.y;
-          smax = fmaxf(smax, f.x);
-        }
-        e_tok = min(156 - kLazy - (int)((__float_as_uint(smax) >> 23) & 0xffu), 100);
-      } else {
-#pragma unroll
-        for (int cg = 0; cg < 4; ++cg) vs[cg] = vmn[cg] = 0.f;
-      }
+      // ---- softmax bookkeeping (team-uniform max and exponent) ----
       bool need = nacc >= p.flush_tiles || (gv && e_cur > e_tok);
 #pragma unroll
       for (int r = 0; r < R; ++r) need = need || scv[r] > m_run[r] + (float)kLazy;
@@ -658,8 +708,8 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
       tc_wait_st();  // A_V stores of this tile
       fence_async_smem();
       tc_fence_before();
-      team_sync(bar_id);  // every read of this ring stage is done, A_V / B_V written
-      if (leader) {
+      __syncwarp();
+      if (last_of_team(cnt_v)) {  // every read of this ring stage is done, A_V / B_V written
         tc_fence_after();
 #pragma unroll
         for (int x = 0; x < 4; ++x)
@@ -667,6 +717,7 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
         mma_commit(vdone);
         if (i + S < n) fetch(i + S);  // refill this stage
       }
+      if (i + S < n) fetch_next();
       fresh = false;
       dirty = true;
       ++nacc;
