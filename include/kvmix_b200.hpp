@@ -18,6 +18,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <istream>
+#include <ostream>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -90,7 +93,35 @@ inline float half_to_float(uint16_t h) {
   return f;
 }
 
+// float -> binary16, round to nearest even, subnormals, inf; NaN -> sign | 0x7e00 (half.hpp:15-42)
+inline uint16_t float_to_half(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  const uint16_t sign = (uint16_t)((u >> 16) & 0x8000u);
+  const uint32_t a = u & 0x7fffffffu;
+  if (a > 0x7f800000u) return sign | 0x7e00u;  // NaN
+  if (a >= 0x477ff000u) return sign | 0x7c00u;  // >= 65520 rounds to inf (and inf)
+  if (a < 0x33000001u) return sign;             // < 2^-25 (+tie) rounds to zero
+  const int e = (int)(a >> 23) - 127;
+  uint32_t man = (a & 0x7fffffu) | 0x800000u;
+  if (e < -14) {  // subnormal result: shift so the LSB is 2^-24
+    const int sh = -14 - e + 13;
+    const uint32_t q = man >> sh, rem = man & ((1u << sh) - 1u), half = 1u << (sh - 1);
+    const uint32_t r = q + ((rem > half || (rem == half && (q & 1u))) ? 1u : 0u);
+    return sign | (uint16_t)r;
+  }
+  const uint32_t q = man >> 13, rem = man & 0x1fffu;
+  uint32_t h = ((uint32_t)(e + 15) << 10) + (q & 0x3ffu);
+  if (rem > 0x1000u || (rem == 0x1000u && (q & 1u))) ++h;  // (carry may reach the exponent: correct)
+  return sign | (uint16_t)h;
+}
+
 }  // namespace b200
+
+// ---- half.hpp:15-71 -----------------------------------------------------------------------
+inline uint16_t half_from_float(float x) { return b200::float_to_half(x); }
+inline float float_from_half(uint16_t h) { return b200::half_to_float(h); }
+inline float round_through_half(float x) { return b200::half_to_float(b200::float_to_half(x)); }
 
 // ---- tensor.hpp:12-41 --------------------------------------------------------------------
 struct Tensor4f {
@@ -157,16 +188,265 @@ struct TensorShape {
   int b = 0, nh = 0, t = 0, d = 0;
   size_t elems() const { return (size_t)b * nh * t * d; }
 };
-// QuantizedGroups with the packed payload as its word vector (PackedBuffer::words,
-// bitpack.hpp:35-46) and the binary16 meta pairs (the KVQG payload) alongside.
+// ---- bitpack.hpp:10-72 (PackedBuffer / PackedWriter; pack_* run on the device) -------------
+enum class PackLayout : uint8_t { kUniform = 0, kMixed3 = 1 };
+constexpr size_t kMixed3Block = 11;  // 10 x 3-bit + 1 x 2-bit fields per word
+inline uint32_t mixed3_q_max(size_t stream_idx) { return stream_idx % kMixed3Block == kMixed3Block - 1 ? 3u : 7u; }
+
+inline int feat_per_word(int bits) {
+  if (bits != 1 && bits != 2 && bits != 4)
+    throw std::invalid_argument("feat_per_word: bits must be 1, 2 or 4, got " + std::to_string(bits));
+  return 32 / bits;
+}
+
+struct PackedBuffer {
+  std::vector<uint32_t> words;
+  PackLayout layout = PackLayout::kUniform;
+  int bits = 0;
+  size_t logical_len = 0;
+  size_t word_count() const { return words.size(); }
+  // bounds-checked read of code idx (LSB-first fields; Mixed3 slot 10 is the 2-bit field)
+  uint32_t get(size_t idx) const {
+    if (idx >= logical_len)
+      throw std::out_of_range("PackedBuffer::get: index " + std::to_string(idx) + " out of bounds (logical_len " +
+                              std::to_string(logical_len) + ")");
+    if (layout == PackLayout::kMixed3) {
+      const uint32_t w = words[idx / kMixed3Block];
+      const size_t pos = idx % kMixed3Block;
+      return pos == kMixed3Block - 1 ? w >> 30 : (w >> (3 * pos)) & 7u;
+    }
+    const size_t fpw = (size_t)(32 / bits);
+    return (words[idx / fpw] >> (bits * (idx % fpw))) & ((1u << bits) - 1u);
+  }
+};
+
+namespace b200 {
+// codes -> words on the device (kvmix_pack: the reference's range errors, bitpack.cpp:23-46)
+inline PackedBuffer device_pack(std::span<const uint32_t> codes, int bits) {
+  PackedBuffer buf;
+  buf.layout = bits == 3 ? PackLayout::kMixed3 : PackLayout::kUniform;
+  buf.bits = bits;
+  buf.logical_len = codes.size();
+  const size_t nw = kvmix_packed_word_count(codes.size(), bits);
+  DevBuf dc(std::max<size_t>(codes.size(), 1) * 4), dw(std::max<size_t>(nw, 1) * 4);
+  if (!codes.empty()) dc.upload(codes.data(), codes.size() * 4);
+  check(kvmix_pack(dc.get<uint32_t>(), codes.size(), bits, dw.get<uint32_t>(), nullptr));
+  buf.words.resize(nw);
+  if (nw) dw.download(buf.words.data(), nw * 4);
+  return buf;
+}
+}  // namespace b200
+
+inline PackedBuffer pack_uniform(std::span<const uint32_t> codes, int bits) {
+  feat_per_word(bits);
+  return b200::device_pack(codes, bits);
+}
+inline PackedBuffer pack_mixed3(std::span<const uint32_t> codes) { return b200::device_pack(codes, 3); }
+inline uint32_t unpack_uniform(const PackedBuffer& buf, size_t idx) {
+  if (buf.layout != PackLayout::kUniform)
+    throw std::invalid_argument("unpack_uniform: buffer does not use a uniform layout");
+  return buf.get(idx);
+}
+inline uint32_t unpack_mixed3(const PackedBuffer& buf, size_t idx) {
+  if (buf.layout != PackLayout::kMixed3)
+    throw std::invalid_argument("unpack_mixed3: buffer does not use the mixed 3-bit layout");
+  return buf.get(idx);
+}
+
+// Streaming writer (host): codes straight into the word array, range-checked per field.
+class PackedWriter {
+ public:
+  static PackedWriter uniform(int bits) {
+    feat_per_word(bits);
+    return PackedWriter(PackLayout::kUniform, bits);
+  }
+  static PackedWriter mixed3() { return PackedWriter(PackLayout::kMixed3, 3); }
+  void push(uint32_t code) {
+    if (layout_ == PackLayout::kUniform) {
+      const uint32_t qm = (1u << bits_) - 1u;
+      if (code > qm)
+        throw std::invalid_argument("pack_uniform: code " + std::to_string(code) + " at index " + std::to_string(n_) +
+                                    " exceeds " + std::to_string(qm) + " for " + std::to_string(bits_) +
+                                    "-bit fields");
+      const size_t f = n_ % (size_t)(32 / bits_);
+      if (f == 0) words_.push_back(0u);
+      words_.back() |= code << (bits_ * f);
+    } else {
+      const size_t pos = n_ % kMixed3Block;
+      const uint32_t qm = mixed3_q_max(n_);
+      if (code > qm)
+        throw std::invalid_argument("pack_mixed3: code " + std::to_string(code) + " in block " +
+                                    std::to_string(n_ / kMixed3Block) + " at intra-block index " +
+                                    std::to_string(pos) + " exceeds " + std::to_string(qm));
+      if (pos == 0) words_.push_back(0u);
+      words_.back() |= code << (pos == kMixed3Block - 1 ? 30u : (uint32_t)(3 * pos));
+    }
+    ++n_;
+  }
+  size_t size() const { return n_; }
+  PackedBuffer finish() && {
+    PackedBuffer b;
+    b.words = std::move(words_);
+    b.layout = layout_;
+    b.bits = bits_;
+    b.logical_len = n_;
+    return b;
+  }
+
+ private:
+  PackedWriter(PackLayout l, int b) : layout_(l), bits_(b) {}
+  std::vector<uint32_t> words_;
+  PackLayout layout_;
+  int bits_;
+  size_t n_ = 0;
+};
+
+// ---- quant.cpp:8-75: scalar group helpers (host, bit-exact with the device kernels) --------
+inline int q_max_for_bits(int bits) {
+  if (bits < 1 || bits > 4) throw std::invalid_argument("unsupported bit width " + std::to_string(bits));
+  return bits == 3 ? 7 : (1 << bits) - 1;
+}
+inline float mixed3_wide_scale(float scale) { return scale * (7.0f / 3.0f); }
+
+// min / max in order from the first element; binary16 (scale, min) of the unrounded extrema
+inline GroupMeta compute_meta(std::span<const float> group, int q_max) {
+  if (group.empty()) throw std::invalid_argument("compute_meta: empty group");
+  if (q_max < 1) throw std::invalid_argument("compute_meta: q_max must be >= 1");
+  float mn = group[0], mx = group[0];
+  for (float v : group) {
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
+  }
+  volatile float range = mx - mn;  // (no contraction with the division)
+  return GroupMeta{round_through_half(range / (float)q_max), round_through_half(mn)};
+}
+namespace b200 {
+// lround((x - min) / s) clamped to [0, q_max]; x86-64 lround gives LONG_MIN for NaN / huge
+inline uint32_t encode_code(float x, float scale, float minv, long q_max) {
+  if (scale == 0.0f) return 0u;
+  volatile float d = x - minv;
+  const float v = d / scale;
+  if (!(std::fabs(v) < 0x1p63f)) return 0u;
+  const long q = std::lround(v);
+  return (uint32_t)(q < 0 ? 0 : q > q_max ? q_max : q);
+}
+inline float decode_code(uint32_t code, float scale, float minv) {
+  volatile float p = (float)code * scale;  // rounded product, then the add (no FMA)
+  return p + minv;
+}
+}  // namespace b200
+inline std::vector<uint32_t> quantize_group(std::span<const float> group, const GroupMeta& meta, int q_max) {
+  std::vector<uint32_t> codes(group.size());
+  for (size_t i = 0; i < group.size(); ++i) codes[i] = b200::encode_code(group[i], meta.scale, meta.min_val, q_max);
+  return codes;
+}
+inline std::vector<float> dequantize_group(std::span<const uint32_t> codes, const GroupMeta& meta) {
+  std::vector<float> out(codes.size());
+  for (size_t i = 0; i < codes.size(); ++i) out[i] = b200::decode_code(codes[i], meta.scale, meta.min_val);
+  return out;
+}
+
+// QuantizedGroups (quant.hpp:64-77): meta + packed codes; meta_half keeps the binary16 pairs
+// the device produced (the KVQG payload).
 struct QuantizedGroups {
   std::vector<GroupMeta> meta;
-  std::vector<uint32_t> words;
+  PackedBuffer codes;
   std::vector<uint16_t> meta_half;  // {scale, min} pairs, KVQG order
   QuantSpec spec;
   TensorShape shape;
   size_t group_count() const { return meta.size(); }
+  // the normative address maps (quant.cpp:77-95)
+  size_t stream_index(int bi, int hi, int ti, int di) const {
+    if (spec.grouping == Grouping::kPerChannelKey)
+      return (((size_t)bi * shape.nh + hi) * shape.d + di) * shape.t + ti;
+    return (((size_t)bi * shape.nh + hi) * shape.t + ti) * shape.d + di;
+  }
+  size_t meta_index(int bi, int hi, int ti, int di) const {
+    const int gs = spec.group_size;
+    if (spec.grouping == Grouping::kPerChannelKey)
+      return (((size_t)bi * shape.nh + hi) * shape.d + di) * (size_t)(shape.t / gs) + ti / gs;
+    return (((size_t)bi * shape.nh + hi) * shape.t + ti) * (size_t)((shape.d + gs - 1) / gs) + di / gs;
+  }
+  // one element read back (quant.cpp:97-100): Mixed3 narrow slots decode with scale * 7/3
+  float value_at(int bi, int hi, int ti, int di) const {
+    const size_t si = stream_index(bi, hi, ti, di);
+    const GroupMeta& m = meta[meta_index(bi, hi, ti, di)];
+    const bool narrow = spec.bits == 3 && si % kMixed3Block == kMixed3Block - 1;
+    return b200::decode_code(codes.get(si), narrow ? mixed3_wide_scale(m.scale) : m.scale, m.min_val);
+  }
 };
+
+// KVQG (quant.hpp:82-89, quant.cpp:148-207), little-endian
+namespace b200 {
+template <typename T>
+inline void put_le(std::vector<uint8_t>& o, T v) {
+  uint8_t b[sizeof(T)];
+  std::memcpy(b, &v, sizeof(T));
+  o.insert(o.end(), b, b + sizeof(T));
+}
+template <typename T>
+inline T take_le(std::span<const uint8_t> in, size_t& off, const char* who) {
+  if (off + sizeof(T) > in.size()) throw std::runtime_error(std::string(who) + ": truncated buffer");
+  T v;
+  std::memcpy(&v, in.data() + off, sizeof(T));
+  off += sizeof(T);
+  return v;
+}
+}  // namespace b200
+
+inline std::vector<uint8_t> serialize_quantized_groups(const QuantizedGroups& qg) {
+  std::vector<uint8_t> o;
+  o.reserve(48 + qg.meta.size() * 4 + qg.codes.words.size() * 4);
+  o.insert(o.end(), {'K', 'V', 'Q', 'G'});
+  b200::put_le<uint8_t>(o, 1);
+  b200::put_le<uint8_t>(o, (uint8_t)qg.spec.bits);
+  b200::put_le<uint8_t>(o, (uint8_t)qg.spec.grouping);
+  b200::put_le<uint8_t>(o, (uint8_t)qg.codes.layout);
+  for (uint32_t x : {(uint32_t)qg.spec.group_size, (uint32_t)qg.shape.b, (uint32_t)qg.shape.nh, (uint32_t)qg.shape.t,
+                     (uint32_t)qg.shape.d})
+    b200::put_le<uint32_t>(o, x);
+  b200::put_le<uint64_t>(o, qg.meta.size());
+  b200::put_le<uint64_t>(o, qg.codes.logical_len);
+  b200::put_le<uint64_t>(o, qg.codes.words.size());
+  for (const GroupMeta& m : qg.meta) {
+    b200::put_le<uint16_t>(o, half_from_float(m.scale));
+    b200::put_le<uint16_t>(o, half_from_float(m.min_val));
+  }
+  for (uint32_t w : qg.codes.words) b200::put_le<uint32_t>(o, w);
+  return o;
+}
+
+inline QuantizedGroups deserialize_quantized_groups(std::span<const uint8_t> in) {
+  static const char* who = "deserialize_quantized_groups";
+  if (in.size() < 4 || std::memcmp(in.data(), "KVQG", 4) != 0) throw std::runtime_error(std::string(who) + ": bad magic");
+  size_t off = 4;
+  const uint8_t version = b200::take_le<uint8_t>(in, off, who);
+  if (version != 1) throw std::runtime_error(std::string(who) + ": unsupported version " + std::to_string(version));
+  QuantizedGroups qg;
+  qg.spec.bits = b200::take_le<uint8_t>(in, off, who);
+  qg.spec.grouping = (Grouping)b200::take_le<uint8_t>(in, off, who);
+  qg.codes.layout = (PackLayout)b200::take_le<uint8_t>(in, off, who);
+  qg.codes.bits = qg.spec.bits;
+  qg.spec.group_size = (int)b200::take_le<uint32_t>(in, off, who);
+  qg.shape.b = (int)b200::take_le<uint32_t>(in, off, who);
+  qg.shape.nh = (int)b200::take_le<uint32_t>(in, off, who);
+  qg.shape.t = (int)b200::take_le<uint32_t>(in, off, who);
+  qg.shape.d = (int)b200::take_le<uint32_t>(in, off, who);
+  const uint64_t ng = b200::take_le<uint64_t>(in, off, who);
+  qg.codes.logical_len = b200::take_le<uint64_t>(in, off, who);
+  const uint64_t nw = b200::take_le<uint64_t>(in, off, who);
+  qg.meta.resize(ng);
+  qg.meta_half.resize(2 * ng);
+  for (uint64_t i = 0; i < ng; ++i) {
+    qg.meta_half[2 * i] = b200::take_le<uint16_t>(in, off, who);
+    qg.meta_half[2 * i + 1] = b200::take_le<uint16_t>(in, off, who);
+    qg.meta[i] = GroupMeta{float_from_half(qg.meta_half[2 * i]), float_from_half(qg.meta_half[2 * i + 1])};
+  }
+  qg.codes.words.resize(nw);
+  for (uint64_t i = 0; i < nw; ++i) qg.codes.words[i] = b200::take_le<uint32_t>(in, off, who);
+  if (off != in.size()) throw std::runtime_error(std::string(who) + ": trailing bytes");
+  return qg;
+}
 
 namespace b200 {
 inline QuantizedGroups quantize(const Tensor4f& x, const QuantSpec& spec) {
@@ -180,9 +460,12 @@ inline QuantizedGroups quantize(const Tensor4f& x, const QuantSpec& spec) {
   if (x.size()) dx.upload(x.data.data(), x.size() * 4);
   check(kvmix_quantize(g, dx.get(), KVMIX_F32, x.b, x.nh, x.t, x.d, spec.bits, spec.group_size, dw.get<uint32_t>(),
                        dm.get<uint16_t>(), nullptr));
-  q.words.resize(nw);
+  q.codes.words.resize(nw);
+  q.codes.layout = spec.bits == 3 ? PackLayout::kMixed3 : PackLayout::kUniform;
+  q.codes.bits = spec.bits;
+  q.codes.logical_len = x.size();
   q.meta_half.resize(2 * ng);
-  if (nw) dw.download(q.words.data(), nw * 4);
+  if (nw) dw.download(q.codes.words.data(), nw * 4);
   if (ng) dm.download(q.meta_half.data(), ng * 4);
   q.meta.resize(ng);
   for (size_t i = 0; i < ng; ++i) q.meta[i] = GroupMeta{half_to_float(q.meta_half[2 * i]), half_to_float(q.meta_half[2 * i + 1])};
@@ -262,11 +545,176 @@ class KVLayerCache {
   int64_t capacity_tokens() const { return cap_; }
   kvmix_cache* handle() const { return h_; }
 
+  // key_segments()/value_segments() (cache.hpp:75-76): one QuantizedGroups per age-out event,
+  // exported from the device store in the reference's word order (by value: a host copy)
+  std::vector<QuantizedGroups> key_segments() const { return segments(0); }
+  std::vector<QuantizedGroups> value_segments() const { return segments(1); }
+
+  // tail reads (cache.hpp:79-86); j indexes tail-local tokens, oldest first
+  float key_tail_at(int bi, int hi, int64_t j, int di) const { return tail_at(0, bi, hi, j, di); }
+  float value_tail_at(int bi, int hi, int64_t j, int di) const { return tail_at(1, bi, hi, j, di); }
+  // whole tail, [token][b][h][d] fp32 (the KVCD tail payload)
+  std::vector<float> tail(int side) const {
+    const int64_t n = side ? value_tail_tokens() : key_tail_tokens();
+    std::vector<float> out((size_t)n * b_ * nh_ * d_);
+    if (!out.empty()) {
+      b200::DevBuf d(out.size() * 4);
+      b200::check(kvmix_cache_export_tail(h_, side, d.get<float>(), nullptr));
+      b200::cuda(cudaDeviceSynchronize(), "export tail");
+      d.download(out.data(), out.size() * 4);
+    }
+    return out;
+  }
+
+  // Versioned binary state dump (cache.cpp:190-249): byte-identical to the reference's
+  void dump(std::ostream& os) const {
+    auto pod = [&os](auto v) { os.write(reinterpret_cast<const char*>(&v), sizeof(v)); };
+    os.write("KVCD", 4);
+    pod((uint8_t)1);
+    pod((int32_t)cfg_.layer_index);
+    pod((uint8_t)cfg_.key_bits);
+    pod((uint8_t)cfg_.value_bits);
+    pod((float)cfg_.key_rpc_ratio);
+    pod((float)cfg_.value_rpc_ratio);
+    pod((uint32_t)cfg_.group_size);
+    pod((uint32_t)b_);
+    pod((uint32_t)nh_);
+    pod((uint32_t)d_);
+    pod((int64_t)key_tail_tokens());
+    pod((int64_t)value_tail_tokens());
+    pod((int64_t)quantized_key_tokens());
+    pod((int64_t)quantized_value_tokens());
+    for (int side = 0; side < 2; ++side) {
+      const std::vector<QuantizedGroups> segs = segments(side);
+      pod((uint32_t)segs.size());
+      for (const QuantizedGroups& q : segs) {
+        const std::vector<uint8_t> bytes = serialize_quantized_groups(q);
+        pod((uint64_t)bytes.size());
+        os.write(reinterpret_cast<const char*>(bytes.data()), (std::streamsize)bytes.size());
+      }
+    }
+    for (int side = 0; side < 2; ++side) {
+      const std::vector<float> t = tail(side);
+      pod((uint64_t)t.size());
+      os.write(reinterpret_cast<const char*>(t.data()), (std::streamsize)(t.size() * 4));
+    }
+  }
+
+  // KVLayerCache::load (cache.cpp:251-281): segments imported in order, then the tails
+  static KVLayerCache load(std::istream& is, int64_t capacity_tokens = 0, kvmix_dtype tail_dtype = KVMIX_F32) {
+    auto pod = [&is](auto& v) {
+      is.read(reinterpret_cast<char*>(&v), sizeof(v));
+      if (!is) throw std::runtime_error("KVLayerCache::load: truncated stream");
+    };
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "KVCD", 4) != 0) throw std::runtime_error("KVLayerCache::load: bad magic");
+    uint8_t version = 0, kb = 0, vb = 0;
+    pod(version);
+    if (version != 1) throw std::runtime_error("KVLayerCache::load: unsupported version " + std::to_string(version));
+    LayerQuantConfig cfg;
+    int32_t layer = 0;
+    uint32_t gs = 0, b = 0, nh = 0, d = 0;
+    int64_t cnt[4];
+    pod(layer);
+    pod(kb);
+    pod(vb);
+    pod(cfg.key_rpc_ratio);
+    pod(cfg.value_rpc_ratio);
+    pod(gs);
+    pod(b);
+    pod(nh);
+    pod(d);
+    for (int64_t& c : cnt) pod(c);
+    cfg.layer_index = layer;
+    cfg.key_bits = kb;
+    cfg.value_bits = vb;
+    cfg.group_size = (int)gs;
+    std::vector<QuantizedGroups> segs[2];
+    for (int side = 0; side < 2; ++side) {
+      uint32_t n = 0;
+      pod(n);
+      for (uint32_t i = 0; i < n; ++i) {
+        uint64_t len = 0;
+        pod(len);
+        std::vector<uint8_t> bytes(len);
+        is.read(reinterpret_cast<char*>(bytes.data()), (std::streamsize)len);
+        if (!is) throw std::runtime_error("KVLayerCache::load: truncated segment");
+        segs[side].push_back(deserialize_quantized_groups(bytes));
+      }
+    }
+    std::vector<float> tails[2];
+    for (int side = 0; side < 2; ++side) {
+      uint64_t n = 0;
+      pod(n);
+      tails[side].resize(n);
+      is.read(reinterpret_cast<char*>(tails[side].data()), (std::streamsize)(n * 4));
+      if (!is) throw std::runtime_error("KVLayerCache::load: truncated tail");
+    }
+    const int64_t total = cnt[2] + cnt[0];
+    KVLayerCache c(cfg, (int)b, (int)nh, (int)d, std::max<int64_t>(capacity_tokens, std::max<int64_t>(total, 1)),
+                   tail_dtype);
+    for (int side = 0; side < 2; ++side) {
+      for (const QuantizedGroups& q : segs[side]) {
+        b200::DevBuf w(std::max<size_t>(q.codes.words.size(), 1) * 4), m(std::max<size_t>(q.meta.size(), 1) * 4);
+        std::vector<uint16_t> mh(2 * q.meta.size());
+        for (size_t i = 0; i < q.meta.size(); ++i) {
+          mh[2 * i] = half_from_float(q.meta[i].scale);
+          mh[2 * i + 1] = half_from_float(q.meta[i].min_val);
+        }
+        if (!q.codes.words.empty()) w.upload(q.codes.words.data(), q.codes.words.size() * 4);
+        if (!mh.empty()) m.upload(mh.data(), mh.size() * 2);
+        b200::check(kvmix_cache_import_segment(c.h_, side, q.shape.t, w.get<uint32_t>(), m.get<uint16_t>(), nullptr));
+      }
+      const int64_t tl = cnt[side];
+      if (tl > 0) {
+        b200::DevBuf t(tails[side].size() * 4);
+        t.upload(tails[side].data(), tails[side].size() * 4);
+        b200::check(kvmix_cache_import_tail(c.h_, side, t.get<float>(), tl, nullptr));
+      }
+    }
+    b200::cuda(cudaDeviceSynchronize(), "load");
+    return c;
+  }
+
  private:
   int64_t counter(int i) const {
     int64_t c[7];
     b200::check(kvmix_cache_counters(h_, c));
     return c[i];
+  }
+  std::vector<QuantizedGroups> segments(int side) const {
+    std::vector<QuantizedGroups> out;
+    const int64_t n = counter(5 + side);
+    const int bits = side ? cfg_.value_bits : cfg_.key_bits;
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t info[3];  // {t, words, groups}
+      b200::check(kvmix_cache_segment_info(h_, side, (int)i, info));
+      b200::DevBuf w(std::max<int64_t>(info[1], 1) * 4), m(std::max<int64_t>(info[2], 1) * 4);
+      b200::check(kvmix_cache_export_segment(h_, side, (int)i, w.get<uint32_t>(), m.get<uint16_t>(), nullptr));
+      b200::cuda(cudaDeviceSynchronize(), "export segment");
+      QuantizedGroups q;
+      q.spec = QuantSpec{bits, side ? Grouping::kPerTokenValue : Grouping::kPerChannelKey, cfg_.group_size};
+      q.shape = TensorShape{b_, nh_, (int)info[0], d_};
+      q.codes.layout = bits == 3 ? PackLayout::kMixed3 : PackLayout::kUniform;
+      q.codes.bits = bits;
+      q.codes.logical_len = q.shape.elems();
+      q.codes.words.resize((size_t)info[1]);
+      q.meta_half.resize(2 * (size_t)info[2]);
+      if (info[1]) w.download(q.codes.words.data(), (size_t)info[1] * 4);
+      if (info[2]) m.download(q.meta_half.data(), (size_t)info[2] * 4);
+      q.meta.resize((size_t)info[2]);
+      for (size_t g = 0; g < q.meta.size(); ++g)
+        q.meta[g] = GroupMeta{b200::half_to_float(q.meta_half[2 * g]), b200::half_to_float(q.meta_half[2 * g + 1])};
+      out.push_back(std::move(q));
+    }
+    return out;
+  }
+  float tail_at(int side, int bi, int hi, int64_t j, int di) const {
+    const int64_t n = side ? value_tail_tokens() : key_tail_tokens();
+    if (j < 0 || j >= n || bi < 0 || bi >= b_ || hi < 0 || hi >= nh_ || di < 0 || di >= d_)
+      throw std::out_of_range("KVLayerCache: tail index out of range");
+    return tail(side)[((size_t)j * b_ * nh_ + (size_t)bi * nh_ + hi) * d_ + di];
   }
   void create(int64_t cap) {
     const kvmix_layer_config cc = cfg_.c();

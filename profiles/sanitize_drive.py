@@ -1,6 +1,6 @@
 """compute-sanitizer target: a small pass over every device path (quantize / pack /
 dequantize, prefill + decode appends incl. Key-group age-outs, the fused append+attend,
-both tensor-core attention kernels and the generic one, multi-row / GQA passes, snapshot and
+the three tensor-core attention kernels (single-warp and warp-specialized IMMA, tcgen05) and the generic one, multi-row / GQA passes, snapshot and
 segment export) on shapes small enough for memcheck / racecheck / synccheck to finish.
 
   compute-sanitizer --tool memcheck --target-processes all python profiles/sanitize_drive.py
@@ -21,7 +21,11 @@ for bits in (2, 3, 4):
         spec = K.QuantSpec(bits, K.Grouping(0 if key else 1), 32)
         qg = (K.quantize_key_tensor if key else K.quantize_value_tensor)(x, spec)
         qg.dequantize()
-for ws in (0, 2):
+# single-warp IMMA, tcgen05 + window launch, warp-specialized IMMA (SANITIZE_CONFIGS=0,1 picks)
+CONFIGS = ((0, 0), (1, 1), (0, 2))
+PICK = [int(i) for i in os.environ.get("SANITIZE_CONFIGS", "0,1,2").split(",")]
+for tc, ws in (CONFIGS[i] for i in PICK):
+    K.set_knob("KVMIX_TC", tc)
     K.set_knob("KVMIX_WS", ws)
     for kb, vb, r, D, G in ((2, 2, 0.1, 128, 1), (3, 4, 0.2, 128, 2), (4, 3, 0.15, 64, 1), (2, 3, 0.1, 128, 4)):
         B, H = 2, 3
