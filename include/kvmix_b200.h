@@ -105,8 +105,10 @@ kvmix_status kvmix_rpc_target(int64_t current, double r, int64_t* out);
 /* KVLayerCache(config, batch, heads, head_dim) (cache.cpp:36-43). `capacity_tokens` is
  * the device reservation (total tokens the cache may ever hold); `tail_dtype` selects
  * the full-precision window storage (KVMIX_F32 keeps arbitrary fp32 inputs exact,
- * KVMIX_F16 matches the 16-bit accounting). Device constraints: head_dim % 64 == 0,
- * head_dim <= 256, group_size % 16 == 0. Allocates on the current device. */
+ * KVMIX_F16 matches the 16-bit accounting). Device constraints: head_dim <= 256 (any value:
+ * the tile layout rounds it up to a multiple of 64 channels whose extra codes are zero;
+ * the tensor-core attention kernels serve 64 / 128, the generic kernel the rest),
+ * group_size % 16 == 0. Allocates on the current device. */
 kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int heads, int head_dim,
                                 int64_t capacity_tokens, kvmix_dtype tail_dtype, kvmix_cache** out);
 void kvmix_cache_destroy(kvmix_cache* cache);

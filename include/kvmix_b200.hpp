@@ -8,7 +8,7 @@
 // the device-pointer performance API is the C ABI itself (kvmix_cache_handle()).
 // Exceptions follow the reference: KVMIX_INVALID_ARGUMENT -> std::invalid_argument,
 // KVMIX_OUT_OF_RANGE -> std::out_of_range, anything else -> std::runtime_error.
-// Device constraints (kvmix_b200.h): head_dim % 64 == 0, head_dim <= 256, group_size % 16 == 0.
+// Device constraints (kvmix_b200.h): head_dim <= 256, group_size % 16 == 0.
 // The device cache reserves capacity; append() grows it (segments and tails re-imported)
 // when a call would exceed it.
 #pragma once

@@ -44,10 +44,12 @@ def _cfg_c(cfg: LayerQuantConfig) -> LayerConfigC:
 
 
 class KVLayerCache:
-    """KVLayerCache(config, batch, heads, head_dim) with a fixed device reservation.
+    """KVLayerCache(config, batch, heads, head_dim) over a device reservation.
 
-    capacity_tokens: total tokens the cache may ever hold (device memory is reserved up
-    front; the reference grows std::vectors instead). tail_dtype: torch.float32 keeps any
+    capacity_tokens: tokens reserved up front; append() grows the reservation (x2, segments
+    and tails re-imported into a new device store) when a call would exceed it, like the
+    reference's std::vectors (append_raw, the benchmark's device-pointer path, does not
+    grow). tail_dtype: torch.float32 keeps any
     fp32 input exact (the reference's fp32 tail); torch.float16 halves the window and is
     exact for inputs on the binary16 grid (the reference's own regime, helpers.hpp:14-18).
     """
@@ -139,7 +141,37 @@ class KVLayerCache:
         self._check_append(k, v)
         if v.dtype != k.dtype:
             v = v.to(k.dtype)
-        check(lib().kvmix_cache_append(self._h, _ptr(k), _ptr(v), _dtype_code(k), int(k.shape[2]), _stream()))
+        t = int(k.shape[2])
+        if self.total_tokens() + t > self._cap:
+            self._grow(max(2 * self._cap, self.total_tokens() + t))
+        check(lib().kvmix_cache_append(self._h, _ptr(k), _ptr(v), _dtype_code(k), t, _stream()))
+
+    def _grow(self, cap: int) -> None:
+        """Re-create the device store with a larger reservation: the reference segments are
+        exported and re-imported in order, then the tails (bit-identical state)."""
+        segs = (self.key_segments(), self.value_segments())
+        tails = (self._tail(0), self._tail(1))
+        h = C.c_void_p()
+        dt = _lib.F16 if self._tail_dtype == torch.float16 else _lib.F32
+        check(lib().kvmix_cache_create(C.byref(_cfg_c(self._cfg)), self._b, self._nh, self._d, int(cap), dt,
+                                       C.byref(h)))
+        try:
+            if getattr(self, "_shard", None):
+                check(lib().kvmix_cache_set_shard(h, *self._shard))
+            for side, lst in enumerate(segs):
+                for qg in lst:
+                    check(lib().kvmix_cache_import_segment(h, side, qg.shape.t, _ptr(qg.codes.words), _ptr(qg.meta),
+                                                           _stream()))
+            for side, tail in enumerate(tails):
+                if tail.shape[0]:
+                    check(lib().kvmix_cache_import_tail(h, side, _ptr(tail), int(tail.shape[0]), _stream()))
+            torch.cuda.current_stream().synchronize()
+        except Exception:
+            lib().kvmix_cache_destroy(h)
+            raise
+        lib().kvmix_cache_destroy(self._h)
+        self._h = h
+        self._cap = int(cap)
 
     def append_raw(self, k_ptr: int, v_ptr: int, dtype_code: int, t: int, stream: int) -> None:
         """Device-pointer append without checks or copies (benchmark hot loop)."""

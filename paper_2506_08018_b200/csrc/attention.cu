@@ -6,8 +6,8 @@
 // dequantization inside the dot products (no K/V materialization), online softmax per
 // query row, split-K over the token axis with a deterministic combine kernel. It handles
 // every shape the device cache accepts (any G = Hq/H, any number of query rows, all bit
-// widths, tokens in the full-precision tail). The tensor-core path (attention_mma.cu)
-// serves D in {64, 128} with 2/3/4-bit Keys and 2/4-bit Values; this kernel the rest.
+// widths, any head_dim up to 256, tokens in the full-precision tail). The tensor-core paths
+// (attention_mma.cu, attention_ws.cu, attention_tc.cu) serve D in {64, 128}; this kernel the rest.
 #include <algorithm>
 #include <cmath>
 
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kWarps * 32) attend_generic_kernel(KV kv, cons
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nch = D / 32;
+  const int nch = (D + 31) / 32;  // channels d = lane + 32 c < D per lane (any head_dim <= 256)
   const int64_t j0 = (int64_t)split * chunk, j1 = min(T, j0 + chunk);
   double cs = 0.0;
   for (int r = 0; r < R; ++r) {
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kWarps * 32) attend_generic_kernel(KV kv, cons
       float part = 0.f;
       for (int c = 0; c < nch; ++c) {
         const int d = lane + 32 * c;
-        part = fmaf(qs[r * D + d], kv.key(bh, j, d), part);
+        if (d < D) part = fmaf(qs[r * D + d], kv.key(bh, j, d), part);
       }
       const float s = warp_sum(part) * inv;
       cs += (double)s;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kWarps * 32) attend_generic_kernel(KV kv, cons
       l = l * alpha + p;
 #pragma unroll
       for (int c = 0; c < kMaxLaneCh; ++c) {
-        if (c < nch) acc[c] = acc[c] * alpha + p * kv.val(bh, j, lane + 32 * c);
+        if (c < nch && lane + 32 * c < D) acc[c] = acc[c] * alpha + p * kv.val(bh, j, lane + 32 * c);
       }
       m = mn;
     }
@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(kWarps * 32) attend_generic_kernel(KV kv, cons
       wm[warp * R + r] = m;
       wl[warp * R + r] = l;
     }
-    for (int c = 0; c < nch; ++c) wacc[(warp * R + r) * D + lane + 32 * c] = acc[c];
+    for (int c = 0; c < nch; ++c)
+      if (lane + 32 * c < D) wacc[(warp * R + r) * D + lane + 32 * c] = acc[c];
   }
   if (lane == 0) wcs[warp] = cs;  // lane 0 saw every score of its warp
   __syncthreads();

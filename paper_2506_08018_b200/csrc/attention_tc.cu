@@ -146,9 +146,12 @@ struct TcGeo {
   static constexpr int AKC = KT / 4;
   static constexpr int cDV = 0, cDK = N, cAK = 2 * N, cAV = 2 * N + AKC;
   static constexpr int kCols = cAV + 32;
-  static constexpr int TC = kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;  // columns per team
-  static constexpr int T = 512 / TC < 4 ? 512 / TC : 4;                      // teams per CTA (one CTA per SM)
-  static constexpr int NCOL = T * TC;
+#ifndef KVB_TC_TEAMS
+#define KVB_TC_TEAMS 4
+#endif
+  static constexpr int TC = (kCols + 31) / 32 * 32;                          // columns per team
+  static constexpr int T = 512 / TC < KVB_TC_TEAMS ? 512 / TC : KVB_TC_TEAMS;  // teams per CTA (one CTA per SM)
+  static constexpr int NCOL = T * TC <= 128 ? 128 : T * TC <= 256 ? 256 : 512;  // (allocation: a power of two)
   static constexpr int THREADS = T * 128;
   // shared memory per team: ring | B_K | B_V | narrow tables | exchange | barriers
   static constexpr int BK = KT * N;   // row k = 16 B, N / 16 chunks of KT rows
@@ -756,7 +759,9 @@ bool launch_tc(const TcParams& p0, int BH, Workspace& ws, cudaStream_t st, TcExt
   const int64_t workers = (int64_t)num_sms() * G::T;
   p.C = (int)std::max<int64_t>(1, std::min<int64_t>(workers, p.NT));
   const int ctas = (p.C + G::T - 1) / G::T;
-  const size_t slots = (size_t)ctas * G::T + BH;
+  // partial slots worker + bh for every possible worker: scratch depends on (B, H, rows, SM
+  // count) only, never on the token count (scratch.hpp:14-21)
+  const size_t slots = (size_t)workers + BH;
   p.part_ml = ws.ml(st, slots * R);
   p.part_acc = ws.acc(st, slots * R * kTcD);
   p.part_cs = ws.cs(st, slots + 1);

@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kWsPairs * 64, KVB_WS_MIN_CTAS) attend_ws_kern
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = r < prows ? sc[(sl * R + r) * 32 + lane] : -INFINITY;
       __syncwarp();
-      if (lane == 0) mbar_arrive_a(sempty_a + 8 * sl);
+      if (lane == 0 && !slot_free) mbar_arrive_a(sempty_a + 8 * sl);  // (slot_free: nobody waits; see above)
       if (++sl == kScoreSlots) {
         sl = 0;
         sphase ^= 1u;

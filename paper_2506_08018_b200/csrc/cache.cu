@@ -151,10 +151,14 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     // ---- key age-out: one group of gs tokens for one bh --------------------------------
     const int bh = blk % a.BH, g = blk / a.BH;  // group index within this segment
     Src<TI, TT> src{static_cast<const TT*>(a.k_tail), a.k_cap, a.k_start, a.k_L, kin, a.t};
-    uint8_t* codes = sm;  // [gs][D]
+    const int Dl = a.kv.dl;
+    uint8_t* codes = sm;  // [gs][Dl] (channels D..Dl-1 of the tile layout: zero codes)
     const int q_max = q_max_for_bits(a.kbits);
     const int64_t gglob = a.k_q0 / gs + g;
-    float* xs = reinterpret_cast<float*>(sm + (size_t)gs * D);  // [gs][D] staged column values
+    float* xs = reinterpret_cast<float*>(sm + (size_t)gs * Dl);  // [gs][D] staged column values
+    if (Dl != D) {
+      for (int e = threadIdx.x; e < gs * (Dl - D); e += blockDim.x) codes[(e / (Dl - D)) * Dl + D + e % (Dl - D)] = 0;
+    }
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       const int64_t j0 = (int64_t)g * gs;
       // stage the channel's gs values with the loads in flight together, then reduce
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       const uint64_t sbase = ((uint64_t)a.kv.gbh(bh) * D + d) * (uint64_t)a.k_n + (uint64_t)j0;
       for (int jj = 0; jj < gs; ++jj) {
         const float x = xs[jj * D + d];
-        codes[jj * D + d] = (uint8_t)encode(x, sc, mnv, a.kbits, is_narrow(a.kbits, sbase + jj));
+        codes[jj * Dl + d] = (uint8_t)encode(x, sc, mnv, a.kbits, is_narrow(a.kbits, sbase + jj));
       }
     }
     if (bh == 0 && threadIdx.x == 0) a.k_info[gglob] = make_int2((int)a.k_n, g * gs);
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     const int64_t tile0 = (a.k_q0 + (int64_t)g * gs) / 16;
     for (int tt = 0; tt < gs / 16; ++tt) {
       uint32_t* tile = a.k_tiles + tile_index(a.kv, bh, tile0 + tt);
-      emit_tile(true, D, a.kbits, codes + tt * 16 * D, tile, false, 0, 16);
+      emit_tile(true, Dl, a.kbits, codes + tt * 16 * Dl, tile, false, 0, 16);
     }
     return;
   }
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     for (int c = 0; c < LC; ++c) {
       const int d = lane * LC + c;
       const uint64_t si = ((uint64_t)a.vv.gbh(bh) * a.v_n + (uint64_t)tl) * D + d;
-      tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
+      tile_or(tp, false, a.vv.dl, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
     }
     return;
   }
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     for (int e = threadIdx.x; e < (i_hi - i_lo) * D; e += blockDim.x) {
       const int i = i_lo + e / D, d = e % D;
       const uint32_t code = codes[i * D + d];
-      tile_or(tp, false, D, a.vbits, i, d, code);
+      tile_or(tp, false, a.vv.dl, a.vbits, i, d, code);
     }
     return;
   }
@@ -340,7 +344,7 @@ __global__ void export_words_kernel(SideView s, bool key, int D, int BH, int64_t
       const int64_t j = S + tl;
       const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
       const int i = (int)(j & 15);
-      const uint32_t code = tile_get(tile, key, D, bits, i, d);
+      const uint32_t code = tile_get(tile, key, s.dl, bits, i, d);
       word |= code << field_shift(bits, (uint32_t)k);
     }
     words[w] = word;
@@ -404,7 +408,7 @@ __global__ void import_kernel(SideView s, uint32_t* tiles, uint32_t* dmeta, int2
     const uint32_t code = (words[p / cpw] >> field_shift(bits, pos)) & field_mask(bits, pos);
     const int64_t j = q0 + tl;
     uint32_t* tile = tiles + tile_index(s, bh, j >> 4);
-    tile_or(tile, key, D, bits, (int)(j & 15), d, code);
+    tile_or(tile, key, s.dl, bits, (int)(j & 15), d, code);
     if (key) {
       if (tl % gs == 0) {
         dmeta[kmeta_index(s, bh, j / gs) + d] = meta[((size_t)bh * D + d) * (n / gs) + tl / gs];
@@ -581,7 +585,7 @@ void cache_append(kvmix_cache* c, const void* k, const void* v, kvmix_dtype dt, 
   const bool any_stay = a.k_stay0 < t || a.v_stay0 < t;
   a.tail_blocks = any_stay ? grid_for((size_t)2 * BH * t * D, kAppendThreads) : 0;
 
-  const size_t smem_k = a.k_blocks ? (size_t)gs * D + (size_t)gs * D * 4 : 0;  // codes + staged values
+  const size_t smem_k = a.k_blocks ? (size_t)gs * c->Dl + (size_t)gs * D * 4 : 0;  // codes + staged values
   const size_t smem_v = a.v_blocks ? (size_t)16 * D + (size_t)16 * (D + 1) * 4 + (size_t)16 * c->cgroups() * 4 : 0;
   const size_t smem = std::max(smem_k, smem_v);
   // ring hazard: new tail slots could alias aged slots still being read only if L + t > cap

