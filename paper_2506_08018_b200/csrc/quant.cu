@@ -16,6 +16,7 @@
 //  * Values: the stream is the input order itself; one CTA per span of R rows (token
 //    slots), thread-per-output-word, same ownership rule at the span end.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -61,25 +62,32 @@ struct Vec<float> {
 };
 
 // One uniform 1/2/4-bit word of CPW codes sharing a group's (scale, min), bit-exact with
-// encode(): branch-free reciprocal path; codes whose va lies near a half-integer (or is NaN
-// or huge) are flagged and redone by the exact encode() afterwards (rare).
-template <int BITS, int CPW>
+// encode(): va = RN(x - min) * rcp(scale) lies within 2^-19 of the reference quotient v, so
+// clamp(va) rounded to the nearest integer (the 1.5 * 2^23 magic add: the integer lands in
+// the low mantissa bits) is lround(v) unless va is within kTie of a half-integer; those codes
+// (and, for fp32 inputs, NaN-free huge quotients the reference maps to 0) are redone by the
+// exact encode() afterwards (rare). NaN -> 0 through the clamp, like the reference. fp16
+// inputs cannot produce |v| >= 2^62 (|x - min| <= 2^17, scale >= 2^-24), so WIDE = false
+// skips that check.
+template <int BITS, int CPW, bool WIDE>
 __device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc, float mnv, int q_max) {
   constexpr float kTie = 0x1p-14f;
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  if (sc == 0.0f) return 0u;
   const float rc = rcp_approx(sc);
+  const float qm = (float)q_max;
   uint32_t word = 0, slow = 0;
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
     const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
-    const float r = floorf(va + 0.5f);
-    const float f = va + 0.5f - r;
-    const bool tie = fabsf(f - 0.5f) > 0.5f - kTie;                          // near an integer t
-    const bool inr = fabsf(va - 0.5f * q_max) <= 0.5f * q_max - 0.5f + kTie;  // not clamped
-    const bool bad = !(fabsf(va) < 0x1p62f);                                  // NaN, inf, huge
-    slow |= (uint32_t)((inr && tie) || bad) << i;
-    word |= (uint32_t)fminf(fmaxf(r, 0.f), (float)q_max) << (BITS * i);
+    const float vc = fminf(fmaxf(va, 0.f), qm);  // (NaN -> 0)
+    const float u = __fadd_rn(vc, kMagic);
+    const float dr = vc - __fsub_rn(u, kMagic);  // vc - RN(vc), in [-0.5, 0.5]
+    bool redo = fabsf(dr) > 0.5f - kTie;         // near a half-integer: ties decide
+    if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
+    slow |= (uint32_t)redo << i;
+    word |= (__float_as_uint(u) & (uint32_t)q_max) << (BITS * i);
   }
-  if (sc == 0.0f) return 0u;
   while (slow) {
     const int i = __ffs(slow) - 1;
     slow &= slow - 1;
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
         for (int k = 0; k < CPW; ++k) v[k] = ld_f(&xs[(j * CPW + k) * D + d]);
         const uint32_t m = ms[d * gpt + (j * CPW) / gs];
         const size_t w = (((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j;
-        words[w] = encode_word<BITS, CPW>(v, meta_scale(m), meta_min(m), q_max);
+        words[w] = encode_word<BITS, CPW, !std::is_same<T, __half>::value>(v, meta_scale(m), meta_min(m), q_max);
       }
       return;
     }
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
   if (!ok) return;
   if (lane == lead) meta[w / L] = m;
   const float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
-  const uint32_t word = encode_word<BITS, CPW>(v, sc, mnv, q_max);
+  const uint32_t word = encode_word<BITS, CPW, !std::is_same<T, __half>::value>(v, sc, mnv, q_max);
   words[w] = word;
 }
 
