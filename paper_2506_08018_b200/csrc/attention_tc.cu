@@ -483,7 +483,9 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
               ytab[(w * R + r) * kTcD + dch[ii]] = qv[r][ii] * (wide_scale(sc[ii]) - sc[ii]);
             }
           }
-          beta[r] = bt;  // lane partial (reduced after the Key arrival, off the MMA's critical path)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
+          beta[r] = bt;
         }
         // A: the group's two 16-token Key tiles -> TMEM rows 32 w + 16 u + (g, g + 8)
 #pragma unroll
@@ -532,29 +534,7 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
         mma_commit(sfull);
       }
 
-      // ---- min-term of the group's scores; this token's Value meta ----
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) beta[r] += __shfl_xor_sync(0xffffffffu, beta[r], o);
-      float vs[4], vmn[4];
-      int e_tok = 100;
-      if (gv) {
-        float smax = 0.f;
-#pragma unroll
-        for (int cg = 0; cg < 4; ++cg) {
-          const float2 f = meta_pair(vm[cg * kTcGS + lane]);
-          vs[cg] = f.x;
-          vmn[cg] = f.y;
-          smax = fmaxf(smax, f.x);
-        }
-        e_tok = min(156 - kLazy - (int)((__float_as_uint(smax) >> 23) & 0xffu), 100);
-      } else {
-#pragma unroll
-        for (int cg = 0; cg < 4; ++cg) vs[cg] = vmn[cg] = 0.f;
-      }
-
-      // ---- Values of all four groups -> A_V ----
+      // ---- Values of all four groups, channels 32 w .. 32 w + 31 -> A_V ----
       if (i >= 1) {  // the previous tile's Value k-steps are done with A_V / B_V / D_V
         mbar_wait(vdone, (i - 1) & 1);
         tc_fence_after();
@@ -643,7 +623,24 @@ __global__ void __launch_bounds__(TcGeo<KB, VB, R>::THREADS, 1) attend_tc_kernel
         }
       }
 
-      // ---- softmax bookkeeping (team-uniform max and exponent) ----
+      // ---- Value meta of this token, softmax bookkeeping (team-uniform max and exponent) ----
+      float vs[4], vmn[4];
+      int e_tok = 100;
+      if (gv) {
+        float smax = 0.f;
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg) {
+          const float2 f = meta_pair(vm[cg * kTcGS + lane]);
+          vs[cg] = f.x;
+          vmn[cg] = f.y;
+          smax = fmaxf(smax, f.x);
+        }
+        e_tok = min(156 - kLazy - (int)((__float_as_uint(smax) >> 23) & 0xffu), 100);
+      } else {
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg) vs[cg] = vmn[cg] = 0.f;
+      }
+
       bool need = nacc >= p.flush_tiles || (gv && e_cur > e_tok);
 #pragma unroll
       for (int r = 0; r < R; ++r) need = need || scv[r] > m_run[r] + (float)kLazy;

@@ -131,11 +131,23 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
 
   for (int i = threadIdx.x; i < D * gpt; i += blockDim.x) {
     const int d = i % D, g = i / D;  // d fastest: conflict-free smem columns
-    float mn = ld_f(&xs[(g * gs) * D + d]), mx = mn;
+    // fminf / fmaxf skip NaN like the reference's ordered fold (quant.hpp:128-139) and differ
+    // from it only in the sign of a zero extremum (the fold keeps the first of -0 / +0) and
+    // when the FIRST element is NaN (the fold then stays NaN): those groups redo the fold
+    const float x0 = ld_f(&xs[(g * gs) * D + d]);
+    float mn = x0, mx = x0;
     for (int j = 1; j < gs; ++j) {
       const float v = ld_f(&xs[(g * gs + j) * D + d]);
-      mn = v < mn ? v : mn;
-      mx = v > mx ? v : mx;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    if (mn == 0.f || mx == 0.f || isnan(x0)) {
+      mn = mx = x0;
+      for (int j = 1; j < gs; ++j) {
+        const float v = ld_f(&xs[(g * gs + j) * D + d]);
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+      }
     }
     const uint32_t m = make_meta(mn, mx, q_max);
     ms[d * gpt + g] = m;
