@@ -45,21 +45,46 @@ struct Src {
   }
 };
 
+// imma_element for a power-of-two channel count (D in {64, 128, 256}) with log2 arguments:
+// shifts and masks instead of the generic divisions (the Key age-out assembles every field
+// of two tiles per group; this keeps it a few instructions per field).
+__device__ __forceinline__ void imma_element_p2(bool key, int ld, int b, int lc, int lane, int w, int f, int* i, int* d,
+                                                int* shift) {
+  const int C = 1 << lc, e = f >> lc, cls = f & (C - 1);
+  const int g = lane >> 2, t = lane & 3;
+  *shift = 8 * e + b * cls;
+  if (key) {
+    const int lnk = ld - 5;  // NK = D / 32
+    const int q = ((w >> 1) << lc) + cls, rb = w & 1;
+    *i = g + 8 * rb;
+    *d = ((q & ((1 << lnk) - 1)) << 5) + ((q >> lnk) << 4) + 4 * t + e;
+  } else {
+    const int lnm = ld - 4;  // NM = D / 16
+    const int q = (w << lc) + cls;
+    *i = 4 * t + e;
+    *d = ((q & ((1 << lnm) - 1)) << 4) + ((q >> lnm) << 3) + g;
+  }
+}
+
 // Assemble one tile from codes[16][D] (u8, shared). For partial value tiles only rows in
 // [i_lo, i_hi) contribute and words are OR-merged.
 __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes, uint32_t* tile, bool atomic,
                                  int i_lo, int i_hi) {
   if (!key) bits = vstore_bits(bits);  // 3-bit Values: 4-bit fields
+  const bool p2 = (D & (D - 1)) == 0;
+  const int ld = 31 - __clz(D);
   if (bits != 3) {  // IMMA layout: 4 bytes x C classes per word
     const int wpl = plane_wpl(D, bits), cw = wpl < 4 ? wpl : 4;
     const int nf = 32 / bits;
+    const int lc = bits == 1 ? 3 : bits == 2 ? 2 : 1;  // log2(8 / bits)
     for (int pw = threadIdx.x; pw < 32 * wpl; pw += blockDim.x) {
       const int chunk = pw / (32 * cw), within = pw % (32 * cw);
       const int lane = within / cw, w = chunk * cw + within % cw;
       uint32_t word = 0;
       for (int f = 0; f < nf; ++f) {
         int i, d, sh;
-        imma_element(key, D, bits, lane, w, f, &i, &d, &sh);
+        if (p2) imma_element_p2(key, ld, bits, lc, lane, w, f, &i, &d, &sh);
+        else imma_element(key, D, bits, lane, w, f, &i, &d, &sh);
         if (i < i_lo || i >= i_hi) continue;
         word |= (uint32_t)codes[i * D + d] << sh;
       }
@@ -79,7 +104,8 @@ __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes
       uint32_t word = 0;
       for (int f = 0; f < 16; ++f) {
         int i, d, sh;
-        imma_element(true, D, 2, lane, w, f, &i, &d, &sh);
+        if (p2) imma_element_p2(true, ld, 2, 2, lane, w, f, &i, &d, &sh);
+        else imma_element(true, D, 2, lane, w, f, &i, &d, &sh);
         if (i < i_lo || i >= i_hi) continue;
         word |= ((uint32_t)codes[i * D + d] & 3u) << sh;
       }
@@ -97,7 +123,15 @@ __device__ inline void emit_tile(bool key, int D, int bits, const uint8_t* codes
       uint32_t word = 0;
       for (int f = 0; f < 32; ++f) {
         int i, d, sh;
-        imma_key_hi_element(D, lane, w, f, &i, &d, &sh);
+        if (p2) {  // imma_key_hi_element with shifts (NK = D / 32 a power of two)
+          const int lnk = ld - 5, e = f >> 3, z = 8 * w + (f & 7);
+          const int q = z & ((2 << lnk) - 1), rb = z >> (lnk + 1);
+          i = (lane >> 2) + 8 * rb;
+          d = ((q & ((1 << lnk) - 1)) << 5) + ((q >> lnk) << 4) + 4 * (lane & 3) + e;
+          sh = 8 * e + (f & 7);
+        } else {
+          imma_key_hi_element(D, lane, w, f, &i, &d, &sh);
+        }
         if (i < i_lo || i >= i_hi) continue;
         word |= ((uint32_t)codes[i * D + d] >> 2) << sh;
       }
@@ -159,11 +193,24 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
     if (Dl != D) {
       for (int e = threadIdx.x; e < gs * (Dl - D); e += blockDim.x) codes[(e / (Dl - D)) * Dl + D + e % (Dl - D)] = 0;
     }
+    const int64_t j0 = (int64_t)g * gs;
+    // ring slot of logical token j0 (the group's tokens walk the ring incrementally)
+    const int64_t slot0 = j0 < src.L ? (src.start + j0) % src.cap : 0;
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
-      const int64_t j0 = (int64_t)g * gs;
       // stage the channel's gs values with the loads in flight together, then reduce
+      int64_t slot = slot0;
 #pragma unroll 8
-      for (int jj = 0; jj < gs; ++jj) xs[jj * D + d] = src.at(bh, j0 + jj, d, D);
+      for (int jj = 0; jj < gs; ++jj) {
+        const int64_t j = j0 + jj;
+        float x;
+        if (j < src.L) {
+          x = ld_f<TT>(src.tail + ((size_t)bh * src.cap + (size_t)slot) * D + d);
+          if (++slot == src.cap) slot = 0;
+        } else {
+          x = round_to<TT>(ld_f<TI>(src.in + ((size_t)bh * src.t + (size_t)(j - src.L)) * D + d));
+        }
+        xs[jj * D + d] = x;
+      }
       float mn = xs[d], mx = mn;
       for (int jj = 1; jj < gs; ++jj) {
         const float x = xs[jj * D + d];
@@ -172,12 +219,16 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(AppendArgs a, co
       }
       const uint32_t m = make_meta(mn, mx, q_max);
       a.k_meta[kmeta_index(a.kv, bh, gglob) + d] = m;
-      const float sc = meta_scale(m), mnv = meta_min(m);
+      const float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
+      const float ws = wide_scale(sc), rcw = rcp_approx(ws);
       // reference stream index inside this segment [B,H,n,D]: (bh*D + d)*n + t_local
       const uint64_t sbase = ((uint64_t)a.kv.gbh(bh) * D + d) * (uint64_t)a.k_n + (uint64_t)j0;
+      int r11 = (int)(sbase % 11u);
       for (int jj = 0; jj < gs; ++jj) {
         const float x = xs[jj * D + d];
-        codes[jj * Dl + d] = (uint8_t)encode(x, sc, mnv, a.kbits, is_narrow(a.kbits, sbase + jj));
+        const bool nar = a.kbits == 3 && r11 == 10;
+        codes[jj * Dl + d] = (uint8_t)encode_fast(x, sc, mnv, nar ? ws : sc, nar ? rcw : rc, nar ? 3 : q_max, a.kbits, nar);
+        if (++r11 == 11) r11 = 0;
       }
     }
     if (bh == 0 && threadIdx.x == 0) a.k_info[gglob] = make_int2((int)a.k_n, g * gs);
