@@ -15,7 +15,8 @@ e2e    = the same through the public API (DecodeStep: kvmix_append_attend_layers
 roofline = the dominant kernel (attend_mma_kernel, which also runs the 1-token append in
          its prologue): algorithmic bytes (MemoryReport total bits / 8 + q + out) per launch
          / launch time from CUDA events on the launch stream inside the timed steps, vs
-         MEASURED_PEAKS hbm_gbs. `step_frac` is the same over the whole step time.
+         MEASURED_PEAKS hbm_gbs. `step_frac` is the same over the whole step time (the
+         timed steps overlap consecutive layers' launches: programmatic dependent launch).
 cpu_baseline = the UNMODIFIED reference (oracle/_ref) timed on this host's cores on a
          bounded sample (one (layer, batch rows) unit per tier), extrapolated.
 Multi-GPU (--gpus N, or under torchrun): the global batch is sharded batch x kv-head with
@@ -257,21 +258,31 @@ def run_b200(args, rank, world, local_rank):
     cap = ctx + 2 * total_steps + 64
     torch.manual_seed(1234 + rank)
 
-    caches = []
-    for l in range(L):
-        c = K.KVLayerCache(cfg.layers[l], B, Hl, D, capacity_tokens=cap, tail_dtype=torch.float16)
-        plan.place(c)
-        k = torch.randn(B, Hl, pre, D, device=dev, dtype=torch.float16)
-        v = torch.randn(B, Hl, pre, D, device=dev, dtype=torch.float16)
-        c.append(k, v)
-        del k, v
-        caches.append(c)
-    # 64 decode appends to reach the steady-state window (trajectory table)
-    kd = torch.randn(64, B, Hl, 1, D, device=dev, dtype=torch.float16)
-    for s in range(64):
-        for c in caches:
-            c.append(kd[s], kd[(s + 1) % 64])
-    del kd
+    # workloads smaller than L2 rotate over R copies of the cache stack (R x bytes > 126 MB), so
+    # every timed step reads its cache from HBM (configs[0]: 12.7 MB per step)
+    est = L * B * Hl * ctx * D * 0.8
+    rot = 1 if est >= 0.25e9 else int(-(-0.3e9 // est))
+
+    def build_stack():
+        cs = []
+        for l in range(L):
+            c = K.KVLayerCache(cfg.layers[l], B, Hl, D, capacity_tokens=cap, tail_dtype=torch.float16)
+            plan.place(c)
+            k = torch.randn(B, Hl, pre, D, device=dev, dtype=torch.float16)
+            v = torch.randn(B, Hl, pre, D, device=dev, dtype=torch.float16)
+            c.append(k, v)
+            del k, v
+            cs.append(c)
+        # 64 decode appends to reach the steady-state window (trajectory table)
+        kd = torch.randn(64, B, Hl, 1, D, device=dev, dtype=torch.float16)
+        for s in range(64):
+            for c in cs:
+                c.append(kd[s], kd[(s + 1) % 64])
+        del kd
+        return cs
+
+    stacks = [build_stack() for _ in range(rot)]
+    caches = stacks[0]
     torch.cuda.synchronize()
 
     # per-step inputs resident in HBM
@@ -282,11 +293,12 @@ def run_b200(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     lib = _lib.lib()
-    steps = [K.DecodeStep(caches, list(kn[s]), list(vn[s]), list(qs[s]), list(outs)) for s in range(total_steps)]
+    steps = [K.DecodeStep(stacks[s % rot], list(kn[s]), list(vn[s]), list(qs[s]), list(outs))
+             for s in range(total_steps)]
 
     def step_instrumented(s, ev):
         # per layer append_attend with CUDA events around each launch (same kernels as step())
-        for l, c in enumerate(caches):
+        for l, c in enumerate(stacks[s % rot]):
             ev[l][0].record(stream)
             st = lib.kvmix_append_attend(c.handle, kn[s, l].data_ptr(), vn[s, l].data_ptr(), _lib.F16, 1,
                                          qs[s, l].data_ptr(), _lib.F16, Hql, 1, outs[l].data_ptr(), None, sp)
@@ -304,8 +316,10 @@ def run_b200(args, rank, world, local_rank):
         steps[s].step(sp)
     barrier()
     bytes_layer = [c.algorithmic_bytes() + B * Hql * D * (2 + 4) for c in caches]  # one attend launch each
-    # CUDA events around every layer's launch on the launch stream, on every 4th timed step
-    inst = list(range(0, args.steps, 4))
+    # CUDA events around every layer's launch on the launch stream, on every 10th timed step
+    # (those steps launch layer by layer, without the programmatic dependent launch that
+    # overlaps a layer's start with the previous layer's drain in DecodeStep.step())
+    inst = list(range(0, args.steps, 10))
     evs = {i: [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
            for i in inst}
     launches0 = _lib.launch_count()
@@ -341,7 +355,7 @@ def run_b200(args, rank, world, local_rank):
     # ---- --check: two sampled (layer, b, head) outputs of the last timed step ----
     check = None
     if not args.no_check:
-        check = check_outputs(caches, qs[total_steps - 1], outs, Hq // H, rank)
+        check = check_outputs(stacks[(total_steps - 1) % rot], qs[total_steps - 1], outs, Hq // H, rank)
 
     # ---- e2e through the public API with pinned host buffers ----
     # Every step copies that step's q/k/v from pinned host memory and reads every layer's
@@ -360,7 +374,8 @@ def run_b200(args, rank, world, local_rank):
         kb = [torch.empty_like(kn[0]) for _ in range(2)]
         vb = [torch.empty_like(vn[0]) for _ in range(2)]
         ob = [torch.empty_like(outs) for _ in range(2)]
-        dsteps = [K.DecodeStep(caches, list(kb[i]), list(vb[i]), list(qb[i]), list(ob[i])) for i in range(2)]
+        dsteps = [[K.DecodeStep(st, list(kb[i]), list(vb[i]), list(qb[i]), list(ob[i])) for st in stacks]
+                  for i in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
         done = [torch.cuda.Event() for _ in range(2)]
         drained = [torch.cuda.Event() for _ in range(2)]
@@ -384,7 +399,7 @@ def run_b200(args, rank, world, local_rank):
                     upload(s + 1, 1 - i)
                 stream.wait_event(ready[i])
                 stream.wait_event(drained[i])  # ob[i] of step s-2 has been read back
-                dsteps[i].step()
+                dsteps[i][s % rot].step()
                 done[i].record(stream)
                 with torch.cuda.stream(cp):
                     cp.wait_event(done[i])
@@ -427,8 +442,11 @@ def run_b200(args, rank, world, local_rank):
                    "parallelism": f"{plan.mode} shards x{world} (rank 0: b {plan.b0}-{plan.b1 - 1}, kv heads "
                                   f"{plan.h0}-{plan.h1 - 1}); no data-path collective",
                    "l2": (f"per-step cache bytes per GPU ({tot_bytes / 1e9:.2f} GB) >> 126 MB L2; no flush needed"
-                          if tot_bytes > 1e9 else f"per-step cache bytes {tot_bytes / 1e6:.0f} MB: partly L2-resident"),
-                   "timed_step": "per layer: append(1 token) + attend = kvmix_append_attend"},
+                          if rot == 1 else f"per-step cache bytes {tot_bytes / 1e6:.1f} MB < L2: steps rotate over "
+                                           f"{rot} copies of the cache stack ({rot * tot_bytes / 1e6:.0f} MB), every "
+                                           f"step reads its cache from HBM"),
+                   "timed_step": "DecodeStep.step(): per layer append(1 token) + attend (kvmix_append_attend_layers; "
+                                 "consecutive layers' launches overlap: programmatic dependent launch)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "attend_mma_kernel (IMMA; 1-token append in its prologue, split partials merged "

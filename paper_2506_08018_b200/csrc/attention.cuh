@@ -45,6 +45,7 @@ class Workspace {
   cudaStream_t st_;
   ScratchPool* pool_;
   size_t off_[2] = {0, 0};  // bump offsets into the arena / the zeroed buffer
+  int set_ = 0;             // scratch set of this call (alternates per stream)
   std::vector<void*> extra_;
   size_t bytes_ = 0;
 };

@@ -64,7 +64,8 @@ Knobs& knobs() {
     x.flush_blocks = iv("KVMIX_TEST_FLUSH_BLOCKS", 1, kFlushBlocks, kFlushBlocks);
     x.min_cost = iv("KVMIX_MIN_COST", 1, 1 << 20, kMinCost);
     x.ws = iv("KVMIX_WS", 0, 2, 1);
-    x.tc = iv("KVMIX_TC", 0, 1, 0);  // default off until it beats attend_mma_kernel end to end
+    x.tc = iv("KVMIX_TC", 0, 1, 0);
+    x.pdl = iv("KVMIX_PDL", 0, 1, 1);  // default off until it beats attend_mma_kernel end to end
     x.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
     x.no_window = getenv("KVMIX_PROF_NO_WINDOW") != nullptr;
     return x;
@@ -72,6 +73,16 @@ Knobs& knobs() {
   return k;
 }
 
+
+// One-shot request for a programmatic dependent launch of the next attention call on this
+// host thread (set by kvmix_*attend_layers for layers after the first).
+static thread_local bool g_pdl_next = false;
+void request_pdl(bool on) { g_pdl_next = on && knobs().pdl; }
+bool take_pdl() {
+  const bool r = g_pdl_next;
+  g_pdl_next = false;
+  return r;
+}
 
 // kvmix_set_knob (test / tuning hook): overrides one knob for later launches
 bool set_knob(const char* name, int v) {
@@ -83,6 +94,7 @@ bool set_knob(const char* name, int v) {
   else if (n == "KVMIX_MIN_COST") k.min_cost = std::max(1, v);
   else if (n == "KVMIX_WS") k.ws = std::max(0, std::min(2, v));
   else if (n == "KVMIX_TC") k.tc = std::max(0, std::min(1, v));
+  else if (n == "KVMIX_PDL") k.pdl = std::max(0, std::min(1, v));
   else return false;
   return true;
 }
@@ -200,6 +212,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
     int w0, w1;
     bh_warps(p, bh, w0, w1);
     if (wg < w0 || wg > w1) return;
+    pdl_gate(p);
     if (lane < prows) p.part_ml[(pbase + wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
     if (lane == 0 && p.want_cs) p.part_cs[pbase + wg + bh] = 0.0;
     if (arrive_last(p, bh, lane, pass, wg)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
@@ -932,6 +945,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
     }
 
     // ---- segment epilogue ----------------------------------------------------------------
+    pdl_gate(p);
     // A (b, kv-head) inside this warp's range is normalized and written directly; otherwise
     // the partial goes to slot wg + bh and the last of its warps to arrive merges them.
     const size_t slot = pbase + wg + bh;
@@ -1042,7 +1056,22 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.flags = p.fused ? ws.zeroed<unsigned>((size_t)p.npass * BH) : nullptr;
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
   const int64_t warps = (int64_t)p.W * p.npass;
-  kern<<<(unsigned)((warps + kMmaWarps - 1) / kMmaWarps), kMmaWarps * 32, smem, st>>>(p);
+  const unsigned grid = (unsigned)((warps + kMmaWarps - 1) / kMmaWarps);
+  if (p.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kMmaWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, p), "attend launch (PDL)");
+  } else {
+    kern<<<grid, kMmaWarps * 32, smem, st>>>(p);
+  }
   return p.W;
 }
 
@@ -1152,6 +1181,9 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     check_cuda(cudaStreamSynchronize(st), "sync");
     cs_total += part;
   }
+  // programmatic dependent launch: only when the caller (kvmix_*attend_layers) asked for it
+  // for this call, a single IMMA launch serves it and no checksum round trip follows
+  p.pdl = (take_pdl() && !use_tc && !checksum && npass_all <= chunk) ? 1 : 0;
   if (use_tc) {
     p.wonly = 1;
     p.ext_ml = ext.ml;
@@ -1182,6 +1214,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     // the warp-specialized kernel serves 3-bit Values (KVMIX_WS = 1, default) or every tier
     // (KVMIX_WS = 2); the single-warp kernel is ~5% faster on the 2/4-bit tiers (profiles/r2)
     if (!use_tc && (knobs().ws == 2 || (knobs().ws == 1 && vb == 3))) {
+      p.pdl = 0;
       W = attend_ws_launch(p, D, nrows, kb, vb, BH, ws, st);
       kname = "attend_ws_kernel";
     }

@@ -34,6 +34,7 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
 void dequantize(kvmix_grouping grouping, const uint32_t* words, const uint16_t* meta, int B, int H, int T, int D,
                 int bits, int gs, float* out, cudaStream_t st);
 bool set_knob(const char* name, int v);
+void request_pdl(bool on);
 void pack(const uint32_t* codes, size_t n, int bits, uint32_t* words, cudaStream_t st);
 void unpack(const uint32_t* words, size_t n, int bits, uint32_t* codes, cudaStream_t st);
 
@@ -413,8 +414,12 @@ kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const
     for (int l = 0; l < n_layers; ++l) {
       KVB_ON_CACHE_DEVICE(caches[l]);
       Workspace ws(as_stream(stream));
+      // layers after the first may overlap the previous layer's drain (different caches;
+      // every input was produced before this call)
+      request_pdl(l > 0 && caches[l] != caches[l - 1] && caches[l]->device == caches[l - 1]->device);
       attend(caches[l], q[l], dt, q_heads, t, out[l], nullptr, ws, as_stream(stream));
     }
+    request_pdl(false);
   });
 }
 
@@ -427,8 +432,10 @@ kvmix_status kvmix_append_attend_layers(kvmix_cache* const* caches, int n_layers
     for (int l = 0; l < n_layers; ++l) {
       KVB_ON_CACHE_DEVICE(caches[l]);
       Workspace ws(as_stream(stream));
+      request_pdl(l > 0 && caches[l] != caches[l - 1] && caches[l]->device == caches[l - 1]->device);
       append_attend(caches[l], k[l], v[l], kv_dt, t, q[l], q_dt, q_heads, tq, out[l], nullptr, ws, as_stream(stream));
     }
+    request_pdl(false);
   });
 }
 

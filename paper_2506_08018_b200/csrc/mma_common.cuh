@@ -187,9 +187,11 @@ struct Knobs {
   int tail_unit = kTailUnit, group_cost = kGroupCost, flush_blocks = kFlushBlocks, min_cost = kMinCost;
   int ws = 1;  // warp-specialized kernel (attention_ws.cu): 0 never, 1 for 3-bit Values, 2 always
   int tc = 0;  // tcgen05 kernel (attention_tc.cu) for the fast groups where it applies
+  int pdl = 1;  // programmatic dependent launch between the layers of kvmix_*attend_layers
   bool skip_tail = false, no_window = false;
 };
 Knobs& knobs();
+bool take_pdl();
 
 // Launch parameters shared by attend_mma_kernel and attend_ws_kernel.
 struct MmaParams {
@@ -236,6 +238,12 @@ struct MmaParams {
   float2* part_ml;  // partial slot of (warp w, bh) = w + bh (unique along the staircase)
   float* part_acc;
   double* part_cs;
+  // programmatic dependent launch (layer after layer inside kvmix_*attend_layers): the launch
+  // may start while the previous layer's kernel drains; every warp waits for it to complete
+  // (griddepcontrol.wait) before its first result / scratch write and only then lets the
+  // next launch start (launch_dependents), so at most two launches are in flight and the
+  // scratch sets they use alternate (Workspace)
+  int pdl;
   // window-only launch (after attend_tc_kernel served the fast groups): warp = (pass, b,
   // kv-head), its window units only; the fast-group partials of attend_tc_kernel (slot c + bh
   // for the CTAs c whose tile ranges hold bh's tiles) are merged into the output here
@@ -263,6 +271,13 @@ bool attend_tc_launch(const kvmix_cache* c, const void* q, bool q16, int Hq, int
 bool attend_tc_eligible(const kvmix_cache* c, int rows);
 
 namespace {
+
+__device__ __forceinline__ void pdl_gate(const MmaParams& p) {
+  if (p.pdl) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  }
+}
 
 // first unit whose start cost is >= c (units: Gf groups of cost Qc, then window units of 1)
 __device__ __forceinline__ int unit_at_cost(const MmaParams& p, int64_t c) {

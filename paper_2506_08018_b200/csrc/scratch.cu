@@ -9,11 +9,15 @@
 
 namespace kvb {
 
+// Two scratch sets used alternately by consecutive calls on a stream: a layer's attention
+// launch may overlap the previous layer's (programmatic dependent launch, attention_mma.cu),
+// never the one before it, so neighbours never share scratch.
 struct ScratchPool {
   std::mutex mu;          // held by the Workspace of the call in flight on this stream
-  void* buf[2] = {nullptr, nullptr};  // arena (uninitialised) / zeroed counters
-  size_t have[2] = {0, 0};
-  size_t want[2] = {0, 0};            // high-water marks seen
+  void* buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [set][arena (uninitialised) / zeroed counters]
+  size_t have[2][2] = {{0, 0}, {0, 0}};
+  size_t want[2] = {0, 0};            // high-water marks seen (both sets grow to them)
+  int parity = 0;                     // set of the next call
   int device = 0;
 };
 
@@ -63,6 +67,8 @@ Workspace::Workspace(cudaStream_t st) : st_(st) {
     pool_ = p.get();
   }
   pool_->mu.lock();
+  set_ = pool_->parity;
+  pool_->parity ^= 1;
   try {
     grow();
   } catch (...) {
@@ -75,16 +81,17 @@ Workspace::Workspace(cudaStream_t st) : st_(st) {
 // stays on stream-ordered allocations)
 void Workspace::grow() {
   cudaStream_t st = st_;
+  const int k = set_;
   for (int z = 0; z < 2; ++z) {
-    if (pool_->want[z] <= pool_->have[z] || capturing(st)) continue;
+    if (pool_->want[z] <= pool_->have[k][z] || capturing(st)) continue;
     check_cuda(cudaStreamSynchronize(st), "sync(scratch growth)");  // old buffer no longer in use
-    if (pool_->buf[z]) check_cuda(cudaFree(pool_->buf[z]), "cudaFree(scratch)");
-    pool_->buf[z] = nullptr;
-    pool_->have[z] = 0;
+    if (pool_->buf[k][z]) check_cuda(cudaFree(pool_->buf[k][z]), "cudaFree(scratch)");
+    pool_->buf[k][z] = nullptr;
+    pool_->have[k][z] = 0;
     const size_t n = (pool_->want[z] + (pool_->want[z] >> 2) + kAlign - 1) / kAlign * kAlign;
-    check_cuda(cudaMalloc(&pool_->buf[z], n), "cudaMalloc(scratch)");
-    if (z == 1) check_cuda(cudaMemset(pool_->buf[z], 0, n), "cudaMemset(scratch)");
-    pool_->have[z] = n;
+    check_cuda(cudaMalloc(&pool_->buf[k][z], n), "cudaMalloc(scratch)");
+    if (z == 1) check_cuda(cudaMemset(pool_->buf[k][z], 0, n), "cudaMemset(scratch)");
+    pool_->have[k][z] = n;
   }
 }
 
@@ -96,7 +103,7 @@ void* Workspace::take(size_t bytes, bool zero) {
   const size_t off = off_[z];
   off_[z] += bytes;
   if (off_[z] > pool_->want[z]) pool_->want[z] = off_[z];
-  if (off_[z] <= pool_->have[z]) return static_cast<char*>(pool_->buf[z]) + off;
+  if (off_[z] <= pool_->have[set_][z]) return static_cast<char*>(pool_->buf[set_][z]) + off;
   keep_pool(pool_->device);
   void* p = nullptr;
   check_cuda(cudaMallocAsync(&p, bytes, st_), "cudaMallocAsync(scratch)");
