@@ -282,6 +282,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
     }
   };
   for (int s = 0; s < S; ++s) issue_next(s);
+  // (PDL: the gate -- wait for the previous layer's launch, then let the next one start -- sits
+  // before the warp's first result write; gating right here, after the ring fill, measured
+  // slower: 3.41 vs 3.26 ms per configs[1] step, the early warps stall on the previous layer)
 
   // fused 1-token append: the warp whose range holds a (b, kv-head)'s first window unit
   // appends its token (only the window path reads what the append writes), then publishes
