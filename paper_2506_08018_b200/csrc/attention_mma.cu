@@ -49,6 +49,9 @@
 // warps to publish a partial (tagged atomic counter) -- no separate combine launch.
 #include "mma_common.cuh"
 
+#include <cstdio>
+#include <vector>
+
 namespace kvb {
 
 // Tuning / test knobs, read from the environment once per process.
@@ -148,6 +151,10 @@ __device__ __forceinline__ void ext_merge_write(const MmaParams& p, int bh, int 
 }
 
 // GS: 0 = runtime group size (a multiple of 32), else compile-time (32 is the KVmix default).
+#ifdef KVB_TRACE
+__device__ uint64_t* g_trace = nullptr;  // debug builds: per-warp timeline (KVMIX_TRACE_FILE)
+#endif
+
 template <int D, int KB, int VB, int R, int GS>
 __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mma_kernel(MmaParams p) {
   static_assert(D == 64 || D == 128, "IMMA attention handles D in {64, 128}");
@@ -175,6 +182,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warps are independent (no CTA barriers); npass adjacent warps share a unit range
   const int gw = blockIdx.x * kMmaWarps + warp;
+#ifdef KVB_TRACE
+  uint64_t tr_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
+#endif
   const int pass = gw % p.npass, wg = gw / p.npass;
   if (wg >= p.W) return;
   const int prow0 = p.row0 + pass * p.rows;                // this pass's query rows
@@ -990,6 +1001,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
     }
     __syncwarp();  // s_acc is rewritten by the next segment
   }
+#ifdef KVB_TRACE
+  if (lane == 0 && g_trace) {  // (start, end, SM, unit range) per warp
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_trace[4 * gw] = tr_start;
+    g_trace[4 * gw + 1] = t1;
+    g_trace[4 * gw + 2] = sm;
+    g_trace[4 * gw + 3] = ((uint64_t)u_beg << 32) | (uint32_t)u_end;
+  }
+#endif
 }
 
 template <int D, int KB, int VB, int R, int GS>
@@ -1073,7 +1096,33 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, kern, p), "attend launch (PDL)");
   } else {
+#ifdef KVB_TRACE
+    static uint64_t* tbuf = nullptr;
+    static size_t tcap = 0;
+    const size_t need = (size_t)grid * kMmaWarps * 4;
+    if (getenv("KVMIX_TRACE_FILE")) {
+      if (need > tcap) {
+        if (tbuf) cudaFree(tbuf);
+        check_cuda(cudaMalloc(&tbuf, need * 8), "trace");
+        tcap = need;
+      }
+      check_cuda(cudaMemset(tbuf, 0, need * 8), "trace");
+      check_cuda(cudaMemcpyToSymbol(g_trace, &tbuf, sizeof(tbuf)), "trace symbol");
+    }
+#endif
     kern<<<grid, kMmaWarps * 32, smem, st>>>(p);
+#ifdef KVB_TRACE
+    if (getenv("KVMIX_TRACE_FILE")) {  // (debug builds) append this launch's timeline
+      std::vector<uint64_t> h(need);
+      check_cuda(cudaMemcpy(h.data(), tbuf, need * 8, cudaMemcpyDeviceToHost), "trace copy");
+      if (FILE* fp = fopen(getenv("KVMIX_TRACE_FILE"), "ab")) {
+        const uint64_t hdr[4] = {0x5452414345ull, need / 4, (uint64_t)p.U, (uint64_t)p.Gf};
+        fwrite(hdr, 8, 4, fp);
+        fwrite(h.data(), 8, need, fp);
+        fclose(fp);
+      }
+    }
+#endif
   }
   return p.W;
 }
