@@ -296,15 +296,17 @@ def run_b200(args, rank, world, local_rank):
     steps = [K.DecodeStep(stacks[s % rot], list(kn[s]), list(vn[s]), list(qs[s]), list(outs))
              for s in range(total_steps)]
 
+    # layer runs with one kernel instance each (the KVmix tiers): kvmix_append_attend_layers
+    # launches each run as ONE multi-layer kernel; instrumented steps call it per run with CUDA
+    # events around each call (the same kernels as step(), without the overlap between runs)
+    runs = [(0, high), (high, L)] if 0 < high < L else [(0, L)]
+    inst_steps = {}
+
     def step_instrumented(s, ev):
-        # per layer append_attend with CUDA events around each launch (same kernels as step())
-        for l, c in enumerate(stacks[s % rot]):
-            ev[l][0].record(stream)
-            st = lib.kvmix_append_attend(c.handle, kn[s, l].data_ptr(), vn[s, l].data_ptr(), _lib.F16, 1,
-                                         qs[s, l].data_ptr(), _lib.F16, Hql, 1, outs[l].data_ptr(), None, sp)
-            if st:
-                _lib.check(st)
-            ev[l][1].record(stream)
+        for j, ds in enumerate(inst_steps[s]):
+            ev[j][0].record(stream)
+            ds.step(sp)
+            ev[j][1].record(stream)
 
     def barrier():
         torch.cuda.synchronize()
@@ -320,8 +322,12 @@ def run_b200(args, rank, world, local_rank):
     # (those steps launch layer by layer, without the programmatic dependent launch that
     # overlaps a layer's start with the previous layer's drain in DecodeStep.step())
     inst = list(range(0, args.steps, 10))
-    evs = {i: [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
+    evs = {i: [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in runs]
            for i in inst}
+    for i in inst:  # (built before the timed region)
+        s = args.warmup + i
+        inst_steps[s] = [K.DecodeStep(stacks[s % rot][a:b], list(kn[s][a:b]), list(vn[s][a:b]),
+                                      list(qs[s][a:b]), list(outs[a:b])) for a, b in runs]
     launches0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local_rank) as clk:
@@ -336,7 +342,7 @@ def run_b200(args, rank, world, local_rank):
         end.synchronize()
     launches = _lib.launch_count() - launches0
     elapsed = start.elapsed_time(end)  # ms for K steps
-    attn_ms = [statistics.mean(evs[i][l][0].elapsed_time(evs[i][l][1]) for i in inst) for l in range(L)]
+    attn_ms = [statistics.mean(evs[i][j][0].elapsed_time(evs[i][j][1]) for i in inst) for j in range(len(runs))]
     elapsed = reduce_max(elapsed, world, dev)
     ms_per_step = elapsed / args.steps
     value = B_glob * args.steps / (elapsed / 1e3)
@@ -445,12 +451,13 @@ def run_b200(args, rank, world, local_rank):
                           if rot == 1 else f"per-step cache bytes {tot_bytes / 1e6:.1f} MB < L2: steps rotate over "
                                            f"{rot} copies of the cache stack ({rot * tot_bytes / 1e6:.0f} MB), every "
                                            f"step reads its cache from HBM"),
-                   "timed_step": "DecodeStep.step(): per layer append(1 token) + attend (kvmix_append_attend_layers; "
-                                 "consecutive layers' launches overlap: programmatic dependent launch)"},
+                   "timed_step": "DecodeStep.step(): per layer append(1 token) + attend (kvmix_append_attend_layers: "
+                                 "one multi-layer launch per tier run, the second overlapping the first's drain "
+                                 "(programmatic dependent launch))"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "attend_mma_kernel (IMMA; 1-token append in its prologue, split partials merged "
-                               "in-kernel), one launch per layer",
+                     "kernel": "attend_mma_layers_kernel (IMMA; 1-token append in its prologue, split partials "
+                               "merged in-kernel), one launch per run of same-tier layers",
                      "step_frac": tot_bytes / (ms_per_step / 1e3) / 1e9 / peak,
                      "traffic_unit": "DRAM bytes per step (profiles/ncu_traffic.json, 1 GPU)",
                      "algorithmic_bytes_per_step": tot_bytes, "attend_ms_per_step": tot_ms,

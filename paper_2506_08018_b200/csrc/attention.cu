@@ -272,7 +272,7 @@ int attend_splits(int BH) {
   return std::max(1, std::min(64, (4 * sms + BH - 1) / std::max(1, BH)));
 }
 
-static void check_query_shape(const kvmix_cache* c, int q_heads, int t) {
+void check_query_shape(const kvmix_cache* c, int q_heads, int t) {
   if (t < 1) invalid("attention: need at least one query row");
   if (q_heads < c->H || q_heads % c->H != 0) invalid("attention: query shape does not match cache");
 }

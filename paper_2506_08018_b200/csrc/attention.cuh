@@ -54,6 +54,7 @@ class Workspace {
 void scratch_add(size_t bytes);
 
 void check_attend(const kvmix_cache* c, int q_heads, int t);
+void check_query_shape(const kvmix_cache* c, int q_heads, int t);
 // split count used by every attention path: ~4 CTAs per SM, independent of T
 int attend_splits(int BH);
 void attend_generic(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
@@ -62,6 +63,11 @@ void attend(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq,
             Workspace& ws, cudaStream_t st);
 void append_attend(kvmix_cache* c, const void* k, const void* v, kvmix_dtype kv_dt, int t, const void* q,
                    kvmix_dtype q_dt, int Hq, int tq, float* out, double* checksum, Workspace& ws, cudaStream_t st);
+// kvmix_*attend_layers on one device with distinct caches (k == nullptr: attention only):
+// the layers the IMMA kernel serves share one launch per kernel instance
+void attend_layers(kvmix_cache* const* caches, int n, const void* const* k, const void* const* v,
+                   kvmix_dtype kv_dt, int t, const void* const* q, kvmix_dtype q_dt, int Hq, int tq,
+                   float* const* out, cudaStream_t st);
 void fused_qk_scores(const kvmix_cache* c, const void* q, kvmix_dtype dt, int tq, float* scores, cudaStream_t st);
 void softmax_rows(float* x, int64_t rows, int64_t cols, cudaStream_t st);
 void fused_pv(const kvmix_cache* c, const float* probs, int tq, float* out, cudaStream_t st);

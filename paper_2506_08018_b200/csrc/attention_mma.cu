@@ -53,6 +53,7 @@
 #include <vector>
 
 namespace kvb {
+int attend_ws_launch(MmaParams& p, int D, int rows, int kb, int vb, int BH, Workspace& ws, cudaStream_t st);
 
 // Tuning / test knobs, read from the environment once per process.
 Knobs& knobs() {
@@ -68,7 +69,8 @@ Knobs& knobs() {
     x.min_cost = iv("KVMIX_MIN_COST", 1, 1 << 20, kMinCost);
     x.ws = iv("KVMIX_WS", 0, 2, 1);
     x.tc = iv("KVMIX_TC", 0, 1, 0);
-    x.pdl = iv("KVMIX_PDL", 0, 1, 1);  // default off until it beats attend_mma_kernel end to end
+    x.pdl = iv("KVMIX_PDL", 0, 1, 1);
+    x.layers = iv("KVMIX_LAYERS", 0, 1, 1);
     x.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
     x.no_window = getenv("KVMIX_PROF_NO_WINDOW") != nullptr;
     return x;
@@ -98,6 +100,7 @@ bool set_knob(const char* name, int v) {
   else if (n == "KVMIX_WS") k.ws = std::max(0, std::min(2, v));
   else if (n == "KVMIX_TC") k.tc = std::max(0, std::min(1, v));
   else if (n == "KVMIX_PDL") k.pdl = std::max(0, std::min(1, v));
+  else if (n == "KVMIX_LAYERS") k.layers = std::max(0, std::min(1, v));
   else return false;
   return true;
 }
@@ -155,8 +158,9 @@ __device__ __forceinline__ void ext_merge_write(const MmaParams& p, int bh, int 
 __device__ uint64_t* g_trace = nullptr;  // debug builds: per-warp timeline (KVMIX_TRACE_FILE)
 #endif
 
+// The kernel body: warp gw (of the layer whose parameters p are) runs its unit range.
 template <int D, int KB, int VB, int R, int GS>
-__global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mma_kernel(MmaParams p) {
+__device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw) {
   static_assert(D == 64 || D == 128, "IMMA attention handles D in {64, 128}");
   static_assert(VB == 2 || VB == 4, "Values: 2 or 4 bits");
   static_assert(R == 1 || R == 2, "one or two query rows per KV head");
@@ -181,7 +185,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warps are independent (no CTA barriers); npass adjacent warps share a unit range
-  const int gw = blockIdx.x * kMmaWarps + warp;
 #ifdef KVB_TRACE
   uint64_t tr_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
@@ -1016,9 +1019,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mm
 }
 
 template <int D, int KB, int VB, int R, int GS>
-int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
+__global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mma_kernel(MmaParams p) {
+  attend_mma_body<D, KB, VB, R, GS>(p, blockIdx.x * kMmaWarps + (threadIdx.x >> 5));
+}
+
+// Several layers of a decode step in one launch: warps [off[l], off[l+1]) run layer l with
+// its own parameters, scratch and unit ranges (each layer exactly as its own launch would,
+// with fewer warps), so the launch ramp and drain are paid once per step instead of once
+// per layer. The parameter block lives in the kernel's constant bank (__grid_constant__:
+// the layer's fields are read in place, not copied).
+template <int D, int KB, int VB, int R, int GS>
+__global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R))
+    attend_mma_layers_kernel(const __grid_constant__ MmaLayers mp) {
+  const int gw = blockIdx.x * kMmaWarps + (threadIdx.x >> 5);
+  int li = 0;
+  while (li + 1 < mp.n && gw >= mp.off[li + 1]) ++li;
+  if (gw >= mp.off[li + 1]) return;
+  attend_mma_body<D, KB, VB, R, GS>(mp.l[li], gw - mp.off[li]);
+}
+
+// Ring depth, dynamic shared memory and the resident wave (warps) of kernel `kern`.
+template <int D, int KB, int VB, int R, int GS, typename Kern>
+void mma_geometry(Kern kern, uint32_t stage_bytes, int& stages_out, size_t& smem, int64_t& wave) {
   using WL = WarpLayout<D, KB, R>;
-  auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
   // ring depth: as many stages (2..4) as fit while keeping the highest CTA residency
   // the registers allow (4, else 3, else 2 CTAs per SM)
   static thread_local int static_smem = -1;
@@ -1032,7 +1055,7 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   for (int occ_target = KVB_MIN_CTAS(KB, R); occ_target >= 1; occ_target = occ_target * 3 / 4) {
     const long per_cta = 227L * 1024 / occ_target - 1024 - static_smem;
     const long per_warp = per_cta / kMmaWarps - (long)fixed - 4 * 8 - 128;
-    const long s_fit = per_warp / (long)p.stage_bytes;
+    const long s_fit = per_warp / (long)stage_bytes;
     if (s_fit >= 2) {
       stages = (int)std::min<long>(4, s_fit);
       break;
@@ -1041,11 +1064,11 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   if constexpr (GS != 0) {
     using SG = StageGeo<D, KB, VB, R, GS>;
     static_assert(SG::kStages >= 2, "stage geometry");
-    if (p.stage_bytes != SG::kStage) throw Error(KVMIX_RUNTIME_ERROR, "attend: record geometry mismatch");
+    if (stage_bytes != SG::kStage) throw Error(KVMIX_RUNTIME_ERROR, "attend: record geometry mismatch");
     stages = SG::kStages;
   }
-  p.stages = stages;
-  const size_t smem = (size_t)kMmaWarps * WL::bytes(p.stages, p.stage_bytes);
+  stages_out = stages;
+  smem = (size_t)kMmaWarps * WL::bytes(stages, stage_bytes);
   // per device: the dynamic shared memory attribute and the residency at this ring size are
   // set / queried once (host cost per call is a few table lookups)
   int dev = 0;
@@ -1059,19 +1082,13 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
     occ_smem = smem;
     occ_dev = dev;
   }
-  // one resident wave of independent warps (persistent): equal unit ranges, no stragglers;
-  // never more warps than units so every range is non-empty
-  // (the npass warps of a unit range count once per pass)
-  const int64_t wave = (int64_t)std::max(1, occ) * num_sms() * kMmaWarps;
-  // small problems: at least kMinCost cost units per warp (a warp's prologue and the merge
-  // of a head split over many warps cost more than a few groups)
-  const int64_t min_cost = knobs().min_cost;
-  const int64_t w_cap = std::max<int64_t>(1, p.Nc / min_cost);
-  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(p.N, wave / p.npass), w_cap));
-  if (p.wonly) p.W = BH;  // one warp per (pass, b, kv-head)
-  // partial slots x * pslots + w + bh (w + bh < W + BH): scratch depends on (B, H, rows, D,
-  // SM count) only
-  p.pslots = (int)(std::max<int64_t>(wave, p.W) + BH);
+  // one resident wave of independent warps (persistent): equal unit ranges, no stragglers
+  wave = (int64_t)std::max(1, occ) * num_sms() * kMmaWarps;
+}
+
+// Partial slots, merge counters and append flags of one layer's launch parameters.
+template <int D>
+void mma_scratch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.nbh = BH;
   const size_t slots = (size_t)p.npass * p.pslots;
   p.part_ml = ws.ml(st, slots * p.rows);
@@ -1081,20 +1098,43 @@ int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
   p.cnt8 = ws.zeroed<unsigned>(slots);
   p.flags = p.fused ? ws.zeroed<unsigned>((size_t)p.npass * BH) : nullptr;
   if (p.want_cs) check_cuda(cudaMemsetAsync(p.part_cs, 0, (slots + 1) * sizeof(double), st), "memset");
+}
+
+template <typename Kern, typename Arg>
+void launch_ex(Kern kern, unsigned grid, size_t smem, cudaStream_t st, bool pdl, const Arg& arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kMmaWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  check_cuda(cudaLaunchKernelEx(&cfg, kern, arg), pdl ? "attend launch (PDL)" : "attend launch");
+}
+
+template <int D, int KB, int VB, int R, int GS>
+int launch(MmaParams& p, int BH, Workspace& ws, cudaStream_t st) {
+  auto kern = attend_mma_kernel<D, KB, VB, R, GS>;
+  size_t smem = 0;
+  int64_t wave = 0;
+  mma_geometry<D, KB, VB, R, GS>(kern, p.stage_bytes, p.stages, smem, wave);
+  // small problems: at least kMinCost cost units per warp (a warp's prologue and the merge
+  // of a head split over many warps cost more than a few groups)
+  const int64_t min_cost = knobs().min_cost;
+  const int64_t w_cap = std::max<int64_t>(1, p.Nc / min_cost);
+  p.W = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(p.N, wave / p.npass), w_cap));
+  if (p.wonly) p.W = BH;  // one warp per (pass, b, kv-head)
+  // partial slots x * pslots + w + bh (w + bh < W + BH): scratch depends on (B, H, rows, D,
+  // SM count) only
+  p.pslots = (int)(std::max<int64_t>(wave, p.W) + BH);
+  mma_scratch<D>(p, BH, ws, st);
   const int64_t warps = (int64_t)p.W * p.npass;
   const unsigned grid = (unsigned)((warps + kMmaWarps - 1) / kMmaWarps);
   if (p.pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kMmaWarps * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, p), "attend launch (PDL)");
+    launch_ex(kern, grid, smem, st, true, p);
   } else {
 #ifdef KVB_TRACE
     static uint64_t* tbuf = nullptr;
@@ -1149,12 +1189,84 @@ int dispatch_bits(MmaParams& p, int kb, int vb, int BH, Workspace& ws, cudaStrea
   }
 }
 
-}  // namespace
 
-int attend_ws_launch(MmaParams& p, int D, int rows, int kb, int vb, int BH, Workspace& ws, cudaStream_t st);
 
-bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
-                Workspace& ws, cudaStream_t st, const DecodeAppend* da) {
+// One launch for the layers L[0, n) (all on this kernel instance): the resident wave is
+// shared among the layers in proportion to their cost, each layer keeps its own unit
+// ranges, partial slots, counters and merges.
+template <int D, int KB, int VB, int R, int GS>
+void launch_layers(MmaParams* L, const int* BHs, int n, Workspace& ws, cudaStream_t st, bool pdl) {
+  auto kern = attend_mma_layers_kernel<D, KB, VB, R, GS>;
+  size_t smem = 0;
+  int64_t wave = 0;
+  int stages = 0;
+  mma_geometry<D, KB, VB, R, GS>(kern, L[0].stage_bytes, stages, smem, wave);
+  double tot = 0.0;
+  for (int l = 0; l < n; ++l) tot += (double)L[l].Nc * L[l].npass;
+  thread_local MmaLayers mp;  // (host staging; the launch copies it)
+  mp.n = n;
+  int64_t off = 0;
+  const int64_t min_cost = knobs().min_cost;
+  for (int l = 0; l < n; ++l) {
+    MmaParams& p = L[l];
+    p.stages = stages;
+    const double share = tot > 0.0 ? (double)wave * (double)p.Nc * p.npass / tot : 1.0;
+    const int64_t w_cap = std::max<int64_t>(1, std::min<int64_t>(p.N, p.Nc / min_cost));
+    p.W = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)(share / p.npass), w_cap));
+    // partial slots: as the single-layer launch (a wave + BH), so scratch does not depend on T
+    p.pslots = (int)(std::max<int64_t>(wave, p.W) + BHs[l]);
+    p.pdl = 1;  // the gate also lets the next launch start early (griddepcontrol.wait is a
+                // no-op in a launch without the PDL attribute)
+    mma_scratch<D>(p, BHs[l], ws, st);
+    mp.off[l] = (int)off;
+    mp.l[l] = p;
+    off += (int64_t)p.W * p.npass;
+  }
+  mp.off[n] = (int)off;
+  const unsigned grid = (unsigned)((off + kMmaWarps - 1) / kMmaWarps);
+  launch_ex(kern, grid, smem, st, pdl, mp);
+}
+
+template <int D, int R>
+bool dispatch_layers(MmaParams* L, const int* BHs, int n, int kb, int vb, Workspace& ws, cudaStream_t st, bool pdl) {
+  switch (kb * 10 + vb) {
+    case 22: launch_layers<D, 2, 2, R, 32>(L, BHs, n, ws, st, pdl); return true;
+    case 24: launch_layers<D, 2, 4, R, 32>(L, BHs, n, ws, st, pdl); return true;
+    case 42: launch_layers<D, 4, 2, R, 32>(L, BHs, n, ws, st, pdl); return true;
+    case 44: launch_layers<D, 4, 4, R, 32>(L, BHs, n, ws, st, pdl); return true;
+    case 32:
+    case 34:
+      if constexpr (D == 128) {
+        if (vb == 2) launch_layers<D, 3, 2, R, 32>(L, BHs, n, ws, st, pdl);
+        else launch_layers<D, 3, 4, R, 32>(L, BHs, n, ws, st, pdl);
+        return true;
+      }
+      return false;
+    default: return false;
+  }
+}
+
+// unit list of a pass: window blocks only with one query row; returns units per (b, kv-head)
+int64_t mma_layout(MmaParams& p, const kvmix_cache* c, int nrows) {
+  const int64_t T = p.T;
+  p.Pw = p.P;
+  p.nwb = 0;
+  if (nrows == 1 && c->k.quantized == p.P && !knobs().no_window) {
+    p.Pw = std::min(T, c->v.quantized);
+    if (p.Pw > p.P) p.nwb = (int)((p.Pw - p.P + 31) / 32);
+    else p.Pw = p.P;
+  }
+  return (int64_t)p.Gf + p.nwb + (T - p.Pw + p.tail_unit - 1) / p.tail_unit;
+}
+
+struct MmaGeo {
+  int per_pass, npass_all, chunk, rows, kb, vb, D, BH;
+};
+
+// The layer fields of the launch parameters (everything but the pass split, the warp
+// count and the scratch); false when the IMMA kernels do not serve this call.
+bool mma_setup(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, bool want_cs,
+               const DecodeAppend* da, MmaParams& p, MmaGeo& g) {
   const int rows = (Hq / c->H) * tq;
   const int kb = c->k.bits, vb = c->v.bits;
   if (vb == 3 && !knobs().ws) return false;  // 3-bit Values: the warp-specialized kernel only
@@ -1170,7 +1282,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   const int chunk = std::min(npass_all, kMaxPasses);
   const int BH = c->B * c->H;
   const int64_t T = c->total();
-  MmaParams p{};
+  p = MmaParams{};
   p.k = view(c->k);
   p.v = view(c->v);
   p.q = q;
@@ -1195,7 +1307,7 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   p.Grec = (int)(c->k.bh_stride / c->k.grp_stride);
   if (p.vm_bytes % 16) return false;
   p.inv = 1.0f / sqrtf((float)D);
-  p.want_cs = checksum != nullptr;
+  p.want_cs = want_cs;
   p.out = out;
   const Knobs kn = knobs();
   p.tail_unit = kn.tail_unit;
@@ -1206,22 +1318,50 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
     if (da->v_age && da->v_j < p.P) return false;
     if (T <= p.P) return false;  // (cannot happen after an append: the new Key is in the window)
   }
-  // unit lists of the passes: window blocks only with one query row
-  auto layout = [&](int nrows) {
-    p.Pw = p.P;
-    p.nwb = 0;
-    if (nrows == 1 && c->k.quantized == p.P && !kn.no_window) {
-      p.Pw = std::min(T, c->v.quantized);
-      if (p.Pw > p.P) p.nwb = (int)((p.Pw - p.P + 31) / 32);
-      else p.Pw = p.P;
-    }
-    return (int64_t)p.Gf + p.nwb + (T - p.Pw + p.tail_unit - 1) / p.tail_unit;
-  };
-  if ((int64_t)BH * layout(per_pass) >= (int64_t)1 << 31) return false;
+  if ((int64_t)BH * mma_layout(p, c, per_pass) >= (int64_t)1 << 31) return false;
+  g.per_pass = per_pass;
+  g.npass_all = npass_all;
+  g.chunk = chunk;
+  g.rows = rows;
+  g.kb = kb;
+  g.vb = vb;
+  g.D = D;
+  g.BH = BH;
+  return true;
 
+}
+
+// the pass fields of launch x0 (row passes [x0, x0 + chunk))
+void mma_pass(MmaParams& p, const kvmix_cache* c, const MmaGeo& g, int x0, const DecodeAppend* da) {
+  const int r0 = x0 * g.per_pass;
+  p.row0 = r0;
+  p.rows = g.per_pass;  // rows per pass (the last pass of a launch may hold fewer)
+  p.npass = std::min(g.chunk, g.npass_all - x0);
+  p.rows_all = std::min(g.rows - r0, p.npass * g.per_pass);
+  p.U = (int)mma_layout(p, c, g.per_pass);
+  p.N = g.BH * p.U;
+  p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
+  p.Nc = (int64_t)g.BH * p.cost_bh;
+  p.fused = 0;
+  if (da && r0 == 0) {  // the first launch runs the append; later launches follow in stream order
+    p.fused = 1;
+    p.da = *da;
+  }
+}
+
+}  // namespace
+
+bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int tq, float* out, double* checksum,
+                Workspace& ws, cudaStream_t st, const DecodeAppend* da) {
+  MmaParams p;
+  MmaGeo g;
+  if (!mma_setup(c, q, dt, Hq, tq, out, checksum != nullptr, da, p, g)) return false;
+  const int per_pass = g.per_pass, npass_all = g.npass_all, chunk = g.chunk, rows = g.rows;
+  const int kb = g.kb, vb = g.vb, D = g.D, BH = g.BH;
   // tcgen05 kernel over the fast groups (all query rows in one pass), then ONE window launch
   // (warp per (pass, b, kv-head)) that runs the fused append and the window and merges
   TcExt ext;
+  (void)rows;
   const bool use_tc = npass_all <= kMaxPasses && p.Gf > 0 && attend_tc_eligible(c, rows) &&
                       attend_tc_launch(c, q, dt == KVMIX_F16, Hq, tq, p.Gf, checksum != nullptr, ws, st, &ext);
   double cs_total = 0.0;
@@ -1247,20 +1387,8 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   }
   for (int x0 = 0; x0 < npass_all; x0 += chunk) {
     const int r0 = x0 * per_pass;
-    const int nrows = per_pass;  // rows per pass (the last pass of a launch may hold fewer)
-    p.row0 = r0;
-    p.rows = nrows;
-    p.npass = std::min(chunk, npass_all - x0);
-    p.rows_all = std::min(rows - r0, p.npass * per_pass);
-    p.U = (int)layout(nrows);
-    p.N = BH * p.U;
-    p.cost_bh = (int64_t)p.Qc * p.Gf + (p.U - p.Gf);
-    p.Nc = (int64_t)BH * p.cost_bh;
-    p.fused = 0;
-    if (da && r0 == 0) {  // the first launch runs the append; later launches follow in stream order
-      p.fused = 1;
-      p.da = *da;
-    }
+    const int nrows = per_pass;
+    mma_pass(p, c, g, x0, da);
     int W = 0;
     const char* kname = "attend_mma_kernel";
     // the warp-specialized kernel serves 3-bit Values (KVMIX_WS = 1, default) or every tier
@@ -1300,4 +1428,82 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
   return true;
 }
 
+// The layers of one decode step (kvmix_*attend_layers; distinct caches on the current
+// device; k == nullptr: attention only). Every layer the single IMMA launch serves is
+// queued with its decode append and launched together with the other layers of the same
+// kernel instance (KVmix tiers: two launches per step); the rest run alone, in order.
+// Layers are independent, so only each layer's own order (append, then attention) matters.
+void attend_layers(kvmix_cache* const* caches, int n, const void* const* k, const void* const* v,
+                   kvmix_dtype kv_dt, int t, const void* const* q, kvmix_dtype q_dt, int Hq, int tq,
+                   float* const* out, cudaStream_t st) {
+  struct Group {
+    int D, kb, vb, R;
+    std::vector<MmaParams> p;
+    std::vector<int> bh;
+  };
+  std::vector<Group> groups;
+  int launched = 0;
+  auto flush = [&](Group& g) {
+    if (g.p.empty()) return;
+    Workspace ws(st);
+    const bool pdl = launched > 0 && knobs().pdl;  // after the call's first launch
+    const int n = (int)g.p.size();
+    bool ok = false;
+    if (g.D == 64) ok = g.R == 1 ? dispatch_layers<64, 1>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
+                                 : dispatch_layers<64, 2>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl);
+    else ok = g.R == 1 ? dispatch_layers<128, 1>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
+                       : dispatch_layers<128, 2>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl);
+    if (!ok) throw Error(KVMIX_RUNTIME_ERROR, "attend: multi-layer launch unavailable");
+    after_launch("attend_mma_layers_kernel");
+    ++launched;
+    g.p.clear();
+    g.bh.clear();
+  };
+  auto try_add = [&](const kvmix_cache* c, const void* ql, float* o, const DecodeAppend* da) {
+    const Knobs& kn = knobs();
+    if (kn.tc || !kn.layers || c->cfg.group_size != 32) return false;
+    MmaParams p;
+    MmaGeo g;
+    if (!mma_setup(c, ql, q_dt, Hq, tq, o, false, da, p, g)) return false;
+    if (g.npass_all > g.chunk) return false;                       // several launches per layer
+    if (kn.ws == 2 || (kn.ws == 1 && g.vb == 3)) return false;    // warp-specialized kernel
+    mma_pass(p, c, g, 0, da);
+    const int R = g.per_pass == 1 ? 1 : 2;
+    Group* gr = nullptr;
+    for (Group& x : groups)
+      if (x.D == g.D && x.kb == g.kb && x.vb == g.vb && x.R == R) gr = &x;
+    if (!gr) {
+      groups.push_back(Group{g.D, g.kb, g.vb, R, {}, {}});
+      gr = &groups.back();
+    }
+    if ((int)gr->p.size() == kMaxLayers) flush(*gr);
+    gr->p.push_back(p);
+    gr->bh.push_back(g.BH);
+    return true;
+  };
+  for (int l = 0; l < n; ++l) {
+    kvmix_cache* c = caches[l];
+    if (k) {
+      if (c->total() + t > c->cap || t < 1) {
+        cache_append(c, k[l], v[l], kv_dt, t, st);  // raises the reference's errors
+      } else {
+        check_query_shape(c, Hq, tq);
+        DecodeAppend da;
+        if (cache_append_decode_plan(c, k[l], v[l], kv_dt, t, &da)) {
+          if (try_add(c, q[l], out[l], &da)) continue;
+          launch_decode_append(da, st);
+        } else {
+          cache_append(c, k[l], v[l], kv_dt, t, st);
+        }
+      }
+    }
+    check_attend(c, Hq, tq);
+    if (try_add(c, q[l], out[l], nullptr)) continue;
+    Workspace ws(st);
+    attend(c, q[l], q_dt, Hq, tq, out[l], nullptr, ws, st);
+  }
+  for (Group& g : groups) flush(g);
+}
+
 }  // namespace kvb
+

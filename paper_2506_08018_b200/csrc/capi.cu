@@ -91,6 +91,37 @@ void check_cache(const kvmix_cache* c) {
   if (!c) invalid("null cache handle");
 }
 
+// kvmix_*attend_layers: one multi-layer launch per kernel instance when every cache is
+// valid, on one device and distinct (a repeated cache needs its appends in order) and no
+// layer's output overlaps another layer's output or any input (the layers of one launch
+// run concurrently; the per-layer loop keeps the sequential semantics for such calls)
+bool batchable(kvmix_cache* const* caches, int n, const void* const* q, size_t q_bytes, const void* const* k,
+               const void* const* v, size_t kv_bytes, float* const* out, size_t out_bytes) {
+  if (n < 2 || !caches || !q || !out) return false;
+  for (int l = 0; l < n; ++l) {
+    check_cache(caches[l]);
+    const kvmix_cache* c = caches[l];
+    if (c->device != caches[0]->device || c->B != caches[0]->B || c->H != caches[0]->H || c->D != caches[0]->D)
+      return false;
+    if (!q[l] || !out[l] || (k && (!k[l] || !v[l]))) return false;
+    for (int j = 0; j < l; ++j)
+      if (caches[j] == caches[l]) return false;
+  }
+  auto overlap = [](const void* a, size_t na, const void* b, size_t nb) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+  };
+  for (int l = 0; l < n; ++l) {
+    for (int j = 0; j < n; ++j) {
+      if (j != l && overlap(out[l], out_bytes, out[j], out_bytes)) return false;
+      if (overlap(out[l], out_bytes, q[j], q_bytes)) return false;
+      if (k && (overlap(out[l], out_bytes, k[j], kv_bytes) || overlap(out[l], out_bytes, v[j], kv_bytes)))
+        return false;
+    }
+  }
+  return true;
+}
+
 // every cache entry point runs on the cache's device (the caller's current device is restored)
 #define KVB_ON_CACHE_DEVICE(c) \
   check_cache(c);              \
@@ -411,6 +442,15 @@ kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const
                                  int q_heads, int t, float* const* out, void* stream) {
   return guard([&] {
     if (n_layers < 0) invalid("n_layers must be non-negative");
+    const auto esz = [](kvmix_dtype d) { return d == KVMIX_F16 ? (size_t)2 : (size_t)4; };
+    if (n_layers >= 2 && caches && caches[0] && (dt == KVMIX_F32 || dt == KVMIX_F16) && q_heads > 0 && t > 0 &&
+        batchable(caches, n_layers, q, (size_t)caches[0]->B * q_heads * t * caches[0]->D * esz(dt), nullptr,
+                  nullptr, 0, out, (size_t)caches[0]->B * q_heads * t * caches[0]->D * 4)) {
+      DeviceGuard dev_guard_(caches[0]->device);
+      attend_layers(const_cast<kvmix_cache* const*>(caches), n_layers, nullptr, nullptr, KVMIX_F32, 0, q, dt,
+                    q_heads, t, out, as_stream(stream));
+      return;
+    }
     for (int l = 0; l < n_layers; ++l) {
       KVB_ON_CACHE_DEVICE(caches[l]);
       Workspace ws(as_stream(stream));
@@ -429,6 +469,15 @@ kvmix_status kvmix_append_attend_layers(kvmix_cache* const* caches, int n_layers
   return guard([&] {
     if (n_layers < 0) invalid("n_layers must be non-negative");
     if (q_dt != KVMIX_F32 && q_dt != KVMIX_F16) invalid("unsupported dtype");
+    const auto esz = [](kvmix_dtype d) { return d == KVMIX_F16 ? (size_t)2 : (size_t)4; };
+    if (n_layers >= 2 && caches && caches[0] && k && v && q_heads > 0 && tq > 0 && t > 0 &&
+        batchable(caches, n_layers, q, (size_t)caches[0]->B * q_heads * tq * caches[0]->D * esz(q_dt), k, v,
+                  (size_t)caches[0]->B * caches[0]->H * t * caches[0]->D * esz(kv_dt), out,
+                  (size_t)caches[0]->B * q_heads * tq * caches[0]->D * 4)) {
+      DeviceGuard dev_guard_(caches[0]->device);
+      attend_layers(caches, n_layers, k, v, kv_dt, t, q, q_dt, q_heads, tq, out, as_stream(stream));
+      return;
+    }
     for (int l = 0; l < n_layers; ++l) {
       KVB_ON_CACHE_DEVICE(caches[l]);
       Workspace ws(as_stream(stream));

@@ -188,6 +188,7 @@ struct Knobs {
   int ws = 1;  // warp-specialized kernel (attention_ws.cu): 0 never, 1 for 3-bit Values, 2 always
   int tc = 0;  // tcgen05 kernel (attention_tc.cu) for the fast groups where it applies
   int pdl = 1;  // programmatic dependent launch between the layers of kvmix_*attend_layers
+  int layers = 1;  // kvmix_*attend_layers: one launch per kernel instance (else per layer)
   bool skip_tail = false, no_window = false;
 };
 Knobs& knobs();
@@ -254,6 +255,16 @@ struct MmaParams {
   int64_t ext_NT;
   int ext_Tb, ext_R;
 };
+
+// Parameters of a multi-layer launch (attend_mma_layers_kernel): layer l's warps are
+// [off[l], off[l + 1]). Passed by value in the kernel's parameter space (<= 32 KB).
+constexpr int kMaxLayers = 32;
+struct MmaLayers {
+  int n;
+  int off[kMaxLayers + 1];
+  MmaParams l[kMaxLayers];
+};
+static_assert(sizeof(MmaLayers) <= 32000, "kernel parameter space");
 
 // Partials of the fast groups written by attend_tc_kernel (attention_tc.cu).
 struct TcExt {
