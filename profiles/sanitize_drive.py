@@ -1,7 +1,7 @@
 """compute-sanitizer target: a small pass over every device path (quantize / pack /
 dequantize, prefill + decode appends incl. Key-group age-outs, the fused append+attend,
 the three tensor-core attention kernels (single-warp and warp-specialized IMMA, tcgen05) and the generic one, multi-row / GQA passes, snapshot and
-segment export) on shapes small enough for memcheck / racecheck / synccheck to finish.
+segment export, multi-layer launches) on shapes small enough for memcheck / racecheck / synccheck to finish.
 
   compute-sanitizer --tool memcheck --target-processes all python profiles/sanitize_drive.py
 """
@@ -40,5 +40,25 @@ for tc, ws in (CONFIGS[i] for i in PICK):
         c.snapshot_dequantized()
         c.key_segments()
         c.value_segments()
+# multi-layer decode steps: layers of one kernel instance share one launch
+# (attend_mma_layers_kernel), consecutive launches overlap (programmatic dependent launch)
+K.set_knob("KVMIX_TC", 0)
+K.set_knob("KVMIX_WS", 1)
+for G in (1, 2, 4):
+    B, H, D = 2, 3, 128
+    stack = []
+    for kb, vb, r in ((2, 2, 0.1), (3, 4, 0.2), (2, 2, 0.1), (2, 3, 0.1), (3, 4, 0.2)):
+        c = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, 32), B, H, D, capacity_tokens=600,
+                           tail_dtype=torch.float16)
+        c.append(torch.randn(B, H, 400, D, device=dev), torch.randn(B, H, 400, D, device=dev))
+        stack.append(c)
+    n = len(stack)
+    for s in range(40):  # crosses a Key-group age-out
+        ks = [torch.randn(B, H, 1, D, device=dev) for _ in range(n)]
+        vs = [torch.randn(B, H, 1, D, device=dev) for _ in range(n)]
+        qs = [torch.randn(B, H * G, 1, D, device=dev) for _ in range(n)]
+        outs = [torch.empty(B, H * G, 1, D, device=dev) for _ in range(n)]
+        K.append_attend_layers(stack, ks, vs, qs, outs)
+    K.attend_layers(stack, qs, outs)
 torch.cuda.synchronize()
 print("sanitize drive ok")
