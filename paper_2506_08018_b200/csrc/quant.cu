@@ -100,6 +100,53 @@ __device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc,
   return word;
 }
 
+// One interior Mixed3 word (quant.hpp:49-53): slots 0..9 3-bit with their group's scale,
+// slot 10 the narrow 2-bit slot with the wide scale (scale * 7/3); slots k < kb belong to
+// group a, k >= kb to group b (a word spans at most two groups). Branch-free like
+// encode_word (the same 2^-19 bound: rcp.approx of the slot's scale, the magic-add rounding,
+// a redo mask for near-ties; a zero scale gives a zero reciprocal, so its codes are 0 like
+// encode()); flagged slots are redone by the exact encode() afterwards (rare).
+template <bool WIDE>
+__device__ __forceinline__ uint32_t encode_m3_word(const float (&v)[11], int kb, float sa, float na, float sb,
+                                                   float nb) {
+  constexpr float kTie = 0x1p-14f;
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const float ra = sa == 0.0f ? 0.0f : rcp_approx(sa), rb = sb == 0.0f ? 0.0f : rcp_approx(sb);
+  uint32_t word = 0, slow = 0;
+#pragma unroll
+  for (int k = 0; k < 11; ++k) {
+    const bool hi = k >= kb;
+    const float mn = hi ? nb : na;
+    float rc = hi ? rb : ra;
+    float qm = 7.0f;
+    if (k == 10) {  // narrow slot: the wide scale's reciprocal, codes 0..3
+      const float ws = wide_scale(hi ? sb : sa);
+      rc = ws == 0.0f ? 0.0f : rcp_approx(ws);
+      qm = 3.0f;
+    }
+    const float va = __fmul_rn(__fsub_rn(v[k], mn), rc);
+    const float vc = fminf(fmaxf(va, 0.f), qm);  // (NaN -> 0)
+    const float u = __fadd_rn(vc, kMagic);
+    const float dr = vc - __fsub_rn(u, kMagic);
+    bool redo = fabsf(dr) > 0.5f - kTie;
+    if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
+    slow |= (uint32_t)redo << k;
+    word |= (__float_as_uint(u) & (k == 10 ? 3u : 7u)) << (k == 10 ? 30 : 3 * k);
+  }
+  while (slow) {
+    const int i = __ffs(slow) - 1;
+    slow &= slow - 1;
+    float xi = v[0];
+#pragma unroll
+    for (int k = 1; k < 11; ++k)
+      if (k == i) xi = v[k];
+    const bool hi = i >= kb;
+    const uint32_t sh = i == 10 ? 30u : 3u * i, mask = i == 10 ? 3u : 7u;
+    word = (word & ~(mask << sh)) | (encode(xi, hi ? sb : sa, hi ? nb : na, 3, i == 10) << sh);
+  }
+  return word;
+}
+
 // ---- Keys -------------------------------------------------------------------------------
 // x: [B,H,T,D]; words/meta in reference order. Tile: n tokens (multiple of gs), all D.
 template <typename T, int BITS>
@@ -111,25 +158,36 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   constexpr int bits = BITS;
   (void)bits_rt;
   extern __shared__ __align__(16) uint8_t qsm[];
-  T* xs = reinterpret_cast<T*>(qsm);  // [n][D] in the input type (fp16 staging: 6 CTAs/SM)
-  uint32_t* ms = reinterpret_cast<uint32_t*>(qsm + ((size_t)n * D * sizeof(T) + 15) / 16 * 16);  // [D][n/gs]
+  // Mixed3 (gs >= 11): the last word of a channel's run holds up to 10 codes of the NEXT
+  // run, all inside that run's first group; that group is staged too (rows nt .. nt+gs-1:
+  // this channel's next span, or, at the end of the (b, kv-head), tokens 0 .. gs-1 for
+  // channel d+1) so those codes and their group meta come from shared memory
+  const int ext = (BITS == 3 && gs >= 11) ? 1 : 0;
+  T* xs = reinterpret_cast<T*>(qsm);  // [n (+ gs)][D] in the input type (fp16 staging: 6 CTAs/SM)
+  uint32_t* ms = reinterpret_cast<uint32_t*>(qsm + ((size_t)(n + ext * gs) * D * sizeof(T) + 15) / 16 * 16);
   const int bh = blockIdx.y;
   const int t0 = blockIdx.x * n;
   const int nt = min(n, T_ - t0);  // always a multiple of gs (T % gs == 0)
   const int gpt = nt / gs;
+  const int gst = gpt + ext;       // meta columns per channel: [D][gst]
   const int gpc = T_ / gs;
   const int q_max = q_max_for_bits(bits);
   const T* src = x + ((size_t)bh * T_ + t0) * D;
+  const bool next_span = t0 + nt < T_;
 
-  if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked): raw 16-byte copies
-    for (int i = threadIdx.x; i < nt * D / Vec<T>::N; i += blockDim.x)
-      reinterpret_cast<uint4*>(xs)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
-  } else {
-    for (int i = threadIdx.x; i < nt * D; i += blockDim.x) xs[i] = src[i];
-  }
+  auto stage = [&](T* dst, const T* from, int rows) {
+    if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked): raw 16-byte copies
+      for (int i = threadIdx.x; i < rows * D / Vec<T>::N; i += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(from) + i);
+    } else {
+      for (int i = threadIdx.x; i < rows * D; i += blockDim.x) dst[i] = from[i];
+    }
+  };
+  stage(xs, src, nt);
+  if (ext) stage(xs + (size_t)nt * D, next_span ? src + (size_t)nt * D : x + (size_t)bh * T_ * D, gs);
   __syncthreads();
 
-  for (int i = threadIdx.x; i < D * gpt; i += blockDim.x) {
+  for (int i = threadIdx.x; i < D * gst; i += blockDim.x) {
     const int d = i % D, g = i / D;  // d fastest: conflict-free smem columns
     // fminf / fmaxf skip NaN like the reference's ordered fold (quant.hpp:128-139) and differ
     // from it only in the sign of a zero extremum (the fold keeps the first of -0 / +0) and
@@ -150,9 +208,8 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       }
     }
     const uint32_t m = make_meta(mn, mx, q_max);
-    ms[d * gpt + g] = m;
-    const size_t c = (size_t)bh * D + d;
-    meta[c * gpc + t0 / gs + g] = m;
+    ms[d * gst + g] = m;
+    if (g < gpt) meta[((size_t)bh * D + d) * gpc + t0 / gs + g] = m;
   }
   __syncthreads();
 
@@ -165,7 +222,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
         float v[CPW];
 #pragma unroll
         for (int k = 0; k < CPW; ++k) v[k] = ld_f(&xs[(j * CPW + k) * D + d]);
-        const uint32_t m = ms[d * gpt + (j * CPW) / gs];
+        const uint32_t m = ms[d * gst + (j * CPW) / gs];
         const size_t w = (((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j;
         words[w] = encode_word<BITS, CPW, !std::is_same<T, __half>::value>(v, meta_scale(m), meta_min(m), q_max);
       }
@@ -192,26 +249,19 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       if (gs >= 11 && p0 + 11 <= s1) {  // interior Mixed3 word: <= two groups, slot 10 narrow
         const int tt0 = (int)(p0 - s0);
         const int j0 = tt0 / gs, kb = (j0 + 1) * gs - tt0;  // first code of group j0 + 1
-        const uint32_t ma = ms[d * gpt + j0], mb = kb < 11 ? ms[d * gpt + j0 + 1] : ma;
-        const float sa = meta_scale(ma), na = meta_min(ma), ra = rcp_approx(sa);
-        const float sb = meta_scale(mb), nb = meta_min(mb), rb = rcp_approx(sb);
+        const uint32_t ma = ms[d * gst + j0], mb = kb < 11 ? ms[d * gst + j0 + 1] : ma;
+        float xv[11];
 #pragma unroll
-        for (int k = 0; k < 10; ++k) {
-          const bool hi = k >= kb;
-          word |= encode_fast(ld_f(&xs[(tt0 + k) * D + d]), hi ? sb : sa, hi ? nb : na, hi ? sb : sa, hi ? rb : ra, 7, 3,
-                              false) << (3 * k);
-        }
-        const float sn = kb <= 10 ? sb : sa, nn = kb <= 10 ? nb : na;
-        word |= encode_fast(ld_f(&xs[(tt0 + 10) * D + d]), sn, nn, wide_scale(sn), rcp_approx(wide_scale(sn)), 3, 3, true)
-                << 30;
-        words[w] = word;
+        for (int k = 0; k < 11; ++k) xv[k] = ld_f(&xs[(tt0 + k) * D + d]);
+        words[w] = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, meta_scale(ma), meta_min(ma), meta_scale(mb),
+                                                                   meta_min(mb));
         continue;
       }
     }
     int tt = (int)(p0 - s0);                                    // token of the first code
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;                  // stream index mod 11
     int g = tt / gs, gend = (g + 1) * gs;                       // current group and its end
-    uint32_t m = ms[d * gpt + g];
+    uint32_t m = ms[d * gst + g];
     float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
     float ws = 0.f, rcw = 0.f;  // Mixed3 narrow slots: wide scale and its reciprocal
     if (bits == 3) {
@@ -223,7 +273,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       if (tt == gend) {
         ++g;
         gend += gs;
-        m = ms[d * gpt + g];
+        m = ms[d * gst + g];
         sc = meta_scale(m);
         mnv = meta_min(m);
         rc = rcp_approx(sc);
@@ -237,7 +287,16 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       word |= code << field_shift(bits, (uint32_t)k);
       if (++r11 == 11) r11 = 0;
     }
-    size_t cached = ~(size_t)0;  // codes of the next run (only at run ends): group meta once
+    if (ext && k < cpw) {  // codes of the next run: its first group, staged at rows nt ..
+      const int dn = next_span ? d : d + 1;
+      if (dn < D) {
+        const uint32_t m2 = ms[dn * gst + gpt];
+        const float s2 = meta_scale(m2), n2 = meta_min(m2);
+        for (int r = 0; k < cpw && p0 + k < n_total; ++k, ++r)
+          word |= encode(ld_f(&xs[(nt + r) * D + dn]), s2, n2, bits, is_narrow(bits, p0 + k)) << field_shift(bits, (uint32_t)k);
+      }
+    }
+    size_t cached = ~(size_t)0;  // codes of the next (b, kv-head): group meta once
     float sc2 = 0.f, mn2 = 0.f;
     for (; k < cpw; ++k) {
       const size_t p = p0 + k;
@@ -493,12 +552,24 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
   __syncwarp();
   const int ng = ne / gs;
   if (lane < ng) {
-    const float* g = xs + lane * gs;
-    float mn = g[0], mx = mn;
-    for (int j = 1; j < gs; ++j) {
-      const float v = g[j];
-      mn = v < mn ? v : mn;
-      mx = v > mx ? v : mx;
+    // fminf / fmaxf skip NaN like the ordered fold and differ from it only in the sign of a
+    // zero extremum and for a NaN first element: those groups redo the fold (rare)
+    const float4* g4 = reinterpret_cast<const float4*>(xs + lane * gs);
+    float mn = xs[lane * gs], mx = mn;
+#pragma unroll 4
+    for (int j = 0; j < gs / 4; ++j) {
+      const float4 q = g4[j];
+      mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+      mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+    }
+    if (mn == 0.f || mx == 0.f || isnan(xs[lane * gs])) {
+      const float* g = xs + lane * gs;
+      mn = mx = g[0];
+      for (int j = 1; j < gs; ++j) {
+        const float v = g[j];
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+      }
     }
     const uint32_t m = make_meta(mn, mx, 7);
     meta[chunk * 11 + lane] = m;
@@ -519,17 +590,11 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
     if (11 * wl + 11 <= ne) {  // every chunk but the stream's last
       // a word spans at most two groups: j0 for its first codes, j0 + 1 after the boundary
       const int j0 = (11 * wl) / gs, kb = (j0 + 1) * gs - 11 * wl;  // first code of group j0 + 1
-      const float s0 = gm[j0], m0 = gm[11 + j0], r0 = gm[22 + j0];
-      const float s1 = kb < 11 ? gm[j0 + 1] : s0, m1 = kb < 11 ? gm[11 + j0 + 1] : m0;
-      const float r1 = kb < 11 ? gm[22 + j0 + 1] : r0;
+      const int j1 = kb < 11 ? j0 + 1 : j0;
+      float xv[11];
 #pragma unroll
-      for (int k = 0; k < 10; ++k) {
-        const bool hi = k >= kb;
-        word |= encode_fast(xs[11 * wl + k], hi ? s1 : s0, hi ? m1 : m0, hi ? s1 : s0, hi ? r1 : r0, 7, 3, false) << (3 * k);
-      }
-      const int j10 = kb <= 10 ? j0 + 1 : j0;  // the narrow slot (k = 10)
-      const float sn = gm[j10];
-      word |= encode_fast(xs[11 * wl + 10], sn, gm[11 + j10], wide_scale(sn), gm[33 + j10], 3, 3, true) << 30;
+      for (int k = 0; k < 11; ++k) xv[k] = xs[11 * wl + k];
+      word = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, gm[j0], gm[11 + j0], gm[j1], gm[11 + j1]);
     } else {
 #pragma unroll
       for (int k = 0; k < 11; ++k) {
@@ -639,7 +704,10 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     // tile of k groups of gs tokens: aim for ~128 tokens, bounded by shared memory
     int k = std::max(1, 128 / gs);
     const size_t esz = dt == KVMIX_F16 ? 2 : 4;  // staged in the input type
-    auto smem_of = [&](int kk) { return ((size_t)kk * gs * D * esz + 15) / 16 * 16 + (size_t)D * kk * 4; };
+    const int ext = (bits == 3 && gs >= 11) ? 1 : 0;  // + the next run's first group (kernel)
+    auto smem_of = [&](int kk) {
+      return ((size_t)(kk + ext) * gs * D * esz + 15) / 16 * 16 + (size_t)D * (kk + ext) * 4;
+    };
     while (k > 1 && smem_of(k) > (size_t)max_smem) --k;
     if (smem_of(k) > (size_t)227 * 1024) invalid("quantize: group_size * head_dim too large for one tile");
     const int n_tok = k * gs;
