@@ -69,33 +69,65 @@ struct Vec<float> {
 // exact encode() afterwards (rare). NaN -> 0 through the clamp, like the reference. fp16
 // inputs cannot produce |v| >= 2^62 (|x - min| <= 2^17, scale >= 2^-24), so WIDE = false
 // skips that check.
+// sm_100 packed fp32 pairs (FADD2 / FMUL2): two IEEE round-to-nearest operations per
+// instruction, bit-identical to two __fadd_rn / __fmul_rn
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+  float2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  float2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
+
 template <int BITS, int CPW, bool WIDE>
 __device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc, float mnv, int q_max) {
   constexpr float kTie = 0x1p-14f;
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  static_assert(CPW % 2 == 0, "codes in pairs");
   if (sc == 0.0f) return 0u;
   const float rc = rcp_approx(sc);
   const float qm = (float)q_max;
-  uint32_t word = 0, slow = 0;
+  const float2 mn2 = make_float2(mnv, mnv), rc2 = make_float2(rc, rc);
+  const float2 mg2 = make_float2(kMagic, kMagic), nmg2 = make_float2(-kMagic, -kMagic);
+  uint32_t word = 0;
+  float far = 0.f;  // largest |vc - RN(vc)| of the word
+  bool huge = false;
 #pragma unroll
-  for (int i = 0; i < CPW; ++i) {
-    const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
-    const float vc = fminf(fmaxf(va, 0.f), qm);  // (NaN -> 0)
-    const float u = __fadd_rn(vc, kMagic);
-    const float dr = vc - __fsub_rn(u, kMagic);  // vc - RN(vc), in [-0.5, 0.5]
-    bool redo = fabsf(dr) > 0.5f - kTie;         // near a half-integer: ties decide
-    if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
-    slow |= (uint32_t)redo << i;
-    word |= (__float_as_uint(u) & (uint32_t)q_max) << (BITS * i);
+  for (int i = 0; i < CPW; i += 2) {
+    const float2 va = f2_mul(f2_sub(make_float2(v[i], v[i + 1]), mn2), rc2);
+    const float2 vc = make_float2(fminf(fmaxf(va.x, 0.f), qm), fminf(fmaxf(va.y, 0.f), qm));  // (NaN -> 0)
+    const float2 u = f2_add(vc, mg2);
+    const float2 dr = f2_sub(vc, f2_add(u, nmg2));  // vc - RN(vc), exact
+    far = fmaxf(far, fmaxf(fabsf(dr.x), fabsf(dr.y)));
+    if constexpr (WIDE) huge = huge || !(fabsf(va.x) < 0x1p62f) || !(fabsf(va.y) < 0x1p62f);
+    word |= (__float_as_uint(u.x) & (uint32_t)q_max) << (BITS * i);
+    word |= (__float_as_uint(u.y) & (uint32_t)q_max) << (BITS * (i + 1));
   }
-  while (slow) {
-    const int i = __ffs(slow) - 1;
-    slow &= slow - 1;
-    float xi = v[0];
+  if (far > 0.5f - kTie || huge) {  // near a half-integer somewhere (rare): ties decide
 #pragma unroll
-    for (int k = 1; k < CPW; ++k)
-      if (k == i) xi = v[k];
-    word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(xi, sc, mnv, BITS, false) << (BITS * i));
+    for (int i = 0; i < CPW; ++i) {
+      const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
+      const float vc = fminf(fmaxf(va, 0.f), qm);
+      const float dr = vc - __fsub_rn(__fadd_rn(vc, kMagic), kMagic);
+      bool redo = fabsf(dr) > 0.5f - kTie;
+      if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
+      if (redo)
+        word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(v[i], sc, mnv, BITS, false) << (BITS * i));
+    }
   }
   return word;
 }
@@ -112,37 +144,50 @@ __device__ __forceinline__ uint32_t encode_m3_word(const float (&v)[11], int kb,
   constexpr float kTie = 0x1p-14f;
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   const float ra = sa == 0.0f ? 0.0f : rcp_approx(sa), rb = sb == 0.0f ? 0.0f : rcp_approx(sb);
-  uint32_t word = 0, slow = 0;
+  const float2 mg2 = make_float2(kMagic, kMagic);
+  uint32_t word = 0;
+  float far = 0.f;  // largest |vc - RN(vc)| of the word
+  bool huge = false;
 #pragma unroll
-  for (int k = 0; k < 11; ++k) {
-    const bool hi = k >= kb;
-    const float mn = hi ? nb : na;
-    float rc = hi ? rb : ra;
-    float qm = 7.0f;
-    if (k == 10) {  // narrow slot: the wide scale's reciprocal, codes 0..3
-      const float ws = wide_scale(hi ? sb : sa);
-      rc = ws == 0.0f ? 0.0f : rcp_approx(ws);
-      qm = 3.0f;
-    }
-    const float va = __fmul_rn(__fsub_rn(v[k], mn), rc);
-    const float vc = fminf(fmaxf(va, 0.f), qm);  // (NaN -> 0)
-    const float u = __fadd_rn(vc, kMagic);
-    const float dr = vc - __fsub_rn(u, kMagic);
-    bool redo = fabsf(dr) > 0.5f - kTie;
-    if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
-    slow |= (uint32_t)redo << k;
-    word |= (__float_as_uint(u) & (k == 10 ? 3u : 7u)) << (k == 10 ? 30 : 3 * k);
+  for (int k = 0; k < 10; k += 2) {  // 3-bit slots in pairs (FADD2 / FMUL2)
+    const float2 mn = make_float2(k >= kb ? nb : na, k + 1 >= kb ? nb : na);
+    const float2 rc = make_float2(k >= kb ? rb : ra, k + 1 >= kb ? rb : ra);
+    const float2 va = f2_mul(f2_sub(make_float2(v[k], v[k + 1]), mn), rc);
+    const float2 vc = make_float2(fminf(fmaxf(va.x, 0.f), 7.f), fminf(fmaxf(va.y, 0.f), 7.f));  // (NaN -> 0)
+    const float2 u = f2_add(vc, mg2);
+    const float2 dr = f2_sub(vc, f2_sub(u, mg2));
+    far = fmaxf(far, fmaxf(fabsf(dr.x), fabsf(dr.y)));
+    if constexpr (WIDE) huge = huge || !(fabsf(va.x) < 0x1p62f) || !(fabsf(va.y) < 0x1p62f);
+    word |= (__float_as_uint(u.x) & 7u) << (3 * k);
+    word |= (__float_as_uint(u.y) & 7u) << (3 * k + 3);
   }
-  while (slow) {
-    const int i = __ffs(slow) - 1;
-    slow &= slow - 1;
-    float xi = v[0];
+  {  // slot 10: the narrow slot (wide scale, codes 0..3)
+    const bool hi = 10 >= kb;
+    const float ws = wide_scale(hi ? sb : sa);
+    const float rw = ws == 0.0f ? 0.0f : rcp_approx(ws);
+    const float va = __fmul_rn(__fsub_rn(v[10], hi ? nb : na), rw);
+    const float vc = fminf(fmaxf(va, 0.f), 3.f);
+    const float u = __fadd_rn(vc, kMagic);
+    far = fmaxf(far, fabsf(vc - __fsub_rn(u, kMagic)));
+    if constexpr (WIDE) huge = huge || !(fabsf(va) < 0x1p62f);
+    word |= (__float_as_uint(u) & 3u) << 30;
+  }
+  if (far > 0.5f - kTie || huge) {  // near a half-integer somewhere (rare): ties decide
 #pragma unroll
-    for (int k = 1; k < 11; ++k)
-      if (k == i) xi = v[k];
-    const bool hi = i >= kb;
-    const uint32_t sh = i == 10 ? 30u : 3u * i, mask = i == 10 ? 3u : 7u;
-    word = (word & ~(mask << sh)) | (encode(xi, hi ? sb : sa, hi ? nb : na, 3, i == 10) << sh);
+    for (int k = 0; k < 11; ++k) {
+      const bool hi = k >= kb;
+      const float s = k == 10 ? wide_scale(hi ? sb : sa) : (hi ? sb : sa);
+      const float rc = s == 0.0f ? 0.0f : rcp_approx(s);
+      const float va = __fmul_rn(__fsub_rn(v[k], hi ? nb : na), rc);
+      const float vc = fminf(fmaxf(va, 0.f), k == 10 ? 3.f : 7.f);
+      const float dr = vc - __fsub_rn(__fadd_rn(vc, kMagic), kMagic);
+      bool redo = fabsf(dr) > 0.5f - kTie;
+      if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
+      if (redo) {
+        const uint32_t sh = k == 10 ? 30u : 3u * k, mask = k == 10 ? 3u : 7u;
+        word = (word & ~(mask << sh)) | (encode(v[k], hi ? sb : sa, hi ? nb : na, 3, k == 10) << sh);
+      }
+    }
   }
   return word;
 }
