@@ -159,8 +159,10 @@ __device__ uint64_t* g_trace = nullptr;  // debug builds: per-warp timeline (KVM
 #endif
 
 // The kernel body: warp gw (of the layer whose parameters p are) runs its unit range.
-template <int D, int KB, int VB, int R, int GS>
+// CS = false: the checksum is compiled out (multi-layer launches never ask for it).
+template <int D, int KB, int VB, int R, int GS, bool CS>
 __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw) {
+  const bool want_cs = CS && p.want_cs;
   static_assert(D == 64 || D == 128, "IMMA attention handles D in {64, 128}");
   static_assert(VB == 2 || VB == 4, "Values: 2 or 4 bits");
   static_assert(R == 1 || R == 2, "one or two query rows per KV head");
@@ -217,7 +219,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) a0[r][c] = 0.f;
     }
-    if (lane == 0 && p.want_cs) p.part_cs[pbase + wg + wg] = 0.0;
+    if (lane == 0 && want_cs) p.part_cs[pbase + wg + wg] = 0.0;
     ext_merge_write<D, R>(p, wg, lane, pass, prow0, prows, m0, l0, a0);
     return;
   }
@@ -228,7 +230,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
     if (wg < w0 || wg > w1) return;
     pdl_gate(p);
     if (lane < prows) p.part_ml[(pbase + wg + bh) * p.rows + lane] = make_float2(-INFINITY, 0.f);
-    if (lane == 0 && p.want_cs) p.part_cs[pbase + wg + bh] = 0.0;
+    if (lane == 0 && want_cs) p.part_cs[pbase + wg + bh] = 0.0;
     if (arrive_last(p, bh, lane, pass, wg)) merge_bh<D>(p, bh, lane, pass, prow0, prows);
     return;
   }
@@ -373,7 +375,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
 #pragma unroll
       for (int c = 0; c < 4; ++c) qc[r][c] = qv[r][c] * clsL;
     float m_run = -INFINITY, l_run = 0.f;  // row my_r (lazy reference max, log2 units)
-    if (p.want_cs) csm[lane] = 0.0;
+    if (want_cs) csm[lane] = 0.0;
     int accv[NM][4];
 #pragma unroll
     for (int i = 0; i < NM; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0;
@@ -701,7 +703,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
             lb[u2] = fmaf(pb, fac[2 * u2 + 1], betaL) + corr[2 * u2 + 1];
           }
         }
-        if (p.want_cs && row_ok && (t & 1) == 0) csm[lane] += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);
+        if (want_cs && row_ok && (t & 1) == 0) csm[lane] += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);
 
         // ---- online softmax (row my_r) -----------------------------------------------------
         float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
@@ -794,7 +796,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
             }
           }
           const float scn = acc * p.inv;
-          if (p.want_cs) csm[lane] += (double)scn;
+          if (want_cs) csm[lane] += (double)scn;
           sl = scn * kLog2e;
         }
         float tmax = sl;
@@ -946,7 +948,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
           for (int r = 0; r < R; ++r) {
             if (r < prows) {
               const float sc = x[i][r] * p.inv;
-              if (p.want_cs && lane == 0) csm[0] += (double)sc;
+              if (want_cs && lane == 0) csm[0] += (double)sc;
               const float ls = sc * kLog2e;
               const float m_new = fmaxf(m_all[r], ls);
               const float alpha = exp2f(m_all[r] - m_new);
@@ -966,7 +968,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
     // A (b, kv-head) inside this warp's range is normalized and written directly; otherwise
     // the partial goes to slot wg + bh and the last of its warps to arrive merges them.
     const size_t slot = pbase + wg + bh;
-    if (p.want_cs) {
+    if (want_cs) {
       double csl = csm[lane];
       for (int o = 16; o > 0; o >>= 1) csl += __shfl_xor_sync(0xffffffffu, csl, o);
       if (lane == 0) p.part_cs[slot] = csl;
@@ -1020,7 +1022,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
 
 template <int D, int KB, int VB, int R, int GS>
 __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R)) attend_mma_kernel(MmaParams p) {
-  attend_mma_body<D, KB, VB, R, GS>(p, blockIdx.x * kMmaWarps + (threadIdx.x >> 5));
+  attend_mma_body<D, KB, VB, R, GS, true>(p, blockIdx.x * kMmaWarps + (threadIdx.x >> 5));
 }
 
 // Several layers of a decode step in one launch: warps [off[l], off[l+1]) run layer l with
@@ -1035,7 +1037,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, KVB_MIN_CTAS(KB, R))
   int li = 0;
   while (li + 1 < mp.n && gw >= mp.off[li + 1]) ++li;
   if (gw >= mp.off[li + 1]) return;
-  attend_mma_body<D, KB, VB, R, GS>(mp.l[li], gw - mp.off[li]);
+  attend_mma_body<D, KB, VB, R, GS, false>(mp.l[li], gw - mp.off[li]);
 }
 
 // Ring depth, dynamic shared memory and the resident wave (warps) of kernel `kern`.
