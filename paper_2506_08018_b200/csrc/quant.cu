@@ -93,8 +93,9 @@ __device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
   return r;
 }
 
-template <int BITS, int CPW, bool WIDE>
-__device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc, float mnv, int q_max) {
+// (get(i): the word's i-th input as fp32, evaluated where used)
+template <int BITS, int CPW, bool WIDE, typename Get>
+__device__ __forceinline__ uint32_t encode_word_g(Get get, float sc, float mnv, int q_max) {
   constexpr float kTie = 0x1p-14f;
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   static_assert(CPW % 2 == 0, "codes in pairs");
@@ -108,7 +109,7 @@ __device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc,
   bool huge = false;
 #pragma unroll
   for (int i = 0; i < CPW; i += 2) {
-    const float2 va = f2_mul(f2_sub(make_float2(v[i], v[i + 1]), mn2), rc2);
+    const float2 va = f2_mul(f2_sub(make_float2(get(i), get(i + 1)), mn2), rc2);
     const float2 vc = make_float2(fminf(fmaxf(va.x, 0.f), qm), fminf(fmaxf(va.y, 0.f), qm));  // (NaN -> 0)
     const float2 u = f2_add(vc, mg2);
     const float2 dr = f2_sub(vc, f2_add(u, nmg2));  // vc - RN(vc), exact
@@ -120,16 +121,21 @@ __device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc,
   if (far > 0.5f - kTie || huge) {  // near a half-integer somewhere (rare): ties decide
 #pragma unroll
     for (int i = 0; i < CPW; ++i) {
-      const float va = __fmul_rn(__fsub_rn(v[i], mnv), rc);
+      const float va = __fmul_rn(__fsub_rn(get(i), mnv), rc);
       const float vc = fminf(fmaxf(va, 0.f), qm);
       const float dr = vc - __fsub_rn(__fadd_rn(vc, kMagic), kMagic);
       bool redo = fabsf(dr) > 0.5f - kTie;
       if constexpr (WIDE) redo = redo || !(fabsf(va) < 0x1p62f);
       if (redo)
-        word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(v[i], sc, mnv, BITS, false) << (BITS * i));
+        word = (word & ~((uint32_t)q_max << (BITS * i))) | (encode(get(i), sc, mnv, BITS, false) << (BITS * i));
     }
   }
   return word;
+}
+
+template <int BITS, int CPW, bool WIDE>
+__device__ __forceinline__ uint32_t encode_word(const float (&v)[CPW], float sc, float mnv, int q_max) {
+  return encode_word_g<BITS, CPW, WIDE>([&](int i) { return v[i]; }, sc, mnv, q_max);
 }
 
 // One interior Mixed3 word (quant.hpp:49-53): slots 0..9 3-bit with their group's scale,
@@ -194,14 +200,18 @@ __device__ __forceinline__ uint32_t encode_m3_word(const float (&v)[11], int kb,
 
 // ---- Keys -------------------------------------------------------------------------------
 // x: [B,H,T,D]; words/meta in reference order. Tile: n tokens (multiple of gs), all D.
-template <typename T, int BITS>
-__global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __restrict__ x, int H, int T_,
-                                                                 int D, int bits_rt, int gs, int n, int vec,
+// DT: compile-time head_dim (64 / 128: immediate shared-memory offsets; fp16 inputs fold and
+// encode channel PAIRS from one 32-bit load) or 0 (runtime D).
+template <typename T, int BITS, int DT>
+__global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_kernel(const T* __restrict__ x, int H, int T_,
+                                                                 int D_rt, int bits_rt, int gs, int n, int vec,
                                                                  uint32_t* __restrict__ words,
                                                                  uint32_t* __restrict__ meta,
                                                                  size_t n_total) {
   constexpr int bits = BITS;
   (void)bits_rt;
+  const int D = DT ? DT : D_rt;
+  constexpr bool PAIRS = DT != 0 && std::is_same<T, __half>::value;
   extern __shared__ __align__(16) uint8_t qsm[];
   // Mixed3 (gs >= 11): the last word of a channel's run holds up to 10 codes of the NEXT
   // run, all inside that run's first group; that group is staged too (rows nt .. nt+gs-1:
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   // channel d+1) so those codes and their group meta come from shared memory
   const int ext = (BITS == 3 && gs >= 11) ? 1 : 0;
   T* xs = reinterpret_cast<T*>(qsm);  // [n (+ gs)][D] in the input type (fp16 staging: 6 CTAs/SM)
-  uint32_t* ms = reinterpret_cast<uint32_t*>(qsm + ((size_t)(n + ext * gs) * D * sizeof(T) + 15) / 16 * 16);
+  uint32_t* ms = reinterpret_cast<uint32_t*>(qsm + ((size_t)(n + ext * gs) * D * sizeof(T) + 15) / 16 * 16);  // [gst][D]
   const int bh = blockIdx.y;
   const int t0 = blockIdx.x * n;
   const int nt = min(n, T_ - t0);  // always a multiple of gs (T % gs == 0)
@@ -232,11 +242,45 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
   if (ext) stage(xs + (size_t)nt * D, next_span ? src + (size_t)nt * D : x + (size_t)bh * T_ * D, gs);
   __syncthreads();
 
+  // group meta: the reference's ordered fold (quant.hpp:128-139); fminf / fmaxf (and the fp16
+  // __hmin2 / __hmax2, exact selections) skip NaN like it and differ from it only in the sign
+  // of a zero extremum (the fold keeps the first of -0 / +0) and when the FIRST element is NaN
+  // (the fold then stays NaN): those groups redo the ordered fold
+  auto ordered = [&](int d, int g, float& mn, float& mx) {
+    mn = mx = ld_f(&xs[(g * gs) * D + d]);
+    for (int j = 1; j < gs; ++j) {
+      const float v = ld_f(&xs[(g * gs + j) * D + d]);
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+  };
+  if constexpr (PAIRS) {
+    constexpr int DP = DT / 2;
+    const __half2* xs2 = reinterpret_cast<const __half2*>(xs);
+    for (int i = threadIdx.x; i < DP * gst; i += blockDim.x) {
+      const int dp = i % DP, g = i / DP;
+      const __half2* col = xs2 + (size_t)(g * gs) * DP + dp;
+      const __half2 x0 = col[0];
+      __half2 mn2 = x0, mx2 = x0;
+      for (int j = 1; j < gs; ++j) {
+        const __half2 v = col[j * DP];
+        mn2 = __hmin2(mn2, v);
+        mx2 = __hmax2(mx2, v);
+      }
+      const float2 fmn = __half22float2(mn2), fmx = __half22float2(mx2), f0 = __half22float2(x0);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int d = 2 * dp + c;
+        float mn = c ? fmn.y : fmn.x, mx = c ? fmx.y : fmx.x;
+        if (mn == 0.f || mx == 0.f || isnan(c ? f0.y : f0.x)) ordered(d, g, mn, mx);
+        const uint32_t m = make_meta(mn, mx, q_max);
+        ms[g * D + d] = m;
+        if (g < gpt) meta[((size_t)bh * D + d) * gpc + t0 / gs + g] = m;
+      }
+    }
+  } else
   for (int i = threadIdx.x; i < D * gst; i += blockDim.x) {
     const int d = i % D, g = i / D;  // d fastest: conflict-free smem columns
-    // fminf / fmaxf skip NaN like the reference's ordered fold (quant.hpp:128-139) and differ
-    // from it only in the sign of a zero extremum (the fold keeps the first of -0 / +0) and
-    // when the FIRST element is NaN (the fold then stays NaN): those groups redo the fold
     const float x0 = ld_f(&xs[(g * gs) * D + d]);
     float mn = x0, mx = x0;
     for (int j = 1; j < gs; ++j) {
@@ -244,16 +288,9 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       mn = fminf(mn, v);
       mx = fmaxf(mx, v);
     }
-    if (mn == 0.f || mx == 0.f || isnan(x0)) {
-      mn = mx = x0;
-      for (int j = 1; j < gs; ++j) {
-        const float v = ld_f(&xs[(g * gs + j) * D + d]);
-        mn = v < mn ? v : mn;
-        mx = v > mx ? v : mx;
-      }
-    }
+    if (mn == 0.f || mx == 0.f || isnan(x0)) ordered(d, g, mn, mx);
     const uint32_t m = make_meta(mn, mx, q_max);
-    ms[d * gst + g] = m;
+    ms[g * D + d] = m;
     if (g < gpt) meta[((size_t)bh * D + d) * gpc + t0 / gs + g] = m;
   }
   __syncthreads();
@@ -262,12 +299,30 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
     constexpr int CPW = 32 / BITS;
     if (gs % CPW == 0) {  // whole-group words (T % gs == 0): one meta per word, no run ends
       const int nwr = nt / CPW;
+      if constexpr (PAIRS) {  // channels (2dp, 2dp+1): one 32-bit load per token, two words
+        constexpr int DP = DT / 2;
+        const __half2* xs2 = reinterpret_cast<const __half2*>(xs);
+        for (int i = threadIdx.x; i < DP * nwr; i += blockDim.x) {
+          const int dp = i % DP, j = i / DP;
+          __half2 hv[CPW];  // (kept packed: 16 registers for the two words' inputs)
+#pragma unroll
+          for (int k = 0; k < CPW; ++k) hv[k] = xs2[(j * CPW + k) * DP + dp];
+          const int g = (j * CPW) / gs;
+          const uint2 m = *reinterpret_cast<const uint2*>(&ms[g * D + 2 * dp]);
+          const size_t w = (((size_t)bh * D + 2 * dp) * (size_t)T_ + t0) / CPW + j;
+          words[w] = encode_word_g<BITS, CPW, false>([&](int k) { return __low2float(hv[k]); }, meta_scale(m.x),
+                                                     meta_min(m.x), q_max);
+          words[w + (size_t)T_ / CPW] = encode_word_g<BITS, CPW, false>([&](int k) { return __high2float(hv[k]); },
+                                                                     meta_scale(m.y), meta_min(m.y), q_max);
+        }
+        return;
+      }
       for (int i = threadIdx.x; i < D * nwr; i += blockDim.x) {
         const int d = i % D, j = i / D;  // a warp reads 32 consecutive channels of a token row
         float v[CPW];
 #pragma unroll
         for (int k = 0; k < CPW; ++k) v[k] = ld_f(&xs[(j * CPW + k) * D + d]);
-        const uint32_t m = ms[d * gst + (j * CPW) / gs];
+        const uint32_t m = ms[(j * CPW) / gs * D + d];
         const size_t w = (((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j;
         words[w] = encode_word<BITS, CPW, !std::is_same<T, __half>::value>(v, meta_scale(m), meta_min(m), q_max);
       }
@@ -294,7 +349,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       if (gs >= 11 && p0 + 11 <= s1) {  // interior Mixed3 word: <= two groups, slot 10 narrow
         const int tt0 = (int)(p0 - s0);
         const int j0 = tt0 / gs, kb = (j0 + 1) * gs - tt0;  // first code of group j0 + 1
-        const uint32_t ma = ms[d * gst + j0], mb = kb < 11 ? ms[d * gst + j0 + 1] : ma;
+        const uint32_t ma = ms[j0 * D + d], mb = kb < 11 ? ms[(j0 + 1) * D + d] : ma;
         float xv[11];
 #pragma unroll
         for (int k = 0; k < 11; ++k) xv[k] = ld_f(&xs[(tt0 + k) * D + d]);
@@ -306,7 +361,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
     int tt = (int)(p0 - s0);                                    // token of the first code
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;                  // stream index mod 11
     int g = tt / gs, gend = (g + 1) * gs;                       // current group and its end
-    uint32_t m = ms[d * gst + g];
+    uint32_t m = ms[g * D + d];
     float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
     float ws = 0.f, rcw = 0.f;  // Mixed3 narrow slots: wide scale and its reciprocal
     if (bits == 3) {
@@ -318,7 +373,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
       if (tt == gend) {
         ++g;
         gend += gs;
-        m = ms[d * gst + g];
+        m = ms[g * D + d];
         sc = meta_scale(m);
         mnv = meta_min(m);
         rc = rcp_approx(sc);
@@ -335,7 +390,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_key_kernel(const T* __rest
     if (ext && k < cpw) {  // codes of the next run: its first group, staged at rows nt ..
       const int dn = next_span ? d : d + 1;
       if (dn < D) {
-        const uint32_t m2 = ms[dn * gst + gpt];
+        const uint32_t m2 = ms[gpt * D + dn];
         const float s2 = meta_scale(m2), n2 = meta_min(m2);
         for (int r = 0; k < cpw && p0 + k < n_total; ++k, ++r)
           word |= encode(ld_f(&xs[(nt + r) * D + dn]), s2, n2, bits, is_narrow(bits, p0 + k)) << field_shift(bits, (uint32_t)k);
@@ -760,20 +815,29 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     dim3 grid((T + n_tok - 1) / n_tok, B * H);
     auto go = [&](auto kern, const auto* xp) {
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      // the whole unified L1 as shared memory: as many staged tiles per SM as fit (the tile
+      // loads of resident CTAs are what keeps HBM busy; L1 caching does not help here)
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
       kern<<<grid, kQThreads, smem, st>>>(xp, H, T, D, bits, gs, n_tok, vec, words, m32, n);
     };
     const float* xf = static_cast<const float*>(x);
     const __half* xh = static_cast<const __half*>(x);
     if (dt == KVMIX_F32) {
-      if (bits == 1) go(quantize_key_kernel<float, 1>, xf);
-      else if (bits == 2) go(quantize_key_kernel<float, 2>, xf);
-      else if (bits == 3) go(quantize_key_kernel<float, 3>, xf);
-      else go(quantize_key_kernel<float, 4>, xf);
+      if (bits == 1) go(quantize_key_kernel<float, 1, 0>, xf);
+      else if (bits == 2) go(quantize_key_kernel<float, 2, 0>, xf);
+      else if (bits == 3) go(quantize_key_kernel<float, 3, 0>, xf);
+      else go(quantize_key_kernel<float, 4, 0>, xf);
     } else {
-      if (bits == 1) go(quantize_key_kernel<__half, 1>, xh);
-      else if (bits == 2) go(quantize_key_kernel<__half, 2>, xh);
-      else if (bits == 3) go(quantize_key_kernel<__half, 3>, xh);
-      else go(quantize_key_kernel<__half, 4>, xh);
+      // the common head_dims at compile time (fp16, 16-byte aligned rows: channel pairs)
+#define KVB_QK_H(DD)                                                   \
+      if (bits == 1) go(quantize_key_kernel<__half, 1, DD>, xh);       \
+      else if (bits == 2) go(quantize_key_kernel<__half, 2, DD>, xh);  \
+      else if (bits == 3) go(quantize_key_kernel<__half, 3, DD>, xh);  \
+      else go(quantize_key_kernel<__half, 4, DD>, xh);
+      if (vec && D == 128) { KVB_QK_H(128) }
+      else if (vec && D == 64) { KVB_QK_H(64) }
+      else { KVB_QK_H(0) }
+#undef KVB_QK_H
     }
     after_launch("quantize_key_kernel");
   } else if (bits != 3 && vec && D % gs == 0 && gs % (32 / bits) == 0 && gs / (32 / bits) <= 32 &&
@@ -802,6 +866,9 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     const size_t smem = (size_t)kM3Warps * (11 * gs + 44) * 4;
     auto go = [&](auto kern, const auto* xp) {
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      // the whole unified L1 as shared memory: as many staged tiles per SM as fit (the tile
+      // loads of resident CTAs are what keeps HBM busy; L1 caching does not help here)
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
       kern<<<grid, kM3Warps * 32, smem, st>>>(xp, n, words, m32);
     };
     const float* xf = static_cast<const float*>(x);
@@ -827,6 +894,9 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     const unsigned grid = (unsigned)((rows + R - 1) / R);
     auto go = [&](auto kern, const auto* xp) {
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      // the whole unified L1 as shared memory: as many staged tiles per SM as fit (the tile
+      // loads of resident CTAs are what keeps HBM busy; L1 caching does not help here)
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
       kern<<<grid, kQThreads, smem, st>>>(xp, rows, D, bits, gs, R, vec, words, m32);
     };
     const float* xf = static_cast<const float*>(x);
