@@ -174,13 +174,18 @@ kvmix_status kvmix_attend(const kvmix_cache* cache, const void* q, kvmix_dtype d
 kvmix_status kvmix_append_attend(kvmix_cache* cache, const void* k, const void* v, kvmix_dtype kv_dtype, int t,
                                  const void* q, kvmix_dtype q_dtype, int q_heads, int tq, float* out,
                                  double* checksum, void* stream);
-/* attend over several layers' caches in one call: q[l], out[l] per layer. */
+/* attend over several layers' caches in one call: q[l], out[l] per layer. Results equal
+ * n_layers kvmix_attend calls in order. Layers served by the same IMMA kernel instance share
+ * ONE launch (attend_mma_layers_kernel) when the caches are distinct, on one device, of one
+ * shape, and no out[l] overlaps another out[] or any q[]; otherwise one launch per layer. */
 kvmix_status kvmix_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* q,
                                  kvmix_dtype dtype, int q_heads, int t, float* const* out,
                                  void* stream);
 /* One decode step of a model stack in one call: kvmix_append_attend for every layer l
  * (k[l], v[l], q[l], out[l]) in order on `stream` -- the per-layer CachedDecoder::step pairs
- * (toymodel.cpp:720-721, 746) without a host round trip per layer. No checksum. */
+ * (toymodel.cpp:720-721, 746) without a host round trip per layer. No checksum. Same shared
+ * launch rule as kvmix_attend_layers (out[] must also not overlap k[] / v[]); the caches
+ * after the call are bit-identical either way, the outputs equal up to fp32 merge order. */
 kvmix_status kvmix_append_attend_layers(kvmix_cache* const* caches, int n_layers, const void* const* k,
                                         const void* const* v, kvmix_dtype kv_dtype, int t, const void* const* q,
                                         kvmix_dtype q_dtype, int q_heads, int tq, float* const* out, void* stream);
