@@ -108,3 +108,53 @@ def test_config3_llama2_13b_128k_slice(cuda):
     worst = _run_shape(2, 2, 0.1, 1, 40, 1, 131072, samples=[(0, 0), (0, 22)], n_decode=40, checks=(39,),
                        seed=30, chunk=16384)
     print(f"configs[3] slice: worst err/max|V| = {worst:.2e}")
+
+
+@pytest.mark.parametrize("G,ctx,B,H", [(1, 8192, 16, 32), (4, 32768, 8, 8)])
+def test_shared_layer_launch_at_bench_shapes(cuda, G, ctx, B, H):
+    """The bench's own path (kvmix_append_attend_layers: one attend_mma_layers_kernel launch
+    per tier run) at the configs[1] / configs[2] shapes: a 4-layer stack (K3V4, K3V4, K2V2,
+    K2V2) through 40 decode steps across a Key-group age-out; sampled (layer, b, kv-head)
+    outputs vs fp64 attention over the device's bit-exact snapshot (pinned against the
+    oracle by the tests above), within 2e-6 * max|V|."""
+    from paper_2506_08018_b200 import _lib
+    D, gs, n_decode = 128, 32, 40
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(7 + G)
+    tiers = [(3, 4, 0.2), (3, 4, 0.2), (2, 2, 0.1), (2, 2, 0.1)]
+    caches = []
+    for kb, vb, r in tiers:
+        c = K.KVLayerCache(K.LayerQuantConfig(0, kb, vb, r, r, gs), B, H, D, capacity_tokens=ctx + 8,
+                           tail_dtype=torch.float16)
+        for a in range(0, ctx - n_decode, 8192):
+            t = min(8192, ctx - n_decode - a)
+            c.append(torch.randn(B, H, t, D, device=dev, dtype=torch.float16, generator=gen),
+                     torch.randn(B, H, t, D, device=dev, dtype=torch.float16, generator=gen))
+        caches.append(c)
+    L = len(caches)
+    n0 = _lib.launch_count_of("attend_mma_layers_kernel")
+    qk0 = caches[-1].quantized_key_tokens()
+    samples = [(0, 0), (B // 2, H // 3), (B - 1, H - 1)]
+    worst = 0.0
+    for s in range(n_decode):
+        ks = [torch.randn(B, H, 1, D, device=dev, dtype=torch.float16, generator=gen) for _ in range(L)]
+        vs = [torch.randn(B, H, 1, D, device=dev, dtype=torch.float16, generator=gen) for _ in range(L)]
+        qs = [torch.randn(B, H * G, 1, D, device=dev, dtype=torch.float16, generator=gen) for _ in range(L)]
+        outs = [torch.empty(B, H * G, 1, D, device=dev) for _ in range(L)]
+        K.append_attend_layers(caches, ks, vs, qs, outs)
+        if s in (19, 39):
+            for l, c in enumerate(caches):
+                kd, vd = c.snapshot_dequantized()
+                for b, h in samples:
+                    kk = kd[b, h].cpu().numpy()
+                    vv = vd[b, h].cpu().numpy()
+                    qq = qs[l][b, h * G:(h + 1) * G, 0].float().cpu().numpy()
+                    o64, _ = O.attend_f64(qq[None, None], kk[None, None], vv[None, None])
+                    err = float(np.abs(outs[l][b, h * G:(h + 1) * G, 0].cpu().numpy() - o64[0, 0]).max()
+                                / np.abs(vv).max())
+                    worst = max(worst, err)
+                    assert err <= TOL, (l, b, h, s, err)
+                del kd, vd
+    assert _lib.launch_count_of("attend_mma_layers_kernel") - n0 == 2 * n_decode  # one per tier run
+    assert caches[-1].quantized_key_tokens() > qk0
+    print(f"shared launch G={G}: worst err/max|V| = {worst:.2e}")
