@@ -38,8 +38,7 @@ struct Vec;
 template <>
 struct Vec<__half> {
   static constexpr int N = 8;
-  __device__ static void load(const __half* p, float* o) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  __device__ static void unpack(const uint4& v, float* o) {
     const __half2* h = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -48,17 +47,18 @@ struct Vec<__half> {
       o[2 * i + 1] = f.y;
     }
   }
+  __device__ static void load(const __half* p, float* o) { unpack(__ldg(reinterpret_cast<const uint4*>(p)), o); }
 };
 template <>
 struct Vec<float> {
   static constexpr int N = 4;
-  __device__ static void load(const float* p, float* o) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-    o[0] = v.x;
-    o[1] = v.y;
-    o[2] = v.z;
-    o[3] = v.w;
+  __device__ static void unpack(const uint4& v, float* o) {
+    o[0] = __uint_as_float(v.x);
+    o[1] = __uint_as_float(v.y);
+    o[2] = __uint_as_float(v.z);
+    o[3] = __uint_as_float(v.w);
   }
+  __device__ static void load(const float* p, float* o) { unpack(__ldg(reinterpret_cast<const uint4*>(p)), o); }
 };
 
 // One uniform 1/2/4-bit word of CPW codes sharing a group's (scale, min), bit-exact with
@@ -231,9 +231,21 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
   const bool next_span = t0 + nt < T_;
 
   auto stage = [&](T* dst, const T* from, int rows) {
-    if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked): raw 16-byte copies
-      for (int i = threadIdx.x; i < rows * D / Vec<T>::N; i += blockDim.x)
-        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(from) + i);
+    if (vec) {  // D % N == 0 and a 16-byte aligned input (host-checked): raw 16-byte copies,
+                // 8 loads in flight per thread before the stores (one DRAM latency per batch)
+      const int n16 = rows * D / Vec<T>::N;
+      const uint4* s4 = reinterpret_cast<const uint4*>(from);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      const int nb = blockDim.x;
+      int i = threadIdx.x;
+      for (; i + 7 * nb < n16; i += 8 * nb) {
+        uint4 r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = __ldg(s4 + i + u * nb);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d4[i + u * nb] = r[u];
+      }
+      for (; i < n16; i += nb) d4[i] = __ldg(s4 + i);
     } else {
       for (int i = threadIdx.x; i < rows * D; i += blockDim.x) dst[i] = from[i];
     }
@@ -640,11 +652,22 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
   const int ne = (int)min((size_t)CE, n - e0);  // a multiple of gs (n % gs == 0)
   // stage (fp32 in shared memory)
   if (ne == CE && (reinterpret_cast<uintptr_t>(x + e0) & 15) == 0) {
-    for (int i = lane; i < CE / Vec<T>::N; i += 32) {
-      float v[Vec<T>::N];
-      Vec<T>::load(x + e0 + (size_t)i * Vec<T>::N, v);
+    // every 16-byte load of the chunk in flight before the first store (one DRAM latency)
+    constexpr int NV = CE / Vec<T>::N, PER = (NV + 31) / 32;
+    uint4 r[PER];
+    const uint4* s4 = reinterpret_cast<const uint4*>(x + e0);
 #pragma unroll
-      for (int k = 0; k < Vec<T>::N; ++k) xs[i * Vec<T>::N + k] = v[k];
+    for (int u = 0; u < PER; ++u)
+      if (lane + 32 * u < NV) r[u] = __ldg(s4 + lane + 32 * u);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = lane + 32 * u;
+      if (i < NV) {
+        float v[Vec<T>::N];
+        Vec<T>::unpack(r[u], v);
+#pragma unroll
+        for (int k = 0; k < Vec<T>::N; ++k) xs[i * Vec<T>::N + k] = v[k];
+      }
     }
   } else {
     for (int i = lane; i < ne; i += 32) xs[i] = ld_f(x + e0 + i);
