@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
       const int nwr = nt / CPW;
       if constexpr (PAIRS) {  // channels (2dp, 2dp+1): one 32-bit load per token, two words
         constexpr int DP = DT / 2;
+        uint32_t* ow = ms + (size_t)gst * D;  // the tile's words [D][nwr + 1]
         const __half2* xs2 = reinterpret_cast<const __half2*>(xs);
         for (int i = threadIdx.x; i < DP * nwr; i += blockDim.x) {
           const int dp = i % DP, j = i / DP;
@@ -322,10 +323,18 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
           const int g = (j * CPW) / gs;
           const uint2 m = *reinterpret_cast<const uint2*>(&ms[g * D + 2 * dp]);
           const size_t w = (((size_t)bh * D + 2 * dp) * (size_t)T_ + t0) / CPW + j;
-          words[w] = encode_word_g<BITS, CPW, false>([&](int k) { return __low2float(hv[k]); }, meta_scale(m.x),
-                                                     meta_min(m.x), q_max);
-          words[w + (size_t)T_ / CPW] = encode_word_g<BITS, CPW, false>([&](int k) { return __high2float(hv[k]); },
-                                                                     meta_scale(m.y), meta_min(m.y), q_max);
+          (void)w;
+          ow[(2 * dp) * (nwr + 1) + j] = encode_word_g<BITS, CPW, false>([&](int k) { return __low2float(hv[k]); },
+                                                                       meta_scale(m.x), meta_min(m.x), q_max);
+          ow[(2 * dp + 1) * (nwr + 1) + j] = encode_word_g<BITS, CPW, false>(
+              [&](int k) { return __high2float(hv[k]); }, meta_scale(m.y), meta_min(m.y), q_max);
+        }
+        // the tile's words leave channel by channel: a channel's run of nwr words is written by
+        // consecutive threads (whole sectors per store instead of one word per channel row)
+        __syncthreads();
+        for (int i = threadIdx.x; i < D * nwr; i += blockDim.x) {
+          const int d = i / nwr, j = i - d * nwr;
+          words[(((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j] = ow[d * (nwr + 1) + j];
         }
         return;
       }
@@ -365,8 +374,8 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
         float xv[11];
 #pragma unroll
         for (int k = 0; k < 11; ++k) xv[k] = ld_f(&xs[(tt0 + k) * D + d]);
-        words[w] = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, meta_scale(ma), meta_min(ma), meta_scale(mb),
-                                                                   meta_min(mb));
+        words[w] = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, meta_scale(ma), meta_min(ma),
+                                                                   meta_scale(mb), meta_min(mb));
         continue;
       }
     }
@@ -825,11 +834,20 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
   const int max_smem = 96 * 1024;
   if (grouping == KVMIX_PER_CHANNEL_KEY) {
     // tile of k groups of gs tokens: aim for ~128 tokens, bounded by shared memory
-    int k = std::max(1, 128 / gs);
+    // uniform 1/2/4-bit words: 64-token tiles of 128 threads (more, smaller CTAs per SM, so
+    // one CTA's fold / encode phases overlap other CTAs' tile loads); Mixed3 keeps 128-token
+    // tiles (its next-group staging costs gs tokens per tile)
+    // (KVMIX_QK_TOK / KVMIX_QK_THREADS: A/B overrides, read once)
+    static const int env_tok = getenv("KVMIX_QK_TOK") ? std::max(8, atoi(getenv("KVMIX_QK_TOK"))) : 0;
+    static const int env_thr = getenv("KVMIX_QK_THREADS") ? std::min(kQThreads, std::max(32, atoi(getenv("KVMIX_QK_THREADS")))) : 0;
+    const int qk_tok = env_tok ? env_tok : (bits == 3 ? 128 : 64);
+    const int qk_threads = env_thr ? env_thr : (bits == 3 ? kQThreads : 128);
+    int k = std::max(1, qk_tok / gs);
     const size_t esz = dt == KVMIX_F16 ? 2 : 4;  // staged in the input type
     const int ext = (bits == 3 && gs >= 11) ? 1 : 0;  // + the next run's first group (kernel)
-    auto smem_of = [&](int kk) {
-      return ((size_t)(kk + ext) * gs * D * esz + 15) / 16 * 16 + (size_t)D * (kk + ext) * 4;
+    auto smem_of = [&](int kk) {  // tile + group meta (+ the words of a uniform-bit tile)
+      const size_t ow = bits == 3 ? 0 : (size_t)D * ((size_t)kk * gs / (32 / bits) + 1) * 4;
+      return ((size_t)(kk + ext) * gs * D * esz + 15) / 16 * 16 + (size_t)D * (kk + ext) * 4 + ow;
     };
     while (k > 1 && smem_of(k) > (size_t)max_smem) --k;
     if (smem_of(k) > (size_t)227 * 1024) invalid("quantize: group_size * head_dim too large for one tile");
@@ -841,7 +859,7 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
       // the whole unified L1 as shared memory: as many staged tiles per SM as fit (the tile
       // loads of resident CTAs are what keeps HBM busy; L1 caching does not help here)
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-      kern<<<grid, kQThreads, smem, st>>>(xp, H, T, D, bits, gs, n_tok, vec, words, m32, n);
+      kern<<<grid, qk_threads, smem, st>>>(xp, H, T, D, bits, gs, n_tok, vec, words, m32, n);
     };
     const float* xf = static_cast<const float*>(x);
     const __half* xh = static_cast<const __half*>(x);
