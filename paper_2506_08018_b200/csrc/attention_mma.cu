@@ -1483,6 +1483,10 @@ void attend_layers(kvmix_cache* const* caches, int n, const void* const* k, cons
     gr->bh.push_back(g.BH);
     return true;
   };
+  // a layer that raises (shape / capacity errors) leaves the layers before it complete, as
+  // the per-layer loop does: their queued launches (which hold their committed appends) run
+  // before the error propagates
+  try {
   for (int l = 0; l < n; ++l) {
     kvmix_cache* c = caches[l];
     if (k) {
@@ -1503,6 +1507,10 @@ void attend_layers(kvmix_cache* const* caches, int n, const void* const* k, cons
     if (try_add(c, q[l], out[l], nullptr)) continue;
     Workspace ws(st);
     attend(c, q[l], q_dt, Hq, tq, out[l], nullptr, ws, st);
+  }
+  } catch (...) {
+    for (Group& g : groups) flush(g);
+    throw;
   }
   for (Group& g : groups) flush(g);
 }

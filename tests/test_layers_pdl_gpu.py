@@ -120,3 +120,63 @@ def test_shared_launch_gqa_and_head_dims(cuda, G, D):
     b, db = go(0)
     assert da == db
     np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+def test_more_layers_than_one_launch_holds(cuda):
+    """34 same-tier layers: the shared launch holds at most 32 layers' parameters (kernel
+    parameter space), so the run splits into two launches; results == per-layer launches."""
+    B, H, D, L, pre = 2, 4, 128, 34, 300
+
+    def go(layers):
+        K.set_knob("KVMIX_LAYERS", layers)
+        torch.manual_seed(11)
+        caches = []
+        for _ in range(L):
+            c = K.KVLayerCache(K.LayerQuantConfig(0, 2, 2, 0.1, 0.1, 32), B, H, D, capacity_tokens=pre + 16,
+                               tail_dtype=torch.float16)
+            c.append(torch.randn(B, H, pre, D, device="cuda", dtype=torch.float16),
+                     torch.randn(B, H, pre, D, device="cuda", dtype=torch.float16))
+            caches.append(c)
+        g = torch.Generator(device="cuda").manual_seed(12)
+        res = []
+        for _ in range(4):
+            ks = [torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16, generator=g) for _ in range(L)]
+            vs = [torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16, generator=g) for _ in range(L)]
+            qs = [torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16, generator=g) for _ in range(L)]
+            outs = [torch.empty(B, H, 1, D, device="cuda") for _ in range(L)]
+            K.append_attend_layers(caches, ks, vs, qs, outs)
+            res.append(torch.stack(outs))
+        torch.cuda.synchronize()
+        K.set_knob("KVMIX_LAYERS", 1)
+        return torch.stack(res).cpu().numpy(), [c.dump() for c in caches]
+
+    n0 = _lib.launch_count_of("attend_mma_layers_kernel")
+    a, da = go(1)
+    assert _lib.launch_count_of("attend_mma_layers_kernel") - n0 == 2 * 4
+    b, db = go(0)
+    assert da == db
+    np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+def test_error_mid_stack_completes_earlier_layers(cuda):
+    """A layer that raises (here: capacity exhausted) propagates the error; the layers
+    before it are appended and attended as by the per-layer loop (their queued shared
+    launch runs first)."""
+    B, H, D, pre = 2, 4, 128, 200
+    caches = []
+    for cap in (pre + 8, pre + 8, pre):  # the third cache is full
+        c = K.KVLayerCache(K.LayerQuantConfig(0, 2, 2, 0.1, 0.1, 32), B, H, D, capacity_tokens=cap,
+                           tail_dtype=torch.float16)
+        c.append(torch.randn(B, H, pre, D, device="cuda", dtype=torch.float16),
+                 torch.randn(B, H, pre, D, device="cuda", dtype=torch.float16))
+        caches.append(c)
+    ks = [torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16) for _ in range(3)]
+    qs = [torch.randn(B, H, 1, D, device="cuda", dtype=torch.float16) for _ in range(3)]
+    outs = [torch.full((B, H, 1, D), float("nan"), device="cuda") for _ in range(3)]
+    with pytest.raises(Exception):
+        K.append_attend_layers(caches, ks, ks, qs, outs)
+    torch.cuda.synchronize()
+    assert [c.total_tokens() for c in caches[:2]] == [pre + 1, pre + 1]
+    for l in range(2):  # earlier layers: appended and attended
+        ref = K.attend(qs[l], caches[l]).output
+        np.testing.assert_allclose(outs[l].cpu().numpy(), ref.cpu().numpy(), rtol=1e-5, atol=1e-6)
