@@ -71,6 +71,7 @@ Knobs& knobs() {
     x.tc = iv("KVMIX_TC", 0, 1, 0);
     x.pdl = iv("KVMIX_PDL", 0, 1, 1);
     x.layers = iv("KVMIX_LAYERS", 0, 1, 1);
+    x.r4 = iv("KVMIX_R4", 0, 1, 1);
     x.skip_tail = getenv("KVMIX_PROF_SKIP_TAIL") != nullptr;
     x.no_window = getenv("KVMIX_PROF_NO_WINDOW") != nullptr;
     return x;
@@ -101,6 +102,7 @@ bool set_knob(const char* name, int v) {
   else if (n == "KVMIX_TC") k.tc = std::max(0, std::min(1, v));
   else if (n == "KVMIX_PDL") k.pdl = std::max(0, std::min(1, v));
   else if (n == "KVMIX_LAYERS") k.layers = std::max(0, std::min(1, v));
+  else if (n == "KVMIX_R4") k.r4 = std::max(0, std::min(1, v));
   else return false;
   return true;
 }
@@ -165,7 +167,8 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
   const bool want_cs = CS && p.want_cs;
   static_assert(D == 64 || D == 128, "IMMA attention handles D in {64, 128}");
   static_assert(VB == 2 || VB == 4, "Values: 2 or 4 bits");
-  static_assert(R == 1 || R == 2, "one or two query rows per KV head");
+  static_assert(R == 1 || R == 2 || R == 4, "one, two or four query rows per KV head");
+  constexpr int NT = R == 4 ? 2 : 1;           // IMMA n8 column tiles (two rows x four digits each)
   constexpr bool K3 = KB == 3;
   static_assert(!K3 || D == 128, "3-bit Keys: D = 128");
   constexpr int NK = D / 32;                   // Key k-steps (32 channels)
@@ -257,9 +260,12 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
   }
   __syncwarp();
 
-  // this lane's softmax row: lanes t = 2r, 2r+1 hold row r (IMMA score columns 4r .. 4r+3)
+  // this lane's softmax rows: in column tile nt, lanes t = 2r, 2r+1 hold row 2 nt + r (IMMA
+  // score columns 4r .. 4r+3 of the tile)
   const int my_r = t >> 1;
-  const bool row_ok = my_r < prows;
+  bool row_ok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) row_ok[nt] = 2 * nt + my_r < prows;
 
   // producer: this warp's fast groups in work-list order, issued S ahead of the consumer
   // (running record pointer, groups left in the current (b, kv-head), groups left to issue)
@@ -374,11 +380,18 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) qc[r][c] = qv[r][c] * clsL;
-    float m_run = -INFINITY, l_run = 0.f;  // row my_r (lazy reference max, log2 units)
-    if (want_cs) csm[lane] = 0.0;
-    int accv[NM][4];
+    float m_run[NT], l_run[NT];  // row 2 nt + my_r (lazy reference max, log2 units)
 #pragma unroll
-    for (int i = 0; i < NM; ++i) accv[i][0] = accv[i][1] = accv[i][2] = accv[i][3] = 0;
+    for (int nt = 0; nt < NT; ++nt) {
+      m_run[nt] = -INFINITY;
+      l_run[nt] = 0.f;
+    }
+    if (want_cs) csm[lane] = 0.0;
+    int accv[NT][NM][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < NM; ++i) accv[nt][i][0] = accv[nt][i][1] = accv[nt][i][2] = accv[nt][i][3] = 0;
     float bias[R];  // sum_j p_j m_jc of this lane's channel group cq = lane / 8 and token quads
 #pragma unroll
     for (int r = 0; r < R; ++r) bias[r] = 0.f;
@@ -392,30 +405,33 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
     __syncwarp();
 
     // Fold the int32 Value accumulators into s_acc (fp32): s_acc = (s_acc + acc 2^-E) alpha.
-    // Lane (g, t) holds digit columns 2t, 2t+1 (row t >> 1) of channels 16 mt + g (+8).
-    auto flush = [&](float alpha) {
+    // Lane (g, t) holds digit columns 2t, 2t+1 (row 2 nt + (t >> 1)) of channels 16 mt + g (+8).
+    auto flush = [&](const float (&alpha)[NT]) {
       const float w0 = pow2i(16 * (t & 1) - e_cur);
       const float w1 = w0 * 256.f;
 #pragma unroll
-      for (int mt = 0; mt < NM; ++mt) {
-        const float c0 = pow2i(-VB * (mt % CV)), c1 = pow2i(-VB * ((mt + NM) % CV));
-        float f0 = fmaf((float)accv[mt][1], w1, (float)accv[mt][0] * w0) * c0;
-        float f1 = fmaf((float)accv[mt][3], w1, (float)accv[mt][2] * w0) * c1;
-        f0 += __shfl_xor_sync(0xffffffffu, f0, 1);
-        f1 += __shfl_xor_sync(0xffffffffu, f1, 1);
-        if ((t & 1) == 0 && my_r < R) {
-          float* a = &s_acc[warp][my_r][16 * mt + g];
-          a[0] = (a[0] + f0) * alpha;  // accumulated with the old max
-          a[8] = (a[8] + f1) * alpha;
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < NM; ++mt) {
+          const float c0 = pow2i(-VB * (mt % CV)), c1 = pow2i(-VB * ((mt + NM) % CV));
+          float f0 = fmaf((float)accv[nt][mt][1], w1, (float)accv[nt][mt][0] * w0) * c0;
+          float f1 = fmaf((float)accv[nt][mt][3], w1, (float)accv[nt][mt][2] * w0) * c1;
+          f0 += __shfl_xor_sync(0xffffffffu, f0, 1);
+          f1 += __shfl_xor_sync(0xffffffffu, f1, 1);
+          if ((t & 1) == 0 && 2 * nt + my_r < R) {
+            float* a = &s_acc[warp][2 * nt + my_r][16 * mt + g];
+            a[0] = (a[0] + f0) * alpha[nt];  // accumulated with the old max
+            a[8] = (a[8] + f1) * alpha[nt];
+          }
+          accv[nt][mt][0] = accv[nt][mt][1] = accv[nt][mt][2] = accv[nt][mt][3] = 0;
         }
-        accv[mt][0] = accv[mt][1] = accv[mt][2] = accv[mt][3] = 0;
-      }
       nacc = 0;
     };
 
     // Value k-step of one 32-token block: lane (g, t) owns token j = g + 8t (p of it for every
     // row in pr); fixed-point exponent / fold bookkeeping, B digits, 8 IMMA.
-    auto value_block = [&](const uint32_t* vt2, const uint32_t* vm2, const float (&pr)[R], float alpha, int nvalid) {
+    auto value_block = [&](const uint32_t* vt2, const uint32_t* vm2, const float (&pr)[R], const float (&alpha)[NT],
+                           int nvalid) {
       // lane (cq, tq) = (lane / 8, lane % 8) handles channel group cq of tokens 4tq .. 4tq+3
       const int cq = lane >> 3, tq = lane & 7;
       const bool cg_ok = cq < CG;
@@ -437,13 +453,19 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
       if (!dirty) {
         e_cur = e_blk - kEHead;
       } else {
-        const bool moved = __any_sync(0xffffffffu, row_ok && alpha != 1.0f);
+        bool mv_lane = false;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mv_lane |= row_ok[nt] && alpha[nt] != 1.0f;
+        const bool moved = __any_sync(0xffffffffu, mv_lane);
         if (moved || e_cur > e_blk || nacc >= p.flush_blocks) {
           flush(alpha);
           if (moved) {
-            const float ax = __shfl_xor_sync(0xffffffffu, alpha, 2);
 #pragma unroll
-            for (int r = 0; r < R; ++r) bias[r] *= (r == my_r) ? alpha : ax;
+            for (int nt = 0; nt < NT; ++nt) {
+              const float ax = __shfl_xor_sync(0xffffffffu, alpha[nt], 2);
+#pragma unroll
+              for (int r = 2 * nt; r < 2 * nt + 2 && r < R; ++r) bias[r] *= (r - 2 * nt == my_r) ? alpha[nt] : ax;
+            }
           }
           e_cur = e_blk - kEHead;
         }
@@ -463,7 +485,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
           uint32_t uu[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) uu[i] = (uint32_t)__float2int_rn(pq[r][i] * pe * sv[i]);
-          store_digits(reinterpret_cast<uint32_t*>(vbs + cq * 256 + (4 * r) * 32 + pos), 8, uu);
+          store_digits(reinterpret_cast<uint32_t*>(vbs + cq * (256 * NT) + (4 * r) * 32 + pos), 8, uu);
         }
       }
       __syncwarp();
@@ -471,16 +493,18 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
         uint32_t vw0[VW], vw1[VW];
         lds_tile<D, VB>(vt2, lane, vw0);
         lds_tile<D, VB>(vt2 + tile_words(D, VB), lane, vw1);
-        uint32_t vb[CGMAX][2];
+        uint32_t vb[NT][CGMAX][2];
         if constexpr (GS != 0) {
 #pragma unroll
-          for (int c = 0; c < CGMAX; ++c) {
-            if (c < D / (GS ? GS : 1)) {
-              const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
-              vb[c][0] = x.x;
-              vb[c][1] = x.y;
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < CGMAX; ++c) {
+              if (c < D / (GS ? GS : 1)) {
+                const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * (256 * NT) + nt * 256 + g * 32 + 8 * t);
+                vb[nt][c][0] = x.x;
+                vb[nt][c][1] = x.y;
+              }
             }
-          }
         }
 #pragma unroll
         for (int mt = 0; mt < NM; ++mt) {
@@ -489,13 +513,16 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
           const uint32_t a1 = vw0[q1 / CV] & (VMASK << (VB * (q1 % CV)));
           const uint32_t a2 = vw1[q0 / CV] & (VMASK << (VB * (q0 % CV)));
           const uint32_t a3 = vw1[q1 / CV] & (VMASK << (VB * (q1 % CV)));
-          if constexpr (GS != 0) {
-            const int c = (mt * 16) / (GS ? GS : 1);
-            imma_uu(accv[mt], a0, a1, a2, a3, vb[c][0], vb[c][1]);
-          } else {
-            const int c = (mt * 16) / gs;
-            const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * 256 + g * 32 + 8 * t);
-            imma_uu(accv[mt], a0, a1, a2, a3, x.x, x.y);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            if constexpr (GS != 0) {
+              const int c = (mt * 16) / (GS ? GS : 1);
+              imma_uu(accv[nt][mt], a0, a1, a2, a3, vb[nt][c][0], vb[nt][c][1]);
+            } else {
+              const int c = (mt * 16) / gs;
+              const uint2 x = *reinterpret_cast<const uint2*>(vbs + c * (256 * NT) + nt * 256 + g * 32 + 8 * t);
+              imma_uu(accv[nt][mt], a0, a1, a2, a3, x.x, x.y);
+            }
           }
         }
       }
@@ -517,9 +544,9 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
       // add the high-bit plane's B = round(4 q s 2^-class_hi sigma) (same sigma, so both
       // planes accumulate into the same int32 scores) and the narrow-slot table
       // ytab[d] = q_d (wide_scale(s_d) - s_d) for the Mixed3 correction.
-      float betaL;       // sum_d q_d m_d of row my_r, scaled to log2 units
-      float wsc0;        // weight of this lane's score column pair (log2 units)
-      uint32_t kb[NK][2], kbh[K3 ? NK : 1][2];
+      float betaL[NT];   // sum_d q_d m_d of row 2 nt + my_r, scaled to log2 units
+      float wsc0[NT];    // weight of this lane's score column pair (log2 units)
+      uint32_t kb[NT][NK][2], kbh[NT][K3 ? NK : 1][2];
       int nmod = 0, omod = 0;  // 3-bit Keys: segment length / group offset mod 11
       {
         const uint4 m4 = *reinterpret_cast<const uint4*>(km + 4 * Lq);
@@ -580,41 +607,47 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
           beta[r] = bt;
         }
         __syncwarp();
-        // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column g (digit g%4 of row g/4)
-        {
-          const bool has_col = g < WL::kKC;
+        // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column 8 nt + g (digit g%4 of row
+        // (8 nt + g)/4)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int col = 8 * nt + g;
+          const bool has_col = col < WL::kKC;
           const uint32_t* zsrc = reinterpret_cast<const uint32_t*>(kstage + WL::kZ) + t * (2 * NK);
-          const uint32_t* src = has_col ? kbs + (g * 4 + t) * (2 * NK) : zsrc;
+          const uint32_t* src = has_col ? kbs + (col * 4 + t) * (2 * NK) : zsrc;
 #pragma unroll
           for (int kk = 0; kk < NK; kk += 2) {
             const uint4 v = *reinterpret_cast<const uint4*>(src + 2 * kk);
-            kb[kk][0] = v.x;
-            kb[kk][1] = v.y;
-            kb[kk + 1][0] = v.z;
-            kb[kk + 1][1] = v.w;
+            kb[nt][kk][0] = v.x;
+            kb[nt][kk][1] = v.y;
+            kb[nt][kk + 1][0] = v.z;
+            kb[nt][kk + 1][1] = v.w;
           }
           if constexpr (K3) {
 #pragma unroll
             for (int kk = 0; kk < NK; kk += 2) {
               const uint32_t* srch = has_col ? src + WL::kKC * 4 * 2 * NK : zsrc;
               const uint4 v = *reinterpret_cast<const uint4*>(srch + 2 * kk);
-              kbh[kk][0] = v.x;
-              kbh[kk][1] = v.y;
-              kbh[kk + 1][0] = v.z;
-              kbh[kk + 1][1] = v.w;
+              kbh[nt][kk][0] = v.x;
+              kbh[nt][kk][1] = v.y;
+              kbh[nt][kk + 1][0] = v.z;
+              kbh[nt][kk + 1][1] = v.w;
             }
           }
         }
-        const int rr = my_r < R ? my_r : 0;
-        float is = isig[0], bb = beta[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r)
-          if (rr == r) {
-            is = isig[r];
-            bb = beta[r];
-          }
-        wsc0 = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
-        betaL = bb * p.inv * kLog2e;
+        for (int nt = 0; nt < NT; ++nt) {
+          const int rr = 2 * nt + my_r < R ? 2 * nt + my_r : 0;
+          float is = isig[0], bb = beta[0];
+#pragma unroll
+          for (int r = 1; r < R; ++r)
+            if (rr == r) {
+              is = isig[r];
+              bb = beta[r];
+            }
+          wsc0[nt] = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
+          betaL[nt] = bb * p.inv * kLog2e;
+        }
       }
 
       // ---- the group's 32-token blocks: 2 Key tiles + one Value k-step each ---------------
@@ -622,14 +655,16 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
         const uint32_t* kt2 = kt + (size_t)(2 * blk) * tile_words(D, KB);
         const uint32_t* vt2 = vt + (size_t)(2 * blk) * tile_words(D, VB);
         const uint32_t* vm2 = vm + 32 * blk;  // V meta [cg][gs]
-        float la[2], lb[2];  // scores (log2 units) of tokens g / g+8 of tile u, row my_r
+        float la[NT][2], lb[NT][2];  // scores (log2 units) of tokens g / g+8 of tile u, row 2 nt + my_r
         {
           uint32_t kw[2][KW];
           lds_tile<D, KB>(kt2, lane, kw[0]);
           lds_tile<D, KB>(kt2 + tile_words(D, KB), lane, kw[1]);
-          int dk[2][4];
+          int dk[NT][2][4];
 #pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) dk[u2][0] = dk[u2][1] = dk[u2][2] = dk[u2][3] = 0;
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int u2 = 0; u2 < 2; ++u2) dk[nt][u2][0] = dk[nt][u2][1] = dk[nt][u2][2] = dk[nt][u2][3] = 0;
 #pragma unroll
           for (int kk = 0; kk < NK; ++kk) {
             const int q0 = kk, q1 = kk + NK;  // channel halves h = 0 / 1
@@ -639,18 +674,22 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
               const uint32_t a1 = kw[u2][(q0 / CK) * 2 + 1] & (KMASK << (KB2 * (q0 % CK)));
               const uint32_t a2 = kw[u2][(q1 / CK) * 2 + 0] & (KMASK << (KB2 * (q1 % CK)));
               const uint32_t a3 = kw[u2][(q1 / CK) * 2 + 1] & (KMASK << (KB2 * (q1 % CK)));
-              imma_us(dk[u2], a0, a1, a2, a3, kb[kk][0], kb[kk][1]);
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) imma_us(dk[nt][u2], a0, a1, a2, a3, kb[nt][kk][0], kb[nt][kk][1]);
               if constexpr (K3) {  // high-bit plane: words (q + 2 NK rb) / 8, class q (D = 128)
                 constexpr int HW = D * 2 / 64;  // first word of the 1-bit plane
                 const uint32_t h0 = kw[u2][HW + 0] & (0x01010101u << q0);
                 const uint32_t h1 = kw[u2][HW + 1] & (0x01010101u << q0);
                 const uint32_t h2 = kw[u2][HW + 0] & (0x01010101u << q1);
                 const uint32_t h3 = kw[u2][HW + 1] & (0x01010101u << q1);
-                imma_us(dk[u2], h0, h1, h2, h3, kbh[kk][0], kbh[kk][1]);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) imma_us(dk[nt][u2], h0, h1, h2, h3, kbh[nt][kk][0], kbh[nt][kk][1]);
               }
             }
           }
-          float corr[4] = {0.f, 0.f, 0.f, 0.f};  // Mixed3 narrow corrections of tokens g, g+8, 16+g, 24+g
+          float corr[NT][4];  // Mixed3 narrow corrections of tokens g, g+8, 16+g, 24+g (row 2 nt + my_r)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) corr[nt][0] = corr[nt][1] = corr[nt][2] = corr[nt][3] = 0.f;
           float fac[4] = {1.f, 1.f, 1.f, 1.f};
           if constexpr (K3) {
             // lane (g, t) corrects token jt = g + 8t of the block: narrow channels d = d0 + 11k
@@ -676,14 +715,16 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
             }
             const float wsn = p.inv * kLog2e;
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {  // row my_r of token g + 8x (lane 4g + x made it)
-              float c = __shfl_sync(0xffffffffu, dlt[0], 4 * g + x);
-              if constexpr (R == 2) {
-                const float c1 = __shfl_sync(0xffffffffu, dlt[1], 4 * g + x);
-                c = my_r ? c1 : c;
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {  // row 2 nt + my_r of token g + 8x (lane 4g + x made it)
+                float c = __shfl_sync(0xffffffffu, dlt[2 * nt], 4 * g + x);
+                if constexpr (R >= 2) {
+                  const float c1 = __shfl_sync(0xffffffffu, dlt[2 * nt + 1], 4 * g + x);
+                  c = my_r ? c1 : c;
+                }
+                corr[nt][x] = c * wsn;
               }
-              corr[x] = c * wsn;
-            }
             if (nmod == 0) {  // every channel of the tokens with (omod + tg) % 11 == 10 is narrow
 #pragma unroll
               for (int x = 0; x < 4; ++x) {
@@ -693,42 +734,52 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
             }
           }
 #pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            // digits n0, n0+1 of this lane's columns: dk0 + 256 dk1 fits int32 (|dk| < 2^23)
-            float pa = (float)(dk[u2][0] + (dk[u2][1] << 8)) * wsc0;
-            float pb = (float)(dk[u2][2] + (dk[u2][3] << 8)) * wsc0;
-            pa += __shfl_xor_sync(0xffffffffu, pa, 1);
-            pb += __shfl_xor_sync(0xffffffffu, pb, 1);
-            la[u2] = fmaf(pa, fac[2 * u2], betaL) + corr[2 * u2];
-            lb[u2] = fmaf(pb, fac[2 * u2 + 1], betaL) + corr[2 * u2 + 1];
-          }
-        }
-        if (want_cs && row_ok && (t & 1) == 0) csm[lane] += (double)(((la[0] + lb[0]) + (la[1] + lb[1])) * kLn2);
-
-        // ---- online softmax (row my_r) -----------------------------------------------------
-        float tmax = fmaxf(fmaxf(la[0], lb[0]), fmaxf(la[1], lb[1]));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-        const float m_new = tmax > m_run + (float)kLazy ? tmax : m_run;
-        const float alpha = fast_exp2(m_run - m_new);
-        float pa[2], pb[2];
+          for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int u2 = 0; u2 < 2; ++u2) {
-          pa[u2] = row_ok ? fast_exp2(la[u2] - m_new) : 0.f;
-          pb[u2] = row_ok ? fast_exp2(lb[u2] - m_new) : 0.f;
+            for (int u2 = 0; u2 < 2; ++u2) {
+              // digits n0, n0+1 of this lane's columns: dk0 + 256 dk1 fits int32 (|dk| < 2^23)
+              float pa = (float)(dk[nt][u2][0] + (dk[nt][u2][1] << 8)) * wsc0[nt];
+              float pb = (float)(dk[nt][u2][2] + (dk[nt][u2][3] << 8)) * wsc0[nt];
+              pa += __shfl_xor_sync(0xffffffffu, pa, 1);
+              pb += __shfl_xor_sync(0xffffffffu, pb, 1);
+              la[nt][u2] = fmaf(pa, fac[2 * u2], betaL[nt]) + corr[nt][2 * u2];
+              lb[nt][u2] = fmaf(pb, fac[2 * u2 + 1], betaL[nt]) + corr[nt][2 * u2 + 1];
+            }
         }
-        l_run = l_run * alpha + ((pa[0] + pb[0]) + (pa[1] + pb[1]));
-        m_run = m_new;
+        if (want_cs && (t & 1) == 0) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            if (row_ok[nt]) csm[lane] += (double)(((la[nt][0] + lb[nt][0]) + (la[nt][1] + lb[nt][1])) * kLn2);
+        }
+
+        // ---- online softmax (rows 2 nt + my_r) ---------------------------------------------
+        float alpha[NT], pa[NT][2], pb[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          float tmax = fmaxf(fmaxf(la[nt][0], lb[nt][0]), fmaxf(la[nt][1], lb[nt][1]));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+          const float m_new = tmax > m_run[nt] + (float)kLazy ? tmax : m_run[nt];
+          alpha[nt] = fast_exp2(m_run[nt] - m_new);
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            pa[nt][u2] = row_ok[nt] ? fast_exp2(la[nt][u2] - m_new) : 0.f;
+            pb[nt][u2] = row_ok[nt] ? fast_exp2(lb[nt][u2] - m_new) : 0.f;
+          }
+          l_run[nt] = l_run[nt] * alpha[nt] + ((pa[nt][0] + pb[nt][0]) + (pa[nt][1] + pb[nt][1]));
+          m_run[nt] = m_new;
+        }
 
         // ---- Value block: lane (g, t) owns token g + 8t of the 32 -------------------------
         float pr[R];  // p of token j for every row
-        {
-          const float mine = (t & 1) ? ((t >> 1) ? pb[1] : pb[0]) : ((t >> 1) ? pa[1] : pa[0]);
-          const float other = (t & 1) ? ((t >> 1) ? pb[0] : pb[1]) : ((t >> 1) ? pa[0] : pa[1]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const float mine = (t & 1) ? ((t >> 1) ? pb[nt][1] : pb[nt][0]) : ((t >> 1) ? pa[nt][1] : pa[nt][0]);
+          const float other = (t & 1) ? ((t >> 1) ? pb[nt][0] : pb[nt][1]) : ((t >> 1) ? pa[nt][0] : pa[nt][1]);
           const float recv = __shfl_xor_sync(0xffffffffu, other, 2);  // partner t^2's token, my row
 #pragma unroll
-          for (int r = 0; r < R; ++r) pr[r] = (r == my_r) ? mine : recv;
+          for (int r = 2 * nt; r < 2 * nt + 2 && r < R; ++r) pr[r] = (r - 2 * nt == my_r) ? mine : recv;
         }
         value_block(vt2, vm2, pr, alpha, 32);
       }
@@ -804,15 +855,15 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
         for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
         // every lane scores a token of row 0: use row 0's reference max (lanes t >= 2 carry
         // the unused row 1 of the fast blocks)
-        const float m_ref = __shfl_sync(0xffffffffu, m_run, 0);
+        const float m_ref = __shfl_sync(0xffffffffu, m_run[0], 0);
         const float m_new = tmax > m_ref + (float)kLazy ? tmax : m_ref;
-        const float alpha = fast_exp2(m_ref - m_new);
+        const float alpha[NT] = {fast_exp2(m_ref - m_new)};
         const float pj = valid ? fast_exp2(sl - m_new) : 0.f;
         // l of row 0 in the lanes t = 0, 1 convention: the quad (g, 0..3) holds tokens g, g+8, 16+g, 24+g
         float quad = pj + __shfl_xor_sync(0xffffffffu, pj, 1);
         quad += __shfl_xor_sync(0xffffffffu, quad, 2);
-        l_run = l_run * alpha + quad;
-        m_run = m_new;
+        l_run[0] = l_run[0] * alpha[0] + quad;
+        m_run[0] = m_new;
         const int gi = (int)(j0 / gs), bi = (int)((j0 - (int64_t)gi * gs) / 32);
         const uint8_t* rec = reinterpret_cast<const uint8_t*>(p.k.tiles) + ((size_t)bh * p.Grec + gi) * SB;
         const uint32_t* vt2 = reinterpret_cast<const uint32_t*>(rec + KTB) + (size_t)(2 * bi) * tile_words(D, VB);
@@ -823,7 +874,12 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
     }
 
     // ---- end of the fast region: fold accumulators, gather the softmax state ------------
-    if (dirty) flush(1.0f);
+    if (dirty) {
+      float one[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) one[nt] = 1.0f;
+      flush(one);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {  // channel group cq's total over its 8 token-quad lanes
       bias[r] += __shfl_xor_sync(0xffffffffu, bias[r], 1);
@@ -831,15 +887,16 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
       bias[r] += __shfl_xor_sync(0xffffffffu, bias[r], 4);
     }
     float m_all[R], l_all[R];
-    {
-      float lr = l_run;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float lr = l_run[nt];
       lr += __shfl_xor_sync(0xffffffffu, lr, 4);
       lr += __shfl_xor_sync(0xffffffffu, lr, 8);
       lr += __shfl_xor_sync(0xffffffffu, lr, 16);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        m_all[r] = __shfl_sync(0xffffffffu, m_run, 2 * r);  // lane (g 0, t 2r)
-        l_all[r] = __shfl_sync(0xffffffffu, lr, 2 * r);
+      for (int r = 2 * nt; r < 2 * nt + 2 && r < R; ++r) {
+        m_all[r] = __shfl_sync(0xffffffffu, m_run[nt], 2 * (r - 2 * nt));  // lane (g 0, t 2r')
+        l_all[r] = __shfl_sync(0xffffffffu, lr, 2 * (r - 2 * nt));
       }
     }
     __syncwarp();
@@ -1276,10 +1333,13 @@ bool mma_setup(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int 
   if (gs % 32 != 0) return false;  // groups are processed in 32-token blocks
   if (D != 64 && D != 128) return false;
   if (kb == 3 && D != 128) return false;
-  // query rows per pass: 2 (the B operand holds two rows' four digits); more rows (GQA G > 2, several query tokens) run
-  // as row passes inside one launch, up to kMaxPasses per launch (their warps stream the
-  // same records together, so the cache is read from DRAM about once per launch)
-  const int per_pass = rows == 1 ? 1 : 2;
+  // query rows per pass: 2 (one n8 B tile holds two rows' four digits), 4 on the single-warp
+  // kernel when there are more (two n8 tiles share every unpacked A fragment: GQA G = 4 reads
+  // and unpacks each record once); more rows (G = 8, several query tokens) run as row passes
+  // inside one launch, up to kMaxPasses per launch (their warps stream the same records
+  // together, so the cache is read from DRAM about once per launch)
+  const bool ws_path = knobs().ws == 2 || (knobs().ws == 1 && vb == 3);
+  const int per_pass = rows == 1 ? 1 : (rows == 2 || ws_path || knobs().tc || !knobs().r4) ? 2 : 4;
   const int npass_all = (rows + per_pass - 1) / per_pass;
   const int chunk = std::min(npass_all, kMaxPasses);
   const int BH = c->B * c->H;
@@ -1405,7 +1465,8 @@ bool attend_mma(const kvmix_cache* c, const void* q, kvmix_dtype dt, int Hq, int
 #define KVB_DISPATCH_D(DD)                                                  \
       if (D == DD) {                                                        \
         if (nrows == 1) W = dispatch_bits<DD, 1>(p, kb, vb, BH, ws, st);   \
-        else W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st);              \
+        else if (nrows == 2) W = dispatch_bits<DD, 2>(p, kb, vb, BH, ws, st); \
+        else W = dispatch_bits<DD, 4>(p, kb, vb, BH, ws, st);              \
       }
       KVB_DISPATCH_D(64)
       KVB_DISPATCH_D(128)
@@ -1451,10 +1512,12 @@ void attend_layers(kvmix_cache* const* caches, int n, const void* const* k, cons
     const bool pdl = launched > 0 && knobs().pdl;  // after the call's first launch
     const int n = (int)g.p.size();
     bool ok = false;
-    if (g.D == 64) ok = g.R == 1 ? dispatch_layers<64, 1>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
-                                 : dispatch_layers<64, 2>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl);
-    else ok = g.R == 1 ? dispatch_layers<128, 1>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
-                       : dispatch_layers<128, 2>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl);
+    if (g.D == 64) ok = g.R == 1   ? dispatch_layers<64, 1>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
+                        : g.R == 2 ? dispatch_layers<64, 2>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
+                                   : dispatch_layers<64, 4>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl);
+    else ok = g.R == 1   ? dispatch_layers<128, 1>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
+              : g.R == 2 ? dispatch_layers<128, 2>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl)
+                         : dispatch_layers<128, 4>(g.p.data(), g.bh.data(), n, g.kb, g.vb, ws, st, pdl);
     if (!ok) throw Error(KVMIX_RUNTIME_ERROR, "attend: multi-layer launch unavailable");
     after_launch("attend_mma_layers_kernel");
     ++launched;
@@ -1470,7 +1533,7 @@ void attend_layers(kvmix_cache* const* caches, int n, const void* const* k, cons
     if (g.npass_all > g.chunk) return false;                       // several launches per layer
     if (kn.ws == 2 || (kn.ws == 1 && g.vb == 3)) return false;    // warp-specialized kernel
     mma_pass(p, c, g, 0, da);
-    const int R = g.per_pass == 1 ? 1 : 2;
+    const int R = g.per_pass;
     Group* gr = nullptr;
     for (Group& x : groups)
       if (x.D == g.D && x.kb == g.kb && x.vb == g.vb && x.R == R) gr = &x;

@@ -25,7 +25,12 @@ constexpr int kMmaWarps = KVB_WARPS;  // independent warps per CTA (no CTA barri
 #endif
 // resident warps per SM the register budget is sized for: 3-bit Keys with two query rows
 // (GQA) get 12 (their B staging leaves shared memory for 12 warps with a two-stage ring anyway)
-#define KVB_MIN_WARPS(KB, R) ((KB) == 3 && (R) == 2 ? 12 : KVB_MIN_WARPS_N)
+// four query rows (GQA G = 4: two IMMA column tiles, twice the accumulators) get KVB_MIN_WARPS_R4
+#ifndef KVB_MIN_WARPS_R4
+#define KVB_MIN_WARPS_R4 12
+#endif
+#define KVB_MIN_WARPS(KB, R) \
+  ((R) == 4 ? ((KB) == 3 ? 8 : KVB_MIN_WARPS_R4) : (KB) == 3 && (R) == 2 ? 12 : KVB_MIN_WARPS_N)
 #define KVB_MIN_CTAS(KB, R) (KVB_MIN_WARPS(KB, R) / KVB_WARPS)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -188,6 +193,7 @@ struct Knobs {
   int ws = 1;  // warp-specialized kernel (attention_ws.cu): 0 never, 1 for 3-bit Values, 2 always
   int tc = 0;  // tcgen05 kernel (attention_tc.cu) for the fast groups where it applies
   int pdl = 1;  // programmatic dependent launch between the layers of kvmix_*attend_layers
+  int r4 = 1;      // four query rows per pass (two IMMA column tiles) on the single-warp kernel
   int layers = 1;  // kvmix_*attend_layers: one launch per kernel instance (else per layer)
   bool skip_tail = false, no_window = false;
 };
@@ -441,7 +447,7 @@ __device__ __forceinline__ void merge_bh(const MmaParams& p, int bh, int lane, i
 }
 
 // Per-warp dynamic shared layout (bytes):
-//   ring[S][stage_bytes] | kstage | vbs[CGMAX][8][32] u8 | bars[S] u64
+//   ring[S][stage_bytes] | kstage | vbs[CGMAX][8 or 16 cols][32] u8 | bars[S] u64
 // kstage: kbs[planes][4R cols][4 t][NK][2] u32 (digit words of the Key B fragments; 3-bit
 //         Keys have a second plane), zeros[4 t][NK][2] (B columns without a query row),
 //         then for 3-bit Keys ytab[R][D] f32 (narrow-slot factors per query row)
@@ -453,7 +459,7 @@ struct WarpLayout {
   static constexpr int kZ = (KB == 3 ? 2 : 1) * kKB;  // zero words read by the lanes g >= kKC
   static constexpr int kY = kZ + 4 * (D / 32) * 2 * 4;
   static constexpr int kK = KB == 3 ? kY + (R + 1) * D * 4 : kY;
-  static constexpr int kV = (D / 32) * 8 * 32;
+  static constexpr int kV = (D / 32) * 8 * (R > 2 ? 2 : 1) * 32;  // [cg][4R cols][32 tokens] u8
   static constexpr int kQ = D * 4 + 32 * 8;  // q of all channels (window blocks), checksum slots
   __host__ __device__ static constexpr size_t bytes(int stages, uint32_t stage_bytes) {
     const size_t n = (size_t)stages * stage_bytes + kK + kV + kQ + (size_t)stages * 8;
