@@ -480,11 +480,14 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
       if (cg_ok) {
         const float pe = pow2i(e_cur);
         const int pos = (tq & 3) * 8 + (tq >> 2) * 4;
+        float se[4];  // s 2^E (exact: power-of-two factor), so (p s) 2^E == p (s 2^E)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) se[i] = pe * sv[i];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           uint32_t uu[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) uu[i] = (uint32_t)__float2int_rn(pq[r][i] * pe * sv[i]);
+          for (int i = 0; i < 4; ++i) uu[i] = (uint32_t)__float2int_rn(pq[r][i] * se[i]);
           store_digits(reinterpret_cast<uint32_t*>(vbs + cq * (256 * NT) + (4 * r) * 32 + pos), 8, uu);
         }
       }
@@ -564,6 +567,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
           omod = inf.y % 11;
         }
         float beta[R], isig[R];
+        float bsel[NT];  // R > 1: sum_d q_d m_d of row 2 nt + my_r
         __syncwarp();  // previous group's reads of kbs / ytab are done
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -602,9 +606,34 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
               *reinterpret_cast<float4*>(ytab + r * D + 4 * lane) = y;
             }
           }
+          if constexpr (R == 1) {
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
-          beta[r] = bt;
+            for (int o = 16; o > 0; o >>= 1) bt += __shfl_xor_sync(0xffffffffu, bt, o);
+          }
+          beta[r] = bt;  // R > 1: this lane's term, reduced below
+        }
+        if constexpr (R > 1) {
+          // transposed butterfly: the xor-16 (and, R = 4, xor-8) steps halve the rows a lane
+          // carries, so lane L ends with the total of row 2 b4 + b3 (R = 4) / b4 (R = 2)
+          const bool hi16 = lane & 16;
+          float x;
+          if constexpr (R == 4) {
+            const float s0 = hi16 ? beta[0] : beta[2], s1 = hi16 ? beta[1] : beta[3];
+            const float k0 = hi16 ? beta[2] : beta[0], k1 = hi16 ? beta[3] : beta[1];
+            const float y0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+            const float y1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+            const bool hi8 = lane & 8;
+            x = (hi8 ? y1 : y0) + __shfl_xor_sync(0xffffffffu, hi8 ? y0 : y1, 8);
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) bsel[nt] = __shfl_sync(0xffffffffu, x, 16 * nt + 8 * my_r);
+          } else {
+            x = (hi16 ? beta[1] : beta[0]) + __shfl_xor_sync(0xffffffffu, hi16 ? beta[0] : beta[1], 16);
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            bsel[0] = __shfl_sync(0xffffffffu, x, 16 * my_r);  // (my_r = 1 without a second row: unused)
+          }
         }
         __syncwarp();
         // B fragments: b0 = k rows 4t..4t+3, b1 = 16+4t.., column 8 nt + g (digit g%4 of row
@@ -638,13 +667,10 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int rr = 2 * nt + my_r < R ? 2 * nt + my_r : 0;
-          float is = isig[0], bb = beta[0];
+          float is = isig[0], bb = R > 1 ? bsel[nt] : beta[0];
 #pragma unroll
           for (int r = 1; r < R; ++r)
-            if (rr == r) {
-              is = isig[r];
-              bb = beta[r];
-            }
+            if (rr == r) is = isig[r];
           wsc0[nt] = pow2i(16 * (t & 1)) * is * p.inv * kLog2e;
           betaL[nt] = bb * p.inv * kLog2e;
         }

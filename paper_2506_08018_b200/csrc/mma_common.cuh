@@ -29,8 +29,11 @@ constexpr int kMmaWarps = KVB_WARPS;  // independent warps per CTA (no CTA barri
 #ifndef KVB_MIN_WARPS_R4
 #define KVB_MIN_WARPS_R4 12
 #endif
+#ifndef KVB_MIN_WARPS_R4K3
+#define KVB_MIN_WARPS_R4K3 8  // 3-bit Keys (a second B plane): 12 warps spill
+#endif
 #define KVB_MIN_WARPS(KB, R) \
-  ((R) == 4 ? ((KB) == 3 ? 8 : KVB_MIN_WARPS_R4) : (KB) == 3 && (R) == 2 ? 12 : KVB_MIN_WARPS_N)
+  ((R) == 4 ? ((KB) == 3 ? KVB_MIN_WARPS_R4K3 : KVB_MIN_WARPS_R4) : (KB) == 3 && (R) == 2 ? 12 : KVB_MIN_WARPS_N)
 #define KVB_MIN_CTAS(KB, R) (KVB_MIN_WARPS(KB, R) / KVB_WARPS)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;

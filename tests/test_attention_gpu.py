@@ -137,6 +137,27 @@ def test_attend_multi_pass_rows(cuda, kb, vb, G, tq):
     check_attend(dev, ora, q, G=G, expect_mma=True)
 
 
+@pytest.mark.parametrize("kb,vb,G,tq,D", [(2, 2, 4, 1, 128), (3, 4, 4, 1, 128), (4, 2, 2, 2, 128), (2, 4, 4, 1, 64),
+                                          (3, 2, 3, 1, 128), (4, 4, 8, 1, 64)])
+def test_four_row_passes_match_two_row_passes(cuda, kb, vb, G, tq, D):
+    """Four query rows per pass (two IMMA column tiles over one unpacked A fragment, the
+    default for > 2 rows) against the two-row passes (KVMIX_R4 = 0) on the same cache: both
+    within the fp64 tolerance, and within 4e-7 max|V| of each other (only the fp32 merge and
+    min-term summation orders differ)."""
+    dev, ora = build(kb, vb, 0.2, 0.2, 32, 2, 2, D, [700] + [1] * 9, seed=61)
+    q = O.random_h16(62, (2, 2 * G, tq, D), sigma=1.5)
+    outs = []
+    try:
+        for r4 in (1, 0):
+            K.set_knob("KVMIX_R4", r4)
+            check_attend(dev, ora, q, G=G, expect_mma=True)
+            outs.append(K.attend(torch.from_numpy(q).cuda(), dev).output.cpu().numpy())
+    finally:
+        K.set_knob("KVMIX_R4", 1)
+    vmax = float(np.abs(ora.snapshot()[1]).max())
+    assert float(np.abs(outs[0] - outs[1]).max()) / vmax <= 4e-7
+
+
 @pytest.mark.parametrize("gs", [64, 128])
 def test_attend_group_sizes(cuda, gs):
     dev, ora = build(2, 4, 0.1, 0.1, gs, 1, 4, 128, [1200, 1, 1, 300] + [1] * 20, seed=31)
