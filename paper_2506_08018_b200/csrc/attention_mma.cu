@@ -339,7 +339,7 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
     for (int d = lane; d < D; d += 32) {
       int w, sh;
       imma_field(true, D, 2, 0, d, &w, &sh);
-      ntab[d] = (uint32_t)w | ((uint32_t)sh << 16);
+      ntab[d] = ((uint32_t)w << 5) | (uint32_t)sh;  // the funnel shift below reads sh = low 5 bits
     }
     __syncwarp();
   }
@@ -732,8 +732,8 @@ __device__ __forceinline__ void attend_mma_body(const MmaParams& p, const int gw
               for (int k = 0; k < (D + 10) / 11; ++k) {
                 const int d = d0 + 11 * k;
                 if (d < D) {
-                  const uint32_t tb = ntab[d];  // {word offset at row 0 | shift << 16}
-                  const uint32_t code = (tile[(tb & 0xffffu) + rowoff] >> (tb >> 16)) & 3u;
+                  const uint32_t tb = ntab[d];  // {word offset at row 0 << 5 | shift}
+                  const uint32_t code = __funnelshift_r(tile[(tb >> 5) + rowoff], 0u, tb) & 3u;
 #pragma unroll
                   for (int r = 0; r < R; ++r) dlt[r] = fmaf((float)code, ytab[r * D + d], dlt[r]);
                 }
