@@ -212,7 +212,8 @@ uint64_t kvmix_scratch_allocated(void);
 /* Tuning / test hook: overrides one kernel knob for later launches ("KVMIX_TAIL_UNIT",
  * "KVMIX_GROUP_COST", "KVMIX_TEST_FLUSH_BLOCKS" (<= 0 restores the default), "KVMIX_MIN_COST",
  * "KVMIX_WS": 0 = single-warp tensor-core kernel only, 1 = warp-specialized kernel for 3-bit
- * Values (default), 2 = warp-specialized kernel for every tier).
+ * Values (default), 2 = warp-specialized kernel for every tier; "KVMIX_R4": 1 = four query rows
+ * per pass on the single-warp kernel when a KV head has more than two (default), 0 = two).
  * The same names are read once from the environment at the first launch. */
 kvmix_status kvmix_set_knob(const char* name, int value);
 
