@@ -653,29 +653,49 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
   extern __shared__ __align__(16) float m3s[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int CE = 11 * gs;  // chunk elements
-  float* xs = m3s + (size_t)warp * (CE + 4 * 11);
-  float* gm = xs + CE;  // [11] scale, [11] min, [11] rcp(scale), [11] rcp(wide scale)
+  float* xs = m3s + (size_t)warp * (CE + 68);  // (16-byte aligned per warp)
+  float* gm = xs + CE;  // [11] scale, [11] min, [11] rcp(scale), [11] rcp(wide scale), [11][2] fold
+  float* gf = gm + 44;  // per-group (fminf, fmaxf) folded from the registers of the staging loads
   const size_t chunk = (size_t)blockIdx.x * kM3Warps + warp;
   const size_t e0 = chunk * CE;
   if (e0 >= n) return;
   const int ne = (int)min((size_t)CE, n - e0);  // a multiple of gs (n % gs == 0)
   // stage (fp32 in shared memory)
-  if (ne == CE && (reinterpret_cast<uintptr_t>(x + e0) & 15) == 0) {
+  const bool full = ne == CE && (reinterpret_cast<uintptr_t>(x + e0) & 15) == 0;
+  if (full) {
     // every 16-byte load of the chunk in flight before the first store (one DRAM latency)
     constexpr int NV = CE / Vec<T>::N, PER = (NV + 31) / 32;
     uint4 r[PER];
     const uint4* s4 = reinterpret_cast<const uint4*>(x + e0);
 #pragma unroll
     for (int u = 0; u < PER; ++u)
-      if (lane + 32 * u < NV) r[u] = __ldg(s4 + lane + 32 * u);
+      r[u] = lane + 32 * u < NV ? __ldg(s4 + lane + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+    // group min / max straight from the loaded vectors: a group is L = gs / N consecutive
+    // vectors, i.e. L adjacent lanes of one load round (32 is a multiple of L)
+    constexpr int L = gs / Vec<T>::N;
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = lane + 32 * u;
+      float v[Vec<T>::N];
+      Vec<T>::unpack(r[u], v);
       if (i < NV) {
-        float v[Vec<T>::N];
-        Vec<T>::unpack(r[u], v);
 #pragma unroll
         for (int k = 0; k < Vec<T>::N; ++k) xs[i * Vec<T>::N + k] = v[k];
+      }
+      float mn = v[0], mx = v[0];
+#pragma unroll
+      for (int k = 1; k < Vec<T>::N; ++k) {
+        mn = fminf(mn, v[k]);
+        mx = fmaxf(mx, v[k]);
+      }
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (i < NV && (lane & (L - 1)) == 0) {
+        gf[2 * (i / L)] = mn;
+        gf[2 * (i / L) + 1] = mx;
       }
     }
   } else {
@@ -686,13 +706,20 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
   if (lane < ng) {
     // fminf / fmaxf skip NaN like the ordered fold and differ from it only in the sign of a
     // zero extremum and for a NaN first element: those groups redo the fold (rare)
-    const float4* g4 = reinterpret_cast<const float4*>(xs + lane * gs);
-    float mn = xs[lane * gs], mx = mn;
+    float mn, mx;
+    if (full) {
+      mn = gf[2 * lane];
+      mx = gf[2 * lane + 1];
+    } else {
+      const float4* g4 = reinterpret_cast<const float4*>(xs + lane * gs);
+      mn = xs[lane * gs];
+      mx = mn;
 #pragma unroll 4
-    for (int j = 0; j < gs / 4; ++j) {
-      const float4 q = g4[j];
-      mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
-      mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+      for (int j = 0; j < gs / 4; ++j) {
+        const float4 q = g4[j];
+        mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+      }
     }
     if (mn == 0.f || mx == 0.f || isnan(xs[lane * gs])) {
       const float* g = xs + lane * gs;
@@ -904,7 +931,7 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     // Mixed3 chunks of 11 * gs elements, one warp each
     const size_t chunks = (n + 11 * (size_t)gs - 1) / (11 * (size_t)gs);
     const unsigned grid = (unsigned)((chunks + kM3Warps - 1) / kM3Warps);
-    const size_t smem = (size_t)kM3Warps * (11 * gs + 44) * 4;
+    const size_t smem = (size_t)kM3Warps * (11 * gs + 68) * 4;
     auto go = [&](auto kern, const auto* xp) {
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
       // the whole unified L1 as shared memory: as many staged tiles per SM as fit (the tile
