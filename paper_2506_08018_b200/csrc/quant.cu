@@ -644,6 +644,11 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
 // min/max, exactly), and every lane emits gs/32 words; a lane's 11 codes sit at stride 11
 // in shared memory (odd: conflict-free). Slot 10 of every word is the narrow slot.
 constexpr int kM3Warps = 8;
+// gs 32: a warp takes two 11-group chunks (22 lanes make the metas at once, 64 words per warp)
+__host__ __device__ constexpr int m3_groups_per_chunk(int gs) { return gs == 32 ? 22 : 11; }
+__host__ __device__ constexpr int m3_warp_floats(int gs) {  // chunk + 6 per group, 16-byte aligned
+  return (m3_groups_per_chunk(gs) * (gs + 6) + 3) / 4 * 4;
+}
 
 template <typename T, int GS>
 __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const T* __restrict__ x, size_t n,
@@ -652,10 +657,12 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
   constexpr int gs = GS;
   extern __shared__ __align__(16) float m3s[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int CE = 11 * gs;  // chunk elements
-  float* xs = m3s + (size_t)warp * (CE + 68);  // (16-byte aligned per warp)
-  float* gm = xs + CE;  // [11] scale, [11] min, [11] rcp(scale), [11] rcp(wide scale), [11][2] fold
-  float* gf = gm + 44;  // per-group (fminf, fmaxf) folded from the registers of the staging loads
+  constexpr int NG = m3_groups_per_chunk(gs);  // groups per chunk (gs 32: two 11-group chunks)
+  constexpr int CE = NG * gs;                    // chunk elements
+  constexpr int WPC = CE / 11;                   // words per chunk
+  float* xs = m3s + (size_t)warp * m3_warp_floats(gs);
+  float* gm = xs + CE;  // [NG] scale, [NG] min, [NG] rcp(scale), [NG] rcp(wide scale)
+  float* gf = gm + 4 * NG;  // [NG][2] (fminf, fmaxf) folded from the registers of the staging loads
   const size_t chunk = (size_t)blockIdx.x * kM3Warps + warp;
   const size_t e0 = chunk * CE;
   if (e0 >= n) return;
@@ -731,19 +738,19 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
       }
     }
     const uint32_t m = make_meta(mn, mx, 7);
-    meta[chunk * 11 + lane] = m;
+    meta[chunk * NG + lane] = m;
     const float sc = meta_scale(m);
     gm[lane] = sc;
-    gm[11 + lane] = meta_min(m);
-    gm[22 + lane] = rcp_approx(sc);
-    gm[33 + lane] = rcp_approx(wide_scale(sc));
+    gm[NG + lane] = meta_min(m);
+    gm[2 * NG + lane] = rcp_approx(sc);
+    gm[3 * NG + lane] = rcp_approx(wide_scale(sc));
   }
   __syncwarp();
   const size_t nw = (n + 10) / 11;
 #pragma unroll
-  for (int i = 0; i < gs / 32; ++i) {
+  for (int i = 0; i < WPC / 32; ++i) {
     const int wl = lane + 32 * i;
-    const size_t w = chunk * gs + wl;
+    const size_t w = chunk * WPC + wl;
     if (w >= nw) break;
     uint32_t word = 0;
     if (11 * wl + 11 <= ne) {  // every chunk but the stream's last
@@ -753,16 +760,16 @@ __global__ void __launch_bounds__(kM3Warps * 32) quantize_value_m3_kernel(const 
       float xv[11];
 #pragma unroll
       for (int k = 0; k < 11; ++k) xv[k] = xs[11 * wl + k];
-      word = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, gm[j0], gm[11 + j0], gm[j1], gm[11 + j1]);
+      word = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, gm[j0], gm[NG + j0], gm[j1], gm[NG + j1]);
     } else {
 #pragma unroll
       for (int k = 0; k < 11; ++k) {
         const int e = 11 * wl + k;
         if (e < ne) {
           const int j = e / gs;
-          const float sc = gm[j], mnv = gm[11 + j];
+          const float sc = gm[j], mnv = gm[NG + j];
           const bool nar = k == 10;
-          const uint32_t code = encode_fast(xs[e], sc, mnv, nar ? wide_scale(sc) : sc, gm[(nar ? 33 : 22) + j],
+          const uint32_t code = encode_fast(xs[e], sc, mnv, nar ? wide_scale(sc) : sc, gm[(nar ? 3 : 2) * NG + j],
                                             nar ? 3 : 7, 3, nar);
           word |= code << (nar ? 30u : 3u * k);
         }
@@ -929,9 +936,10 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     after_launch("quantize_value_words_kernel");
   } else if (bits == 3 && D % gs == 0 && (gs == 32 || gs == 64 || gs == 128)) {
     // Mixed3 chunks of 11 * gs elements, one warp each
-    const size_t chunks = (n + 11 * (size_t)gs - 1) / (11 * (size_t)gs);
+    const size_t ce = (size_t)m3_groups_per_chunk(gs) * gs;
+    const size_t chunks = (n + ce - 1) / ce;
     const unsigned grid = (unsigned)((chunks + kM3Warps - 1) / kM3Warps);
-    const size_t smem = (size_t)kM3Warps * (11 * gs + 68) * 4;
+    const size_t smem = (size_t)kM3Warps * m3_warp_floats(gs) * 4;
     auto go = [&](auto kern, const auto* xp) {
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
       // the whole unified L1 as shared memory: as many staged tiles per SM as fit (the tile
