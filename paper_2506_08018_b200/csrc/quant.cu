@@ -355,28 +355,23 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
   // channels of one token row: conflict-free), word j = i / D of that channel's run. A
   // run's owned words are those whose FIRST code lies in it; trailing codes of the last
   // one that belong to the next run are encoded straight from global memory.
-  const int nwr_max = (nt + cpw - 1) / cpw + 1;  // owned words per run are at most this
-  for (int i = threadIdx.x; i < D * nwr_max; i += blockDim.x) {
-    const int d = i % D, j = i / D;
-    const size_t c = (size_t)bh * D + d;
-    const size_t s0 = c * (size_t)T_ + t0;
+  // (gs a power of two: group index by shift)
+  const int gsh = (gs & (gs - 1)) == 0 ? __ffs(gs) - 1 : -1;
+  auto emit = [&](const int d, const size_t s0, const size_t w) {
     const size_t s1 = s0 + nt;
-    const size_t w_begin = (s0 + cpw - 1) / cpw, w_end = (s1 + cpw - 1) / cpw;
-    const size_t w = w_begin + j;
-    if (w >= w_end) continue;
     const size_t p0 = w * cpw;
     uint32_t word = 0;
     if constexpr (BITS == 3) {
       if (gs >= 11 && p0 + 11 <= s1) {  // interior Mixed3 word: <= two groups, slot 10 narrow
         const int tt0 = (int)(p0 - s0);
-        const int j0 = tt0 / gs, kb = (j0 + 1) * gs - tt0;  // first code of group j0 + 1
+        const int j0 = gsh >= 0 ? tt0 >> gsh : tt0 / gs, kb = (j0 + 1) * gs - tt0;  // first code of group j0 + 1
         const uint32_t ma = ms[j0 * D + d], mb = kb < 11 ? ms[(j0 + 1) * D + d] : ma;
         float xv[11];
 #pragma unroll
         for (int k = 0; k < 11; ++k) xv[k] = ld_f(&xs[(tt0 + k) * D + d]);
         words[w] = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, meta_scale(ma), meta_min(ma),
                                                                    meta_scale(mb), meta_min(mb));
-        continue;
+        return;
       }
     }
     int tt = (int)(p0 - s0);                                    // token of the first code
@@ -444,6 +439,21 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
       word |= encode(xv, sc2, mn2, bits, is_narrow(bits, p)) << field_shift(bits, (uint32_t)k);
     }
     words[w] = word;
+  };
+  if (blockDim.x % D == 0) {  // a thread keeps its channel: run bounds once per thread
+    const int d = threadIdx.x % D;
+    const size_t s0 = ((size_t)bh * D + d) * (size_t)T_ + t0, s1 = s0 + nt;
+    const size_t w_begin = (s0 + cpw - 1) / cpw, w_end = (s1 + cpw - 1) / cpw;
+    for (size_t w = w_begin + threadIdx.x / D; w < w_end; w += blockDim.x / D) emit(d, s0, w);
+    return;
+  }
+  const int nwr_max = (nt + cpw - 1) / cpw + 1;  // owned words per run are at most this
+  for (int i = threadIdx.x; i < D * nwr_max; i += blockDim.x) {
+    const int d = i % D, j = i / D;
+    const size_t s0 = ((size_t)bh * D + d) * (size_t)T_ + t0, s1 = s0 + nt;
+    const size_t w_begin = (s0 + cpw - 1) / cpw, w_end = (s1 + cpw - 1) / cpw;
+    const size_t w = w_begin + j;
+    if (w < w_end) emit(d, s0, w);
   }
 }
 
