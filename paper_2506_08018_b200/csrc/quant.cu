@@ -373,6 +373,21 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
                                                                    meta_scale(mb), meta_min(mb));
         return;
       }
+      // run-end word: codes of this run's last group, then (from slot kb = nt - tt0, 1..10)
+      // of the next run's first group, staged at rows nt .. (channel d of the next span, or
+      // channel d + 1 at the end of the (b, kv-head)); p0 % 11 == 0, so slot 10 is the narrow
+      // one as in an interior word
+      const int dn = next_span ? d : d + 1;
+      if (ext && dn < D && p0 + 11 <= n_total) {
+        const int tt0 = (int)(p0 - s0), kb = nt - tt0;
+        const uint32_t ma = ms[(gpt - 1) * D + d], mb = ms[gpt * D + dn];
+        float xv[11];
+#pragma unroll
+        for (int k = 0; k < 11; ++k) xv[k] = k < kb ? ld_f(&xs[(tt0 + k) * D + d]) : ld_f(&xs[(nt + k - kb) * D + dn]);
+        words[w] = encode_m3_word<!std::is_same<T, __half>::value>(xv, kb, meta_scale(ma), meta_min(ma),
+                                                                   meta_scale(mb), meta_min(mb));
+        return;
+      }
     }
     int tt = (int)(p0 - s0);                                    // token of the first code
     int r11 = bits == 3 ? (int)(p0 % 11u) : 0;                  // stream index mod 11
