@@ -600,27 +600,19 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_kernel(const T* __re
 // earlier of equal values, and a NaN first element makes the result NaN.
 // (fold_min / fold_max: common.cuh)
 
+__host__ __device__ constexpr int value_words_per_thread(int bits) { return bits == 4 ? 2 : 1; }
+
 template <typename T, int N>
 __device__ __forceinline__ void load_n(const T* p, float (&o)[N]) {
 #pragma unroll
   for (int i = 0; i < N; i += Vec<T>::N) Vec<T>::load(p + i, o + i);
 }
 
+// words of one slot: v = the word's inputs (zeros for idle lanes), w = its index
 template <typename T, int BITS>
-__global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T* __restrict__ x, size_t nw, int L,
-                                                                         uint32_t* __restrict__ words,
-                                                                         uint32_t* __restrict__ meta) {
+__device__ __forceinline__ void value_word(const float (&v)[32 / BITS], bool ok, size_t w, int lane, int L,
+                                           uint32_t* __restrict__ words, uint32_t* __restrict__ meta) {
   constexpr int CPW = 32 / BITS;
-  static_assert(CPW % Vec<T>::N == 0, "word = whole input vectors");
-  const size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool ok = w < nw;  // groups are whole L-lane blocks: idle lanes form whole blocks
-  float v[CPW];
-  if (ok) load_n<T, CPW>(x + w * CPW, v);
-  else {
-#pragma unroll
-    for (int i = 0; i < CPW; ++i) v[i] = 0.f;
-  }
   // fminf/fmaxf skip NaN like the fold; they differ from it only in the sign of a zero
   // extremum (the fold keeps the first of -0 / +0), so groups whose min or max is zero redo
   // the ordered fold
@@ -655,11 +647,39 @@ __global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T
   if (__shfl_sync(0xffffffffu, isnan(v[0]) ? 1 : 0, lead)) mn = mx = NAN;  // NaN first element
   constexpr int q_max = BITS == 1 ? 1 : BITS == 2 ? 3 : 15;
   const uint32_t m = make_meta(mn, mx, q_max);
-  if (!ok) return;
+  if (!ok) return;  // (after the warp-wide shuffles)
   if (lane == lead) meta[w / L] = m;
   const float sc = meta_scale(m), mnv = meta_min(m), rc = rcp_approx(sc);
   const uint32_t word = encode_word<BITS, CPW, !std::is_same<T, __half>::value>(v, sc, mnv, q_max);
   words[w] = word;
+}
+
+
+// P words per thread (4-bit: two, so a thread keeps 32 bytes of loads in flight like the
+// 2-bit words): slot p of the grid covers words [p S, (p + 1) S), S = threads in the grid (a
+// multiple of 32, so every group stays inside one warp); all loads issue before the folds
+template <typename T, int BITS>
+__global__ void __launch_bounds__(kQThreads) quantize_value_words_kernel(const T* __restrict__ x, size_t nw, int L,
+                                                                         uint32_t* __restrict__ words,
+                                                                         uint32_t* __restrict__ meta) {
+  constexpr int CPW = 32 / BITS;
+  constexpr int P = value_words_per_thread(BITS);
+  static_assert(CPW % Vec<T>::N == 0, "word = whole input vectors");
+  const size_t S = (size_t)gridDim.x * blockDim.x;
+  const size_t w0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  float v[P][CPW];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const size_t w = w0 + p * S;
+    if (w < nw) load_n<T, CPW>(x + w * CPW, v[p]);  // groups are whole L-lane blocks: idle
+    else {                                             // lanes form whole blocks
+#pragma unroll
+      for (int i = 0; i < CPW; ++i) v[p][i] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) value_word<T, BITS>(v[p], w0 + p * S < nw, w0 + p * S, lane, L, words, meta);
 }
 
 // ---- Values, Mixed3 (3-bit), D % gs == 0 and gs % 32 == 0 ------------------------------
@@ -945,7 +965,8 @@ void quantize(kvmix_grouping grouping, const void* x, kvmix_dtype dt, int B, int
     // whole-group words: one thread per word (the common KVmix shapes: gs 32/64/128)
     const int cpw = 32 / bits, L = gs / cpw;
     const size_t nw = n / cpw;
-    const unsigned grid = (unsigned)((nw + kQThreads - 1) / kQThreads);
+    const size_t per_block = (size_t)kQThreads * value_words_per_thread(bits);
+    const unsigned grid = (unsigned)((nw + per_block - 1) / per_block);
     const float* xf = static_cast<const float*>(x);
     const __half* xh = static_cast<const __half*>(x);
 #define KVB_QVW(TT, XP)                                                                             \
