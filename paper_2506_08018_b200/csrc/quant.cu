@@ -311,6 +311,8 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
     constexpr int CPW = 32 / BITS;
     if (gs % CPW == 0) {  // whole-group words (T % gs == 0): one meta per word, no run ends
       const int nwr = nt / CPW;
+      const int nwr_sh = (nwr & (nwr - 1)) == 0 ? __ffs(nwr) - 1 : -1;
+      const int gsh = (gs & (gs - 1)) == 0 ? __ffs(gs) - 1 : -1;  // (gs a power of two: shifts)
       if constexpr (PAIRS) {  // channels (2dp, 2dp+1): one 32-bit load per token, two words
         constexpr int DP = DT / 2;
         uint32_t* ow = ms + (size_t)gst * D;  // the tile's words [D][nwr + 1]
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
           __half2 hv[CPW];  // (kept packed: 16 registers for the two words' inputs)
 #pragma unroll
           for (int k = 0; k < CPW; ++k) hv[k] = xs2[(j * CPW + k) * DP + dp];
-          const int g = (j * CPW) / gs;
+          const int g = gsh >= 0 ? (j * CPW) >> gsh : (j * CPW) / gs;
           const uint2 m = *reinterpret_cast<const uint2*>(&ms[g * D + 2 * dp]);
           const size_t w = (((size_t)bh * D + 2 * dp) * (size_t)T_ + t0) / CPW + j;
           (void)w;
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
         // consecutive threads (whole sectors per store instead of one word per channel row)
         __syncthreads();
         for (int i = threadIdx.x; i < D * nwr; i += blockDim.x) {
-          const int d = i / nwr, j = i - d * nwr;
+          const int d = nwr_sh >= 0 ? i >> nwr_sh : i / nwr, j = i - d * nwr;
           words[(((size_t)bh * D + d) * (size_t)T_ + t0) / CPW + j] = ow[d * (nwr + 1) + j];
         }
         return;
