@@ -269,6 +269,9 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
   if constexpr (PAIRS) {
     constexpr int DP = DT / 2;
     const __half2* xs2 = reinterpret_cast<const __half2*>(xs);
+    // (uniform bits: the tile's meta offset once; Mixed3 keeps the per-store index, its 42-
+    // register budget has no room for another live 64-bit value)
+    const size_t mbase = BITS == 3 ? 0 : (size_t)bh * D * gpc + t0 / gs;
     for (int i = threadIdx.x; i < DP * gst; i += blockDim.x) {
       const int dp = i % DP, g = i / DP;
       const __half2* col = xs2 + (size_t)(g * gs) * DP + dp;
@@ -287,7 +290,8 @@ __global__ void __launch_bounds__(kQThreads, BITS == 2 ? 5 : 6) quantize_key_ker
         if (mn == 0.f || mx == 0.f || isnan(c ? f0.y : f0.x)) ordered(d, g, mn, mx);
         const uint32_t m = make_meta(mn, mx, q_max);
         ms[g * D + d] = m;
-        if (g < gpt) meta[((size_t)bh * D + d) * gpc + t0 / gs + g] = m;
+        if (g < gpt)
+          meta[BITS == 3 ? ((size_t)bh * D + d) * gpc + t0 / gs + g : mbase + (size_t)d * gpc + g] = m;
       }
     }
   } else
